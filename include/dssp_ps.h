@@ -1,0 +1,182 @@
+/*
+ * dssp_ps.h -- C-ABI of the B200 parameter-server engine (push / pull / DSSP gate).
+ *
+ * Plain pointers, sizes and POD structs only: no torch or CUDA types cross this
+ * boundary, so the reference's Python host side (or any FFI) can bind it. The
+ * binding the reference would add is shown in INTEGRATION.md; the Python shim in
+ * paper_1908_11848_b200/ uses ctypes.
+ *
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference/pkg/src/stalesync/):
+ *
+ *   ps_create           ParameterServer.__init__ + SyncPolicy.__init__   server.py:45-52, policy.py:138-150
+ *   ps_apply            ParameterServer.apply_gradient / apply_update     server.py:58-69, :29-42
+ *   ps_decide           ParameterServer.decide_push -> SyncPolicy.on_push server.py:71-78, policy.py:152-206
+ *   ps_push             ParameterServer.handle_push (apply, then decide)  server.py:80-82
+ *   ps_pull             ParameterServer.handle_pull (materialized copy)   server.py:84-91
+ *   ps_read_weights     ParameterServer.weights.values / .version         server.py:47, config.py:54-68
+ *   ps_get_state/peek   SyncPolicy.clocks / .history / .credits / .deferred  policy.py:43-105
+ *   ps_set_state        direct table writes the reference tests perform   tests/test_policy.py:156-166, :209-220
+ *   ps_controller_batch synchronization_controller (pure grid, oracle hook)  policy.py:108-132
+ *   ps_apply_vectors    apply_update on plain vectors (stateless)          server.py:29-42
+ *   ps_sim_run          Simulation.run event loop, device-resident          simnet.py:127-201
+ *   ps_sim_trace        Simulation.entries (TraceEntry rows)               simnet.py:110-112, trace.py:28-37
+ *
+ *   ps_shard_*          the same push/pull/gate over G GPUs (one process per
+ *                       GPU, contiguous-range shards, P2P over NVLink)
+ *
+ * Threading: like the reference ("callers serialize on_push calls",
+ * policy.py:136), calls on one handle must be serialized by the caller.
+ * Status codes: PS_OK (0), PS_REJECTED (1: non-finite gradient, counted, not an
+ * error -- server.py:65-67), negative values map 1:1 onto the reference's
+ * exceptions; ps_last_error() returns the message of the last failure.
+ */
+#ifndef DSSP_PS_H
+#define DSSP_PS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_MAX_WORKERS 64
+
+enum ps_paradigm { PS_BSP = 0, PS_ASP = 1, PS_SSP = 2, PS_DSSP = 3 };
+
+enum ps_status {
+  PS_OK = 0,
+  PS_REJECTED = 1,       /* non-finite gradient: rejected_updates += 1 (server.py:65-67) */
+  PS_E_PROTOCOL = -1,    /* ProtocolError (policy.py:29-30, :153-156; server.py:87-90) */
+  PS_E_VALUE = -2,       /* ValueError: dimension mismatch, lr <= 0, bad config (server.py:31-35, :61-64) */
+  PS_E_DIVERGED = -3,    /* DivergenceError (server.py:20-21, :38-41) */
+  PS_E_CUDA = -4,        /* CUDA runtime failure */
+  PS_E_DEADLOCK = -5,    /* DeadlockError (simnet.py:28-31, :150-153) */
+  PS_E_BUDGET = -6,      /* event budget exceeded (simnet.py:131-132) */
+  PS_E_TIMEOUT = -7      /* a device wait exceeded its watchdog (multi-GPU flags) */
+};
+
+enum ps_dtype { PS_F32 = 0, PS_F64 = 1 };
+
+typedef struct ps_config {
+  int32_t paradigm;      /* enum ps_paradigm */
+  int32_t worker_count;  /* P, 1..PS_MAX_WORKERS */
+  int32_t s_lower;       /* normalized as validate_config does (config.py:304-308) */
+  int32_t r_max;
+  double learning_rate;  /* > 0 */
+  int64_t dimension;     /* d >= 1 */
+  int32_t device;        /* CUDA ordinal of the (single-GPU) server */
+  int32_t reserved[7];
+} ps_config;
+
+/* Host mirror of the device control block (policy.py:43-105 tables). */
+typedef struct ps_gate_state {
+  int32_t paradigm, worker_count, s_lower, r_max, threshold, _pad;
+  int64_t clocks[PS_MAX_WORKERS];
+  double latest[PS_MAX_WORKERS];
+  double previous[PS_MAX_WORKERS];
+  int64_t populated[PS_MAX_WORKERS];
+  int64_t credits[PS_MAX_WORKERS];
+  uint64_t deferred;      /* bit q set: worker q is deferred */
+  int64_t version;        /* applied updates (WeightVector.version) */
+  int64_t rejected;       /* rejected_updates */
+  int64_t decisions;      /* on_push calls decided */
+} ps_gate_state;
+
+typedef struct ps_server ps_server;
+
+/* Lifecycle. w0 is the initial weight vector on the host (PS_F64 as the
+ * reference draws it, server.py:24-26, or PS_F32); it is rounded to fp32. */
+int ps_create(const ps_config* cfg, const void* w0_host, int32_t w0_dtype, ps_server** out);
+void ps_destroy(ps_server* h);
+const char* ps_last_error(const ps_server* h); /* h may be NULL (last create failure) */
+int ps_device_count(int32_t* n);
+
+/* Push path. g is d values in g_dtype, on the host or (g_on_device=1) in the
+ * server's device memory, borrowed for the call. *applied = 0 when rejected. */
+int ps_apply(ps_server* h, int32_t worker, const void* g, int32_t g_dtype, int32_t g_on_device,
+             int32_t* applied);
+int ps_decide(ps_server* h, int32_t worker, double now, int32_t* granted, uint64_t* released);
+int ps_push(ps_server* h, int32_t worker, const void* g, int32_t g_dtype, int32_t g_on_device,
+            double now, int32_t* applied, int32_t* granted, uint64_t* released);
+
+/* Pull path: materializes the current weights into dst (d values). */
+int ps_pull(ps_server* h, int32_t worker, void* dst, int32_t dst_dtype, int32_t dst_on_device,
+            int64_t* version);
+int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_device,
+                    int64_t* version);
+
+/* Gate state. ps_get_state synchronizes with the device; ps_peek_state returns
+ * the host mirror refreshed by the last synchronous call (no device traffic). */
+int ps_get_state(ps_server* h, ps_gate_state* out);
+int ps_peek_state(const ps_server* h, ps_gate_state* out);
+int ps_set_state(ps_server* h, const ps_gate_state* in);
+
+/* Oracle hooks. tables: n rows of (latest_p, prev_p, latest_s, prev_s). */
+int ps_controller_batch(int32_t device, const double* tables, const int32_t* r_max, int32_t n,
+                        int32_t* out);
+int ps_apply_vectors(int32_t device, const void* w, const void* g, int32_t dtype, int64_t n,
+                     double lr, void* out, int32_t* status);
+
+/* ------------------------------------------------------------------------
+ * Device-resident simulation (simnet.py:127-201): the whole event loop,
+ * gate decisions, pulls, gradient production and applies run in ONE
+ * persistent kernel; the host only launches it and reads the trace.
+ * ---------------------------------------------------------------------- */
+enum ps_grad_kind { PS_GRAD_BOWL = 0, PS_GRAD_SYNTHETIC = 1 };
+enum ps_event_kind {
+  PS_EV_COMPUTE_DONE = 0, PS_EV_PUSH_ARRIVE = 1, PS_EV_GRANT_DELIVER = 2,
+  PS_EV_PULL_ARRIVE = 3, PS_EV_PULL_RETURN = 4   /* trace.py:19-25 */
+};
+
+typedef struct ps_sim_config {
+  int32_t budget;              /* pushes per worker (engine.py:243-248) */
+  int32_t grad_kind;           /* enum ps_grad_kind */
+  int32_t loss_every;          /* 0: no loss sampling (simnet.py:118-125) */
+  int32_t n_synthetic;         /* synthetic update buffers per worker */
+  double comm_delay;           /* TimingSpec.comm_delay */
+  const double* compute_time;  /* host [P * budget]: the k-th compute draw of worker p */
+  const void* center;          /* host [d] bowl center (PS_GRAD_BOWL) */
+  int32_t center_dtype;
+  int32_t record_trace;        /* 1: keep TraceEntry rows */
+  const float* synthetic;      /* device [P][n_synthetic][d] (PS_GRAD_SYNTHETIC) */
+  int64_t max_events;          /* 0: unbounded */
+  int32_t data_ctas;           /* 0: one per SM minus the control CTA */
+  int32_t threads;             /* 0: default */
+} ps_sim_config;
+
+typedef struct ps_sim_result {
+  int64_t events;              /* events processed */
+  int64_t pushes;              /* push decisions */
+  int64_t applied;             /* updates applied (final version delta) */
+  int64_t rejected;
+  int64_t trace_rows;
+  int64_t loss_samples;
+  uint64_t unfinished;         /* DeadlockError workers */
+  int32_t status;              /* enum ps_status */
+  int32_t diverged_worker;
+  double device_ms;            /* kernel time, CUDA events on the launch stream */
+} ps_sim_result;
+
+typedef struct ps_trace_row {
+  double time;
+  int32_t worker;
+  int32_t kind;                /* enum ps_event_kind */
+  int64_t count;               /* clocks[worker] at the event (trace.py:32) */
+  int32_t decision;            /* -1 none, 0 grant, 1 defer */
+  int32_t _pad;
+  uint64_t released;           /* ascending ids as a bit mask */
+} ps_trace_row;
+
+int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* out);
+int ps_sim_trace(ps_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
+/* Loss samples of the last run: (version, 0.5*||w - c||^2 in fp64). */
+int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, int64_t* n);
+
+/* Per-kernel device time of the last ps_* call that launched work, in ms. */
+int ps_last_kernel_ms(ps_server* h, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSSP_PS_H */

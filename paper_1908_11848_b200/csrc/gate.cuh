@@ -1,0 +1,192 @@
+// gate.cuh -- the device-resident DSSP synchronization gate.
+//
+// One warp runs one decision: lane 0 owns the state machine (clock table,
+// two-deep push history, credits, deferred mask) and all 32 lanes share the
+// controller's (r_max+1)^2 fp64 grid. BSP, ASP and SSP are the degenerate
+// settings of the same machine, exactly as in the reference:
+//
+//   policy.py:84-90    record / interval (floor 1e-9)
+//   policy.py:60-73    minimum / maximum / slowest (ties -> smallest id) / is_fastest (ties count)
+//   policy.py:108-132  synchronization_controller
+//   policy.py:152-170  on_push        policy.py:172-195  _dssp_decide
+//   policy.py:197-206  _release (only on GRANT, ascending ids)
+//
+// Bit-exactness: every controller product and sum is an explicitly rounded
+// __dmul_rn / __dadd_rn / __dsub_rn (numpy evaluates r*I then latest + that,
+// never an FMA), the per-r minimum is exact, and the argmin keeps the smallest
+// r among equal minima (numpy argmin returns the first occurrence).
+#pragma once
+
+#include <stdint.h>
+#include "../../include/dssp_ps.h"
+
+namespace dssp {
+
+constexpr double kIntervalFloor = 1e-9;  // policy.py:26
+constexpr unsigned kFull = 0xffffffffu;
+
+struct GateResult {
+  int status;                 // PS_OK or PS_E_PROTOCOL
+  int outcome;                // 0 grant, 1 defer
+  unsigned long long released;
+};
+
+__device__ __forceinline__ double interval_of(double latest, double prev) {
+  double d = __dsub_rn(latest, prev);
+  return (kIntervalFloor > d) ? kIntervalFloor : d;  // Python max(d, floor)
+}
+
+// Warp-collective controller grid; every lane passes the same arguments.
+__device__ __forceinline__ int controller_grid(double lp, double pp, double ls, double ps, int r_max) {
+  const int lane = threadIdx.x & 31;
+  const double ip = interval_of(lp, pp);
+  const double is = interval_of(ls, ps);
+  double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  int best_r = 0x7fffffff;
+  for (int r = lane; r <= r_max; r += 32) {
+    const double cand = __dadd_rn(lp, __dmul_rn((double)r, ip));
+    double m = __longlong_as_double(0x7ff0000000000000ll);
+    for (int k = 0; k <= r_max; ++k) {
+      const double slow = __dadd_rn(ls, __dmul_rn((double)(k + 1), is));
+      const double gap = fabs(__dsub_rn(slow, cand));
+      if (gap < m) m = gap;
+    }
+    if (m < best) { best = m; best_r = r; }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ob = __shfl_xor_sync(kFull, best, off);
+    const int orr = __shfl_xor_sync(kFull, best_r, off);
+    if (ob < best || (ob == best && orr < best_r)) { best = ob; best_r = orr; }
+  }
+  return best_r;
+}
+
+__device__ __forceinline__ void record(ps_gate_state* s, int q, double t) {
+  s->previous[q] = s->latest[q];
+  s->latest[q] = t;
+  s->populated[q] += 1;
+}
+
+__device__ __forceinline__ long long min_clock(const ps_gate_state* s) {
+  long long m = s->clocks[0];
+  for (int q = 1; q < s->worker_count; ++q) m = s->clocks[q] < m ? s->clocks[q] : m;
+  return m;
+}
+
+__device__ __forceinline__ long long max_clock(const ps_gate_state* s) {
+  long long m = s->clocks[0];
+  for (int q = 1; q < s->worker_count; ++q) m = s->clocks[q] > m ? s->clocks[q] : m;
+  return m;
+}
+
+__device__ __forceinline__ int slowest(const ps_gate_state* s) {
+  const long long m = min_clock(s);
+  for (int q = 0; q < s->worker_count; ++q)
+    if (s->clocks[q] == m) return q;
+  return 0;
+}
+
+__device__ __forceinline__ unsigned long long release_ready(ps_gate_state* s) {
+  if (!s->deferred) return 0ull;
+  const long long low = min_clock(s);
+  unsigned long long ready = 0ull;
+  for (int q = 0; q < s->worker_count; ++q)
+    if (((s->deferred >> q) & 1ull) && s->clocks[q] - low <= s->threshold) ready |= 1ull << q;
+  s->deferred &= ~ready;
+  return ready;
+}
+
+// Warp-collective SyncPolicy.on_push. Only lane 0 touches *s; the result is
+// broadcast to every lane.
+__device__ inline GateResult gate_on_push(ps_gate_state* s, int p, double now) {
+  const int lane = threadIdx.x & 31;
+  int status = PS_OK, outcome = 0, stage = 0;  // stage 1: DSSP mint needs the controller grid
+  long long gap = 0;
+  double lp = 0, pp = 0, ls = 0, ps = 0;
+  int r_max = 0;
+  if (lane == 0) {
+    if (p < 0 || p >= s->worker_count) {
+      status = PS_E_PROTOCOL;                       // unknown worker
+    } else if ((s->deferred >> p) & 1ull) {
+      status = PS_E_PROTOCOL;                       // pushed while deferred
+    } else {
+      const long long count = ++s->clocks[p];
+      if (s->paradigm == PS_ASP) {
+        record(s, p, now);
+        outcome = 0;
+        stage = 3;                                  // grant, no release scan
+      } else if (s->paradigm == PS_DSSP) {
+        if (s->credits[p] > 0) {
+          s->credits[p] -= 1;
+          record(s, p, now);
+          outcome = 0;
+        } else {
+          gap = count - min_clock(s);
+          if (gap <= s->s_lower) {
+            record(s, p, now);
+            outcome = 0;
+          } else if (!(s->clocks[p] >= max_clock(s))) {
+            record(s, p, now);
+            outcome = 1;
+          } else {
+            record(s, p, now);                      // the controller records first
+            r_max = s->r_max;
+            stage = 2;                              // pred = 0 unless the grid runs
+            if (r_max > 0) {
+              const int sl = slowest(s);
+              if (s->populated[p] >= 2 && s->populated[sl] >= 2) {
+                lp = s->latest[p]; pp = s->previous[p];
+                ls = s->latest[sl]; ps = s->previous[sl];
+                stage = 1;
+              }
+            }
+          }
+        }
+      } else {
+        record(s, p, now);
+        outcome = (count - min_clock(s) <= s->threshold) ? 0 : 1;
+      }
+    }
+  }
+  stage = __shfl_sync(kFull, stage, 0);
+  int pred = 0;
+  if (stage == 1) {
+    lp = __shfl_sync(kFull, lp, 0); pp = __shfl_sync(kFull, pp, 0);
+    ls = __shfl_sync(kFull, ls, 0); ps = __shfl_sync(kFull, ps, 0);
+    r_max = __shfl_sync(kFull, r_max, 0);
+    pred = controller_grid(lp, pp, ls, ps, r_max);
+  }
+  unsigned long long released = 0ull;
+  if (lane == 0 && status == PS_OK) {
+    if (stage == 1 || stage == 2) {
+      long long headroom = (long long)s->s_lower + s->r_max - gap;
+      if (headroom < 0) headroom = 0;
+      const long long c = (long long)pred < headroom ? (long long)pred : headroom;
+      s->credits[p] = c;
+      outcome = c > 0 ? 0 : 1;
+    }
+    if (outcome == 1) {
+      s->deferred |= 1ull << p;
+    } else if (stage != 3) {
+      released = release_ready(s);
+    }
+    s->decisions += 1;
+  }
+  GateResult r;
+  r.status = __shfl_sync(kFull, status, 0);
+  r.outcome = __shfl_sync(kFull, outcome, 0);
+  r.released = __shfl_sync(kFull, released, 0);
+  return r;
+}
+
+__device__ __forceinline__ void gate_init(ps_gate_state* s, int paradigm, int workers, int s_lower,
+                                          int r_max) {
+  s->paradigm = paradigm;
+  s->worker_count = workers;
+  s->s_lower = s_lower;
+  s->r_max = r_max;
+  s->threshold = paradigm == PS_BSP ? 0 : s_lower;
+}
+
+}  // namespace dssp

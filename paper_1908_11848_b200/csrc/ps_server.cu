@@ -1,0 +1,550 @@
+// ps_server.cu -- single-GPU parameter server: push-apply, pull and the device
+// gate behind the C-ABI of include/dssp_ps.h.
+//
+// Push-apply (server.py:29-69). The weights are double buffered: one pass
+// reads w[cur] and the update, writes w[cur^1] (12 B/parameter: read w, read g,
+// write w) and ORs two flags per CTA -- non-finite gradient, non-finite result.
+// The last CTA to finish (threadfence-reduction election) publishes the
+// outcome: a clean pass flips `cur` and bumps the version; a non-finite
+// gradient is rejected and counted (server.py:65-67) and a non-finite result
+// is a DivergenceError (server.py:38-41) -- in both cases w[cur] was never
+// touched, so the reference's "weights unchanged" semantics hold exactly with
+// a single streaming pass and no grid barrier. In the fused push
+// (handle_push, server.py:80-82) the same last CTA then runs the gate
+// decision, so apply + clock increment + decision is one launch.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "gate.cuh"
+#include "server.h"
+
+using namespace dssp;
+
+static thread_local std::string g_create_error;
+
+int ps_fail(ps_server* h, int code, const std::string& msg) {
+  if (h) h->err = msg; else g_create_error = msg;
+  return code;
+}
+
+int ps_cuda_fail(ps_server* h, cudaError_t e, const char* what) {
+  std::string m = std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what;
+  return ps_fail(h, PS_E_CUDA, m);
+}
+
+namespace {
+
+constexpr int kApplyThreads = 256;
+constexpr int kApplyUnroll = 4;
+
+template <typename G>
+struct Vec4Load;
+template <>
+struct Vec4Load<float> {
+  static __device__ __forceinline__ float4 load(const float* g, long long j) {
+    return ld_stream(reinterpret_cast<const float4*>(g) + j);
+  }
+  static __device__ __forceinline__ float one(const float* g, long long i) { return g[i]; }
+};
+template <>
+struct Vec4Load<double> {
+  static __device__ __forceinline__ float4 load(const double* g, long long j) {
+    const double2* p = reinterpret_cast<const double2*>(g) + 2 * j;
+    double2 a = p[0], b = p[1];
+    return make_float4((float)a.x, (float)a.y, (float)b.x, (float)b.y);
+  }
+  static __device__ __forceinline__ float one(const double* g, long long i) { return (float)g[i]; }
+};
+
+// One streaming pass w[cur^1] = w[cur] - lr*g with flag reduction; the last CTA
+// publishes the result and (fuse=1) runs the gate decision.
+template <typename G>
+__global__ void __launch_bounds__(kApplyThreads)
+k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g, long long n,
+        float lr, Ctrl* ctrl, int fuse, int worker, double now) {
+  const int cur = *reinterpret_cast<volatile int*>(&ctrl->cur);
+  const float4* src = reinterpret_cast<const float4*>(cur ? w1 : w0);
+  float4* dst = reinterpret_cast<float4*>(cur ? w0 : w1);
+  const long long nv = n >> 2;
+  unsigned bad = 0;
+  const long long step = (long long)gridDim.x * kApplyThreads * kApplyUnroll;
+  for (long long base = (long long)blockIdx.x * kApplyThreads * kApplyUnroll + threadIdx.x; base < nv;
+       base += step) {
+    float4 a[kApplyUnroll], b[kApplyUnroll];
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u) {
+      const long long j = base + (long long)u * kApplyThreads;
+      if (j < nv) {
+        a[u] = src[j];
+        b[u] = Vec4Load<G>::load(g, j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kApplyUnroll; ++u) {
+      const long long j = base + (long long)u * kApplyThreads;
+      if (j < nv) {
+        const float4 r = apply4(a[u], lr, b[u]);
+        bad |= nonfinite4(b[u]) ? 1u : 0u;
+        bad |= nonfinite4(r) ? 2u : 0u;
+        dst[j] = r;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {  // ragged tail
+    const long long i = (nv << 2) + threadIdx.x;
+    const float* s = cur ? w1 : w0;
+    float* o = cur ? w0 : w1;
+    const float gi = Vec4Load<G>::one(g, i);
+    const float r = apply1(s[i], lr, gi);
+    bad |= nonfinite(gi) ? 1u : 0u;
+    bad |= nonfinite(r) ? 2u : 0u;
+    o[i] = r;
+  }
+  bad = __reduce_or_sync(kFull, bad);
+  __shared__ unsigned s_bad;
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && bad) atomicOr(&s_bad, bad);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_bad) atomicOr(&ctrl->bad, s_bad);
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
+  __threadfence();
+  const int lane = threadIdx.x;
+  int status = PS_OK;
+  if (lane == 0) {
+    const unsigned b = atomicAdd(&ctrl->bad, 0u);
+    int applied = 0;
+    if (b & 1u) {
+      status = PS_REJECTED;
+      ctrl->gate.rejected += 1;
+    } else if (b & 2u) {
+      status = PS_E_DIVERGED;
+    } else {
+      ctrl->cur = cur ^ 1;
+      ctrl->gate.version += 1;
+      applied = 1;
+    }
+    ctrl->arrive = 0;
+    ctrl->bad = 0;
+    ctrl->status = status;
+    ctrl->applied = applied;
+    ctrl->granted = 0;
+    ctrl->released = 0;
+  }
+  status = __shfl_sync(kFull, status, 0);
+  if (fuse && status != PS_E_DIVERGED) {
+    const GateResult r = gate_on_push(&ctrl->gate, worker, now);
+    if (lane == 0) {
+      if (r.status != PS_OK) ctrl->status = r.status;
+      ctrl->granted = (r.status == PS_OK && r.outcome == 0) ? 1 : 0;
+      ctrl->released = r.released;
+    }
+  }
+}
+
+__global__ void k_decide(Ctrl* ctrl, int worker, double now) {
+  const GateResult r = gate_on_push(&ctrl->gate, worker, now);
+  if (threadIdx.x == 0) {
+    ctrl->status = r.status;
+    ctrl->granted = (r.status == PS_OK && r.outcome == 0) ? 1 : 0;
+    ctrl->released = r.released;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_copy_out(const float* __restrict__ src, T* __restrict__ dst,
+                                                  long long n) {
+  const long long nv = n >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += stride) {
+    const float4 v = reinterpret_cast<const float4*>(src)[j];
+    if constexpr (sizeof(T) == 4) {
+      reinterpret_cast<float4*>(dst)[j] = v;
+    } else {
+      double2* o = reinterpret_cast<double2*>(dst) + 2 * j;
+      o[0] = make_double2(v.x, v.y);
+      o[1] = make_double2(v.z, v.w);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const long long i = (nv << 2) + threadIdx.x;
+    dst[i] = (T)src[i];
+  }
+}
+
+template <typename T>
+__global__ void k_load_in(const T* __restrict__ src, float* __restrict__ dst, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = (float)src[i];
+}
+
+__global__ void k_controller_batch(const double* tables, const int* r_max, int n, int* out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= n) return;  // warp-uniform
+  const double* t = tables + 4 * (long long)row;
+  const int rm = r_max[row];
+  const int r = rm <= 0 ? 0 : controller_grid(t[0], t[1], t[2], t[3], rm);
+  if ((threadIdx.x & 31) == 0) out[row] = r;
+}
+
+int grid_for(const ps_server* h, long long nv) {
+  long long per_block = (long long)kApplyThreads * kApplyUnroll;
+  long long blocks = (nv + per_block - 1) / per_block;
+  long long cap = (long long)h->sm_count * 8;
+  if (blocks < 1) blocks = 1;
+  if (blocks > cap) blocks = cap;
+  return (int)blocks;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int ensure_stage(ps_server* h, size_t bytes) {
+  if (h->stage_bytes >= bytes) return PS_OK;
+  if (h->stage) cudaFree(h->stage);
+  if (h->hstage) cudaFreeHost(h->hstage);
+  h->stage = nullptr;
+  h->hstage = nullptr;
+  h->stage_bytes = 0;
+  PS_CK(h, cudaMalloc(&h->stage, bytes));
+  PS_CK(h, cudaMallocHost(&h->hstage, bytes));
+  h->stage_bytes = bytes;
+  return PS_OK;
+}
+
+int sync_ctrl(ps_server* h) {
+  PS_CK(h, cudaMemcpyAsync(h->hctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  h->cur = h->hctrl->cur;
+  return PS_OK;
+}
+
+struct DevGuard {
+  int prev = 0;
+  explicit DevGuard(int d) { cudaGetDevice(&prev); cudaSetDevice(d); }
+  ~DevGuard() { cudaSetDevice(prev); }
+};
+
+// Launch the apply (optionally fused with the decision) on a device- or host-
+// resident update. Host updates go through pinned staging (one H2D copy).
+int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_device, int fuse,
+                 double now) {
+  if (g_dtype != PS_F32 && g_dtype != PS_F64) return ps_fail(h, PS_E_VALUE, "bad gradient dtype");
+  if (!g) return ps_fail(h, PS_E_VALUE, "null gradient");
+  const size_t esz = g_dtype == PS_F64 ? 8 : 4;
+  const size_t bytes = (size_t)h->d * esz;
+  const void* dg = g;
+  if (!g_on_device || !aligned16(g)) {
+    int rc = ensure_stage(h, bytes);
+    if (rc) return rc;
+    if (!g_on_device) {
+      PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, cudaMemcpyHostToDevice, h->stream));
+    } else {
+      PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    }
+    dg = h->stage;
+  }
+  const float lr = (float)h->cfg.learning_rate;
+  const int grid = grid_for(h, h->nv);
+  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  if (g_dtype == PS_F32)
+    k_apply<float><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const float*)dg, h->d,
+                                                          lr, h->ctrl, fuse, worker, now);
+  else
+    k_apply<double><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const double*)dg,
+                                                           h->d, lr, h->ctrl, fuse, worker, now);
+  PS_CK(h, cudaGetLastError());
+  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
+  int rc = sync_ctrl(h);
+  if (rc) return rc;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->last_ms = ms;
+  return PS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_device_count(int32_t* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  *n = (e == cudaSuccess) ? c : 0;
+  return e == cudaSuccess ? PS_OK : ps_cuda_fail(nullptr, e, "cudaGetDeviceCount");
+}
+
+const char* ps_last_error(const ps_server* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int ps_create(const ps_config* cfg, const void* w0_host, int32_t w0_dtype, ps_server** out) {
+  *out = nullptr;
+  if (!cfg) return ps_fail(nullptr, PS_E_VALUE, "null config");
+  if (cfg->paradigm < PS_BSP || cfg->paradigm > PS_DSSP)
+    return ps_fail(nullptr, PS_E_VALUE, "paradigm: must be one of bsp, asp, ssp, dssp");
+  if (cfg->worker_count < 1 || cfg->worker_count > PS_MAX_WORKERS)
+    return ps_fail(nullptr, PS_E_VALUE, "worker_count: must be in [1, 64]");
+  if (cfg->s_lower < 0 || cfg->r_max < 0)
+    return ps_fail(nullptr, PS_E_VALUE, "staleness: s_lower and r_max must be >= 0");
+  if (!(cfg->learning_rate > 0)) return ps_fail(nullptr, PS_E_VALUE, "learning_rate must be > 0");
+  if (cfg->dimension < 1) return ps_fail(nullptr, PS_E_VALUE, "dimension: must be >= 1");
+  ps_server* h = new ps_server();
+  h->cfg = *cfg;
+  h->dev = cfg->device;
+  DevGuard guard(h->dev);
+  cudaError_t e = cudaSetDevice(h->dev);
+  if (e != cudaSuccess) {
+    delete h;
+    return ps_cuda_fail(nullptr, e, "cudaSetDevice");
+  }
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->dev);
+  h->d = cfg->dimension;
+  h->nv = (h->d + 3) / 4;
+  h->dpad = h->nv * 4;
+  auto bail = [&](cudaError_t err, const char* what) {
+    int rc = ps_cuda_fail(nullptr, err, what);
+    ps_destroy(h);
+    return rc;
+  };
+  if ((e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking))) return bail(e, "stream");
+  if ((e = cudaEventCreate(&h->ev0)) || (e = cudaEventCreate(&h->ev1))) return bail(e, "event");
+  for (int b = 0; b < 2; ++b) {
+    if ((e = cudaMalloc(&h->w[b], h->dpad * sizeof(float)))) return bail(e, "cudaMalloc weights");
+    if ((e = cudaMemsetAsync(h->w[b], 0, h->dpad * sizeof(float), h->stream))) return bail(e, "memset");
+  }
+  if ((e = cudaMalloc(&h->ctrl, sizeof(Ctrl)))) return bail(e, "cudaMalloc ctrl");
+  if ((e = cudaMallocHost(&h->hctrl, sizeof(Ctrl)))) return bail(e, "cudaMallocHost ctrl");
+  std::memset(h->hctrl, 0, sizeof(Ctrl));
+  ps_gate_state& gs = h->hctrl->gate;
+  gs.paradigm = cfg->paradigm;
+  gs.worker_count = cfg->worker_count;
+  gs.s_lower = cfg->s_lower;
+  gs.r_max = cfg->r_max;
+  gs.threshold = cfg->paradigm == PS_BSP ? 0 : cfg->s_lower;  // policy.py:143-146
+  if ((e = cudaMemcpyAsync(h->ctrl, h->hctrl, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream)))
+    return bail(e, "ctrl upload");
+  if (w0_host) {
+    const size_t esz = w0_dtype == PS_F64 ? 8 : 4;
+    void* tmp = nullptr;
+    if ((e = cudaMalloc(&tmp, h->d * esz))) return bail(e, "cudaMalloc w0");
+    if ((e = cudaMemcpyAsync(tmp, w0_host, h->d * esz, cudaMemcpyHostToDevice, h->stream)))
+      return bail(e, "w0 upload");
+    if (w0_dtype == PS_F64)
+      k_load_in<double><<<h->sm_count * 4, 256, 0, h->stream>>>((const double*)tmp, h->w[0], h->d);
+    else
+      k_load_in<float><<<h->sm_count * 4, 256, 0, h->stream>>>((const float*)tmp, h->w[0], h->d);
+    if ((e = cudaStreamSynchronize(h->stream))) return bail(e, "w0 convert");
+    cudaFree(tmp);
+  }
+  if ((e = cudaStreamSynchronize(h->stream))) return bail(e, "create sync");
+  *out = h;
+  return PS_OK;
+}
+
+void ps_destroy(ps_server* h) {
+  if (!h) return;
+  DevGuard guard(h->dev);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  cudaFree(h->w[0]);
+  cudaFree(h->w[1]);
+  cudaFree(h->ctrl);
+  cudaFreeHost(h->hctrl);
+  cudaFree(h->stage);
+  cudaFreeHost(h->hstage);
+  ps_sim_buffers& s = h->sim;
+  cudaFree(s.ops); cudaFree(s.produced); cudaFree(s.gcount); cudaFree(s.gbad);
+  cudaFree(s.rep); cudaFree(s.gbuf); cudaFree(s.center); cudaFree(s.ctime);
+  cudaFree(s.trace); cudaFree(s.losses); cudaFree(s.out);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int ps_apply(ps_server* h, int32_t worker, const void* g, int32_t g_dtype, int32_t g_on_device,
+             int32_t* applied) {
+  DevGuard guard(h->dev);
+  int rc = launch_apply(h, worker, g, g_dtype, g_on_device, 0, 0.0);
+  if (rc) return rc;
+  *applied = h->hctrl->applied;
+  const int st = h->hctrl->status;
+  if (st == PS_E_DIVERGED)
+    return ps_fail(h, PS_E_DIVERGED, "non-finite weights after update " +
+                                         std::to_string(h->hctrl->gate.version + 1) + " from worker " +
+                                         std::to_string(worker));
+  return st;
+}
+
+int ps_decide(ps_server* h, int32_t worker, double now, int32_t* granted, uint64_t* released) {
+  DevGuard guard(h->dev);
+  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  k_decide<<<1, 32, 0, h->stream>>>(h->ctrl, worker, now);
+  PS_CK(h, cudaGetLastError());
+  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
+  int rc = sync_ctrl(h);
+  if (rc) return rc;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->last_ms = ms;
+  *granted = h->hctrl->granted;
+  *released = h->hctrl->released;
+  if (h->hctrl->status == PS_E_PROTOCOL)
+    return ps_fail(h, PS_E_PROTOCOL, "worker " + std::to_string(worker) +
+                                         " is unknown or pushed while deferred");
+  return PS_OK;
+}
+
+int ps_push(ps_server* h, int32_t worker, const void* g, int32_t g_dtype, int32_t g_on_device,
+            double now, int32_t* applied, int32_t* granted, uint64_t* released) {
+  DevGuard guard(h->dev);
+  int rc = launch_apply(h, worker, g, g_dtype, g_on_device, 1, now);
+  if (rc) return rc;
+  *applied = h->hctrl->applied;
+  *granted = h->hctrl->granted;
+  *released = h->hctrl->released;
+  const int st = h->hctrl->status;
+  if (st == PS_E_DIVERGED)
+    return ps_fail(h, PS_E_DIVERGED, "non-finite weights after update " +
+                                         std::to_string(h->hctrl->gate.version + 1));
+  if (st == PS_E_PROTOCOL)
+    return ps_fail(h, PS_E_PROTOCOL, "worker " + std::to_string(worker) +
+                                         " is unknown or pushed while deferred");
+  return st;
+}
+
+int ps_pull(ps_server* h, int32_t worker, void* dst, int32_t dst_dtype, int32_t dst_on_device,
+            int64_t* version) {
+  if (worker < 0 || worker >= h->cfg.worker_count)
+    return ps_fail(h, PS_E_PROTOCOL, "unknown worker " + std::to_string(worker));
+  if ((h->hctrl->gate.deferred >> worker) & 1ull)
+    return ps_fail(h, PS_E_PROTOCOL, "worker " + std::to_string(worker) + " pulled while deferred");
+  return ps_read_weights(h, dst, dst_dtype, dst_on_device, version);
+}
+
+int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_device,
+                    int64_t* version) {
+  DevGuard guard(h->dev);
+  if (dst_dtype != PS_F32 && dst_dtype != PS_F64) return ps_fail(h, PS_E_VALUE, "bad dtype");
+  const float* src = h->w[h->cur];
+  const size_t esz = dst_dtype == PS_F64 ? 8 : 4;
+  if (version) *version = h->hctrl->gate.version;
+  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  if (dst_on_device && aligned16(dst)) {
+    const int grid = grid_for(h, h->nv);
+    if (dst_dtype == PS_F32)
+      k_copy_out<float><<<grid, 256, 0, h->stream>>>(src, (float*)dst, h->d);
+    else
+      k_copy_out<double><<<grid, 256, 0, h->stream>>>(src, (double*)dst, h->d);
+    PS_CK(h, cudaGetLastError());
+  } else if (dst_dtype == PS_F32) {
+    PS_CK(h, cudaMemcpyAsync(dst, src, h->d * 4, cudaMemcpyDefault, h->stream));
+  } else {
+    int rc = ensure_stage(h, h->d * esz);
+    if (rc) return rc;
+    k_copy_out<double><<<grid_for(h, h->nv), 256, 0, h->stream>>>(src, (double*)h->stage, h->d);
+    PS_CK(h, cudaGetLastError());
+    PS_CK(h, cudaMemcpyAsync(dst, h->stage, h->d * esz, cudaMemcpyDefault, h->stream));
+  }
+  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->last_ms = ms;
+  return PS_OK;
+}
+
+int ps_get_state(ps_server* h, ps_gate_state* out) {
+  DevGuard guard(h->dev);
+  int rc = sync_ctrl(h);
+  if (rc) return rc;
+  *out = h->hctrl->gate;
+  return PS_OK;
+}
+
+int ps_peek_state(const ps_server* h, ps_gate_state* out) {
+  *out = h->hctrl->gate;
+  return PS_OK;
+}
+
+int ps_set_state(ps_server* h, const ps_gate_state* in) {
+  DevGuard guard(h->dev);
+  if (in->worker_count != h->cfg.worker_count || in->paradigm != h->cfg.paradigm)
+    return ps_fail(h, PS_E_VALUE, "state does not match the server configuration");
+  for (int q = 0; q < in->worker_count; ++q)
+    if (in->credits[q] < 0) return ps_fail(h, PS_E_VALUE, "credits cannot go negative");
+  h->hctrl->gate = *in;
+  PS_CK(h, cudaMemcpyAsync(&h->ctrl->gate, &h->hctrl->gate, sizeof(ps_gate_state),
+                           cudaMemcpyHostToDevice, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  return PS_OK;
+}
+
+int ps_last_kernel_ms(ps_server* h, double* ms) {
+  *ms = h->last_ms;
+  return PS_OK;
+}
+
+int ps_controller_batch(int32_t device, const double* tables, const int32_t* r_max, int32_t n,
+                        int32_t* out) {
+  if (n <= 0) return PS_OK;
+  DevGuard guard(device);
+  double* dt = nullptr;
+  int* dr = nullptr;
+  int* dout = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc(&dt, sizeof(double) * 4 * n)) || (e = cudaMalloc(&dr, sizeof(int) * n)) ||
+      (e = cudaMalloc(&dout, sizeof(int) * n)))
+    return ps_cuda_fail(nullptr, e, "controller alloc");
+  cudaMemcpy(dt, tables, sizeof(double) * 4 * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dr, r_max, sizeof(int) * n, cudaMemcpyHostToDevice);
+  const int warps_per_block = 4;
+  k_controller_batch<<<(n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block>>>(dt, dr, n,
+                                                                                            dout);
+  e = cudaMemcpy(out, dout, sizeof(int) * n, cudaMemcpyDeviceToHost);
+  cudaFree(dt);
+  cudaFree(dr);
+  cudaFree(dout);
+  return e == cudaSuccess ? PS_OK : ps_cuda_fail(nullptr, e, "controller batch");
+}
+
+int ps_apply_vectors(int32_t device, const void* w, const void* g, int32_t dtype, int64_t n,
+                     double lr, void* out, int32_t* status) {
+  if (!(lr > 0)) return ps_fail(nullptr, PS_E_VALUE, "learning_rate must be > 0");
+  if (n < 1) return ps_fail(nullptr, PS_E_VALUE, "dimension must be >= 1");
+  ps_config cfg{};
+  cfg.paradigm = PS_ASP;
+  cfg.worker_count = 1;
+  cfg.learning_rate = lr;
+  cfg.dimension = n;
+  cfg.device = device;
+  ps_server* h = nullptr;
+  int rc = ps_create(&cfg, w, dtype, &h);
+  if (rc) return rc;
+  int32_t applied = 0;
+  rc = ps_apply(h, 0, g, dtype, 0, &applied);
+  // apply_update (server.py:29-42) has no gradient check of its own: a
+  // non-finite gradient surfaces as a non-finite result.
+  const unsigned reject = (rc == PS_REJECTED);
+  *status = (rc == PS_E_DIVERGED || reject) ? PS_E_DIVERGED : rc;
+  if (rc == PS_OK) {
+    int64_t v = 0;
+    rc = ps_read_weights(h, out, dtype, 0, &v);
+  }
+  if (rc == PS_REJECTED || rc == PS_E_DIVERGED) rc = PS_OK;
+  if (rc != PS_OK) g_create_error = h->err;
+  ps_destroy(h);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,603 @@
+// ps_sim.cu -- the device-resident parameter-server run loop.
+//
+// One cooperative persistent kernel executes a whole simulated cluster run
+// (simnet.py:127-201) with the host out of the loop:
+//
+//   * warp 0 of CTA 0 is the CONTROL warp. Lane 0 runs the reference's event
+//     loop -- (time, seq) ordered events, one in flight per worker, same-instant
+//     push aggregation (simnet.py:167-201: apply every gradient of the group in
+//     seq order, then decide each) -- and the whole warp runs each gate
+//     decision (gate.cuh). It appends TraceEntry rows (trace.py:28-37) and emits
+//     data operations into an in-HBM op log that it publishes with a release
+//     store. It never waits for the data side.
+//   * every other warp is a DATA warp that owns a fixed contiguous slice of
+//     the parameter vector and replays the op log in order over its slice:
+//       PULL  (handle_pull, server.py:84-91)  copy the weights into the
+//             worker's staging replica -- the snapshot is materialized at
+//             PULL_ARRIVE, adopted at PULL_RETURN (simnet.py:135-138, :156-159);
+//       GRAD  (WorkerState.begin_iteration, engine.py:263-272) produce the
+//             worker's update (quadratic bowl g = w_local - c, engine.py:46-60,
+//             or a resident synthetic N(0,1) buffer) and contribute to its
+//             whole-vector finiteness flag;
+//       APPLY (apply_gradient, server.py:58-69) wait until every data warp
+//             has flagged that update, then w = w - lr*g on the slice, or skip
+//             it when any element was non-finite (rejected, counted).
+//     Every element is touched by exactly one thread in op order, so per-element
+//     update order equals the global push order with no atomics on weights and
+//     no grid barrier; the only cross-warp dependency is the per-update
+//     finiteness count.
+#include <cuda_runtime.h>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gate.cuh"
+#include "server.h"
+
+using namespace dssp;
+
+namespace {
+
+enum OpType : int32_t { OP_PULL = 1, OP_GRAD = 2, OP_APPLY = 3, OP_END = 4 };
+
+struct Op {
+  int32_t type;
+  int32_t worker;
+  int32_t buf;    // PULL: staging replica; GRAD: active replica (bowl) / synthetic index; APPLY: synthetic index
+  int32_t slot;   // update id (GRAD/APPLY)
+};
+
+struct SimOut {
+  long long events, pushes, trace_rows, applied, rejected;
+  unsigned long long unfinished;
+  int status, diverged_worker;
+};
+
+struct SimArgs {
+  int P, budget, grad_kind, n_synth, loss_every, record_trace;
+  long long nv, dpad, max_events, trace_cap, loss_cap, ops_cap;
+  double comm_delay;
+  float lr;
+  float* W;
+  float* rep;
+  float* gbuf;
+  const float* center;
+  const float* synth;
+  const double* ctime;
+  Op* ops;
+  unsigned long long* produced;
+  unsigned* gcount;
+  unsigned* gbad;
+  ps_trace_row* trace;
+  double* losses;
+  Ctrl* ctrl;
+  SimOut* out;
+  unsigned n_data_warps;
+  unsigned long long timeout_ns;
+  long long base_version;
+};
+
+constexpr int kSimThreads = 256;
+constexpr int kMaxP = PS_MAX_WORKERS;
+
+struct CtlState {
+  ps_gate_state gate;
+  double ev_time[kMaxP];
+  long long ev_seq[kMaxP];
+  int ev_kind[kMaxP];         // -1: no event in flight for this worker
+  int iterations[kMaxP];
+  int active[kMaxP];          // replica the worker computes on
+  int staged[kMaxP];          // replica the last pull wrote
+  int grad_slot[kMaxP];
+  int synth_idx[kMaxP];
+  int finished[kMaxP];
+  int group[kMaxP];           // current push group, in seq order
+  int group_len, group_pos;
+  double group_at;
+  long long seq, processed, n_ops, n_trace, pushes, next_slot;
+  int status;
+};
+
+__device__ __forceinline__ void ctl_trace(const SimArgs& a, CtlState& s, double t, int w, int kind,
+                                          int decision, unsigned long long released) {
+  if (a.record_trace && s.n_trace < a.trace_cap) {
+    ps_trace_row r;
+    r.time = t;
+    r.worker = w;
+    r.kind = kind;
+    r.count = s.gate.clocks[w];
+    r.decision = decision;
+    r._pad = 0;
+    r.released = released;
+    a.trace[s.n_trace] = r;
+  }
+  s.n_trace += 1;
+}
+
+__device__ __forceinline__ void ctl_schedule(CtlState& s, double at, int kind, int w) {
+  s.ev_time[w] = at;
+  s.ev_seq[w] = s.seq++;
+  s.ev_kind[w] = kind;
+}
+
+__device__ __forceinline__ void ctl_emit(const SimArgs& a, CtlState& s, int type, int w, int buf,
+                                         int slot) {
+  Op op;
+  op.type = type;
+  op.worker = w;
+  op.buf = buf;
+  op.slot = slot;
+  a.ops[s.n_ops] = op;
+  s.n_ops += 1;
+}
+
+__device__ __forceinline__ void ctl_publish(const SimArgs& a, CtlState& s) {
+  st_release_u64(a.produced, (unsigned long long)s.n_ops);
+}
+
+// Lane 0 only. Advances the event loop until a decision is needed (returns 1,
+// *p/*now set) or the run is over (returns 2).
+__device__ int ctl_advance(const SimArgs& a, CtlState& s, int* p, double* now) {
+  for (;;) {
+    if (s.group_pos < s.group_len) {
+      *p = s.group[s.group_pos];
+      *now = s.group_at;
+      return 1;
+    }
+    if (s.status != PS_OK) return 2;
+    // pop the (time, seq)-minimum event
+    int w = -1;
+    for (int q = 0; q < a.P; ++q) {
+      if (s.ev_kind[q] < 0) continue;
+      if (w < 0 || s.ev_time[q] < s.ev_time[w] ||
+          (s.ev_time[q] == s.ev_time[w] && s.ev_seq[q] < s.ev_seq[w]))
+        w = q;
+    }
+    if (w < 0) return 2;
+    if (a.max_events > 0 && s.processed >= a.max_events) {
+      s.status = PS_E_BUDGET;
+      return 2;
+    }
+    const double at = s.ev_time[w];
+    const int kind = s.ev_kind[w];
+    s.ev_kind[w] = -1;
+    s.processed += 1;
+    if (kind == PS_EV_PULL_ARRIVE) {
+      const int st = 1 - s.active[w];
+      ctl_emit(a, s, OP_PULL, w, st, 0);
+      s.staged[w] = st;
+      ctl_trace(a, s, at, w, kind, -1, 0);
+      ctl_schedule(s, at + a.comm_delay, PS_EV_PULL_RETURN, w);
+    } else if (kind == PS_EV_PULL_RETURN) {
+      s.active[w] = s.staged[w];  // adopt (simnet.py:156-165)
+      ctl_trace(a, s, at, w, kind, -1, 0);
+      if (s.iterations[w] < a.budget) {
+        ctl_schedule(s, at + a.ctime[(long long)w * a.budget + s.iterations[w]], PS_EV_COMPUTE_DONE, w);
+      } else {
+        s.finished[w] = 1;
+      }
+    } else if (kind == PS_EV_COMPUTE_DONE) {
+      s.iterations[w] += 1;
+      const int slot = (int)s.next_slot++;
+      s.grad_slot[w] = slot;
+      const int buf = a.grad_kind == PS_GRAD_BOWL ? s.active[w] : (s.synth_idx[w] % a.n_synth);
+      ctl_emit(a, s, OP_GRAD, w, buf, slot);
+      ctl_trace(a, s, at, w, kind, -1, 0);
+      ctl_schedule(s, at + a.comm_delay, PS_EV_PUSH_ARRIVE, w);
+    } else if (kind == PS_EV_GRANT_DELIVER) {
+      ctl_trace(a, s, at, w, kind, -1, 0);
+      ctl_schedule(s, at + a.comm_delay, PS_EV_PULL_ARRIVE, w);
+    } else {
+      // PUSH_ARRIVE: aggregate every push queued at the same instant
+      // (simnet.py:167-182), ordered by seq, the popped one first.
+      int n = 0;
+      s.group[n++] = w;
+      for (int q = 0; q < a.P; ++q) {
+        if (s.ev_kind[q] == PS_EV_PUSH_ARRIVE && s.ev_time[q] == at) {
+          int i = n++;
+          while (i > 1 && s.ev_seq[s.group[i - 1]] > s.ev_seq[q]) {
+            s.group[i] = s.group[i - 1];
+            --i;
+          }
+          s.group[i] = q;
+          s.ev_kind[q] = -1;
+        }
+      }
+      for (int i = 0; i < n; ++i) {
+        const int m = s.group[i];
+        const int buf = a.grad_kind == PS_GRAD_BOWL ? 0 : (s.synth_idx[m] % a.n_synth);
+        ctl_emit(a, s, OP_APPLY, m, buf, s.grad_slot[m]);
+        s.synth_idx[m] += 1;
+      }
+      s.group_len = n;
+      s.group_pos = 0;
+      s.group_at = at;
+    }
+    ctl_publish(a, s);
+  }
+}
+
+__device__ void ctl_after_decision(const SimArgs& a, CtlState& s, const GateResult& r) {
+  const int m = s.group[s.group_pos++];
+  const double at = s.group_at;
+  s.pushes += 1;
+  if (r.status != PS_OK) {
+    s.status = r.status;
+    s.group_len = s.group_pos;
+    return;
+  }
+  ctl_trace(a, s, at, m, PS_EV_PUSH_ARRIVE, r.outcome, r.released);
+  if (r.outcome == 0) {
+    ctl_schedule(s, at + a.comm_delay, PS_EV_GRANT_DELIVER, m);
+    for (int q = 0; q < a.P; ++q)
+      if ((r.released >> q) & 1ull) ctl_schedule(s, at + a.comm_delay, PS_EV_GRANT_DELIVER, q);
+  }
+}
+
+__device__ void control_warp(const SimArgs& a, CtlState& s) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s.gate = a.ctrl->gate;
+    for (int q = 0; q < kMaxP; ++q) {
+      s.ev_kind[q] = -1;
+      s.iterations[q] = 0;
+      s.active[q] = 0;
+      s.staged[q] = 0;
+      s.grad_slot[q] = 0;
+      s.synth_idx[q] = 0;
+      s.finished[q] = 0;
+    }
+    s.group_len = s.group_pos = 0;
+    s.seq = s.processed = s.n_ops = s.n_trace = s.pushes = s.next_slot = 0;
+    s.status = PS_OK;
+    for (int q = 0; q < a.P; ++q) ctl_schedule(s, a.comm_delay, PS_EV_PULL_ARRIVE, q);
+  }
+  __syncwarp();
+  for (;;) {
+    int cmd = 0, p = 0;
+    double now = 0.0;
+    if (lane == 0) cmd = ctl_advance(a, s, &p, &now);
+    cmd = __shfl_sync(kFull, cmd, 0);
+    if (cmd == 2) break;
+    p = __shfl_sync(kFull, p, 0);
+    now = __shfl_sync(kFull, now, 0);
+    const GateResult r = gate_on_push(&s.gate, p, now);
+    if (lane == 0) ctl_after_decision(a, s, r);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    ctl_emit(a, s, OP_END, 0, 0, 0);
+    ctl_publish(a, s);
+    unsigned long long unfinished = 0;
+    for (int q = 0; q < a.P; ++q)
+      if (!s.finished[q]) unfinished |= 1ull << q;
+    // gate tables back to the control block; version/rejected belong to the data side
+    const long long v = a.ctrl->gate.version, rj = a.ctrl->gate.rejected;
+    a.ctrl->gate = s.gate;
+    a.ctrl->gate.version = v;
+    a.ctrl->gate.rejected = rj;
+    a.out->events = s.processed;
+    a.out->pushes = s.pushes;
+    a.out->trace_rows = s.n_trace;
+    a.out->unfinished = s.status == PS_OK ? unfinished : 0ull;
+    if (s.status != PS_OK) atomicCAS(&a.out->status, PS_OK, s.status);
+  }
+}
+
+__device__ void data_warp(const SimArgs& a, unsigned dw) {
+  const int lane = threadIdx.x & 31;
+  const long long per = (a.nv + a.n_data_warps - 1) / a.n_data_warps;
+  const long long lo = (long long)dw * per;
+  const long long hi = lo + per < a.nv ? lo + per : a.nv;
+  float4* W = reinterpret_cast<float4*>(a.W);
+  const float4* C = reinterpret_cast<const float4*>(a.center);
+  long long avail = 0, applied = 0, rejected = 0;
+  const unsigned long long t0 = globaltimer_ns();
+  for (long long i = 0;; ++i) {
+    if (i >= avail) {
+      unsigned long long v = 0;
+      if (lane == 0) {
+        for (;;) {
+          v = ld_acquire_u64(a.produced);
+          if ((long long)v > i) break;
+          if (globaltimer_ns() - t0 > a.timeout_ns) { v = 0; break; }
+          __nanosleep(64);
+        }
+      }
+      v = __shfl_sync(kFull, v, 0);
+      if ((long long)v <= i) {  // watchdog: never hang the GPU
+        if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
+        return;
+      }
+      avail = (long long)v;
+    }
+    const int4 raw = __ldcg(reinterpret_cast<const int4*>(a.ops) + i);
+    const int type = raw.x, w = raw.y, buf = raw.z, slot = raw.w;
+    if (type == OP_END) break;
+    if (type == OP_PULL) {
+      float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)w * 2 + buf) * a.dpad);
+      for (long long j = lo + lane; j < hi; j += 32) dst[j] = W[j];
+    } else if (type == OP_GRAD) {
+      bool bad = false;
+      if (a.grad_kind == PS_GRAD_BOWL) {
+        const float4* src = reinterpret_cast<const float4*>(a.rep + ((long long)w * 2 + buf) * a.dpad);
+        float4* g = reinterpret_cast<float4*>(a.gbuf + (long long)w * a.dpad);
+        for (long long j = lo + lane; j < hi; j += 32) {
+          const float4 x = src[j], c = C[j];
+          const float4 r = make_float4(__fsub_rn(x.x, c.x), __fsub_rn(x.y, c.y),
+                                       __fsub_rn(x.z, c.z), __fsub_rn(x.w, c.w));
+          bad |= nonfinite4(r);
+          g[j] = r;
+        }
+      } else {
+        const float4* src =
+            reinterpret_cast<const float4*>(a.synth + ((long long)w * a.n_synth + buf) * a.dpad);
+        for (long long j = lo + lane; j < hi; j += 32) bad |= nonfinite4(ld_stream(src + j));
+      }
+      const bool any_bad = __any_sync(kFull, bad);
+      if (lane == 0) {
+        if (any_bad) atomicOr(&a.gbad[slot], 1u);
+        __threadfence();
+        atomicAdd(&a.gcount[slot], 1u);
+      }
+    } else if (type == OP_APPLY) {
+      unsigned bad = 0;
+      if (lane == 0) {
+        while (ld_acquire_u32(&a.gcount[slot]) < a.n_data_warps) {
+          if (globaltimer_ns() - t0 > a.timeout_ns) { bad = 2; break; }
+          __nanosleep(32);
+        }
+        if (!bad) bad = ld_relaxed_u32(&a.gbad[slot]);
+      }
+      bad = __shfl_sync(kFull, bad, 0);
+      if (bad == 2) {
+        if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
+        return;
+      }
+      if (bad) {
+        rejected += 1;
+        continue;
+      }
+      const float4* g = a.grad_kind == PS_GRAD_BOWL
+                            ? reinterpret_cast<const float4*>(a.gbuf + (long long)w * a.dpad)
+                            : reinterpret_cast<const float4*>(a.synth + ((long long)w * a.n_synth + buf) * a.dpad);
+      bool dbad = false;
+      for (long long j = lo + lane; j < hi; j += 32) {
+        const float4 r = apply4(W[j], a.lr, g[j]);
+        dbad |= nonfinite4(r);
+        W[j] = r;
+      }
+      applied += 1;
+      if (__any_sync(kFull, dbad) && lane == 0) {
+        if (atomicCAS(&a.out->status, PS_OK, PS_E_DIVERGED) == PS_OK) a.out->diverged_worker = w;
+      }
+      if (a.loss_every > 0 && (a.base_version + applied) % a.loss_every == 0) {
+        double acc = 0.0;
+        for (long long j = lo + lane; j < hi; j += 32) {
+          const float4 x = W[j], c = C[j];
+          const double d0 = (double)x.x - (double)c.x, d1 = (double)x.y - (double)c.y;
+          const double d2 = (double)x.z - (double)c.z, d3 = (double)x.w - (double)c.w;
+          acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+        const long long sample = (a.base_version + applied) / a.loss_every - 1 -
+                                 a.base_version / a.loss_every;
+        if (lane == 0 && sample >= 0 && sample < a.loss_cap) atomicAdd(&a.losses[sample], 0.5 * acc);
+      }
+    }
+  }
+  if (dw == 0 && lane == 0) {
+    a.out->applied = applied;
+    a.out->rejected = rejected;
+  }
+}
+
+__global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
+  __shared__ CtlState s;
+  const unsigned gw = (blockIdx.x * kSimThreads + threadIdx.x) >> 5;
+  if (gw == 0) {
+    control_warp(a, s);
+  } else {
+    data_warp(a, gw - 1);
+  }
+}
+
+// After the run: fold the data side's counters into the control block.
+__global__ void k_sim_finish(Ctrl* ctrl, SimOut* out) {
+  ctrl->gate.version += out->applied;
+  ctrl->gate.rejected += out->rejected;
+}
+
+template <typename T>
+__global__ void k_to_f32(const T* src, float* dst, long long n, long long dpad) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < dpad; i += stride)
+    dst[i] = i < n ? (float)src[i] : 0.f;
+}
+
+struct DevGuard {
+  int prev = 0;
+  explicit DevGuard(int d) { cudaGetDevice(&prev); cudaSetDevice(d); }
+  ~DevGuard() { cudaSetDevice(prev); }
+};
+
+template <typename T>
+int grow(ps_server* h, T** p, size_t* cap, size_t need) {
+  if (*cap >= need && *p) return PS_OK;
+  cudaFree(*p);
+  *p = nullptr;
+  PS_CK(h, cudaMalloc((void**)p, need * sizeof(T)));
+  *cap = need;
+  return PS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
+  DevGuard guard(h->dev);
+  std::memset(res, 0, sizeof(*res));
+  const int P = h->cfg.worker_count;
+  if (sc->budget < 0) return ps_fail(h, PS_E_VALUE, "budget must be >= 0");
+  if (sc->grad_kind == PS_GRAD_SYNTHETIC && (!sc->synthetic || sc->n_synthetic < 1))
+    return ps_fail(h, PS_E_VALUE, "synthetic updates need a device buffer");
+  if (sc->grad_kind == PS_GRAD_BOWL && !sc->center) return ps_fail(h, PS_E_VALUE, "bowl needs a center");
+  if (!sc->compute_time && sc->budget > 0) return ps_fail(h, PS_E_VALUE, "compute_time missing");
+  ps_sim_buffers& b = h->sim;
+  const size_t budget = (size_t)sc->budget;
+  const size_t slots = (size_t)P * budget + 1;
+  const size_t ops = (size_t)P * (3 * budget + 2) + 8;
+  int rc;
+  size_t cap;
+  cap = b.ops_cap; if ((rc = grow(h, (Op**)&b.ops, &cap, ops))) return rc; b.ops_cap = cap;
+  cap = b.slots_cap;
+  if (cap < slots || !b.gcount) {
+    cudaFree(b.gcount); cudaFree(b.gbad);
+    b.gcount = nullptr; b.gbad = nullptr;
+    PS_CK(h, cudaMalloc(&b.gcount, slots * sizeof(unsigned)));
+    PS_CK(h, cudaMalloc(&b.gbad, slots * sizeof(unsigned)));
+    b.slots_cap = slots;
+  }
+  if (!b.produced) PS_CK(h, cudaMalloc(&b.produced, sizeof(unsigned long long)));
+  if (!b.out) PS_CK(h, cudaMalloc(&b.out, sizeof(SimOut)));
+  if (b.P != P || !b.rep) {
+    cudaFree(b.rep); cudaFree(b.gbuf);
+    b.rep = nullptr; b.gbuf = nullptr;
+    PS_CK(h, cudaMalloc(&b.rep, (size_t)P * 2 * h->dpad * sizeof(float)));
+    PS_CK(h, cudaMalloc(&b.gbuf, (size_t)P * h->dpad * sizeof(float)));
+    PS_CK(h, cudaMemsetAsync(b.rep, 0, (size_t)P * 2 * h->dpad * sizeof(float), h->stream));
+    b.P = P;
+  }
+  if (!b.center) {
+    PS_CK(h, cudaMalloc(&b.center, h->dpad * sizeof(float)));
+    PS_CK(h, cudaMemsetAsync(b.center, 0, h->dpad * sizeof(float), h->stream));
+  }
+  if (sc->grad_kind == PS_GRAD_BOWL) {
+    const size_t esz = sc->center_dtype == PS_F64 ? 8 : 4;
+    void* tmp = nullptr;
+    PS_CK(h, cudaMalloc(&tmp, h->d * esz));
+    PS_CK(h, cudaMemcpyAsync(tmp, sc->center, h->d * esz, cudaMemcpyHostToDevice, h->stream));
+    if (esz == 8)
+      k_to_f32<double><<<h->sm_count * 4, 256, 0, h->stream>>>((const double*)tmp, b.center, h->d, h->dpad);
+    else
+      k_to_f32<float><<<h->sm_count * 4, 256, 0, h->stream>>>((const float*)tmp, b.center, h->d, h->dpad);
+    PS_CK(h, cudaStreamSynchronize(h->stream));
+    cudaFree(tmp);
+  }
+  const size_t nct = (size_t)P * budget + 1;
+  cap = b.ctime_cap; if ((rc = grow(h, &b.ctime, &cap, nct))) return rc; b.ctime_cap = cap;
+  if (budget) PS_CK(h, cudaMemcpyAsync(b.ctime, sc->compute_time, (size_t)P * budget * sizeof(double),
+                                       cudaMemcpyHostToDevice, h->stream));
+  // trace rows: every event yields one row; events <= P*(5*budget+2)
+  const size_t trace_need = sc->record_trace ? (size_t)P * (5 * budget + 2) + 8 : 1;
+  cap = b.trace_cap; if ((rc = grow(h, &b.trace, &cap, trace_need))) return rc; b.trace_cap = cap;
+  const size_t loss_need = sc->loss_every > 0 ? (size_t)P * budget / sc->loss_every + 2 : 1;
+  cap = b.loss_cap; if ((rc = grow(h, &b.losses, &cap, loss_need))) return rc; b.loss_cap = cap;
+  PS_CK(h, cudaMemsetAsync(b.gcount, 0, slots * sizeof(unsigned), h->stream));
+  PS_CK(h, cudaMemsetAsync(b.gbad, 0, slots * sizeof(unsigned), h->stream));
+  PS_CK(h, cudaMemsetAsync(b.produced, 0, sizeof(unsigned long long), h->stream));
+  PS_CK(h, cudaMemsetAsync(b.out, 0, sizeof(SimOut), h->stream));
+  PS_CK(h, cudaMemsetAsync(b.losses, 0, loss_need * sizeof(double), h->stream));
+
+  int per_sm = 0;
+  PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim, kSimThreads, 0));
+  int grid = sc->data_ctas > 0 ? sc->data_ctas + 1 : h->sm_count;
+  if (grid > per_sm * h->sm_count) grid = per_sm * h->sm_count;
+  if (grid < 1) return ps_fail(h, PS_E_CUDA, "k_sim cannot be resident");
+
+  SimArgs a{};
+  a.P = P;
+  a.budget = sc->budget;
+  a.grad_kind = sc->grad_kind;
+  a.n_synth = sc->n_synthetic > 0 ? sc->n_synthetic : 1;
+  a.loss_every = sc->loss_every;
+  a.record_trace = sc->record_trace;
+  a.nv = h->nv;
+  a.dpad = h->dpad;
+  a.max_events = sc->max_events;
+  a.trace_cap = (long long)trace_need;
+  a.loss_cap = (long long)loss_need;
+  a.ops_cap = (long long)ops;
+  a.comm_delay = sc->comm_delay;
+  a.lr = (float)h->cfg.learning_rate;
+  a.W = h->w[h->cur];
+  a.rep = b.rep;
+  a.gbuf = b.gbuf;
+  a.center = b.center;
+  a.synth = sc->synthetic;
+  a.ctime = b.ctime;
+  a.ops = (Op*)b.ops;
+  a.produced = b.produced;
+  a.gcount = b.gcount;
+  a.gbad = b.gbad;
+  a.trace = b.trace;
+  a.losses = b.losses;
+  a.ctrl = h->ctrl;
+  a.out = (SimOut*)b.out;
+  a.n_data_warps = (unsigned)(grid * (kSimThreads / 32) - 1);
+  a.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  a.base_version = h->hctrl->gate.version;
+  b.last_base_version = a.base_version;
+  void* args[] = {&a};
+  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  PS_CK(h, cudaLaunchCooperativeKernel((const void*)k_sim, dim3(grid), dim3(kSimThreads), args, 0,
+                                       h->stream));
+  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
+  k_sim_finish<<<1, 1, 0, h->stream>>>(h->ctrl, (SimOut*)b.out);
+  PS_CK(h, cudaGetLastError());
+  SimOut o{};
+  PS_CK(h, cudaMemcpyAsync(&o, b.out, sizeof(SimOut), cudaMemcpyDeviceToHost, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->last_ms = ms;
+  PS_CK(h, cudaMemcpy(h->hctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  h->cur = h->hctrl->cur;
+  res->events = o.events;
+  res->pushes = o.pushes;
+  res->applied = o.applied;
+  res->rejected = o.rejected;
+  res->trace_rows = o.trace_rows < a.trace_cap ? o.trace_rows : a.trace_cap;
+  res->loss_samples = sc->loss_every > 0 ? o.applied / sc->loss_every : 0;
+  res->unfinished = o.unfinished;
+  res->status = o.status;
+  res->diverged_worker = o.diverged_worker;
+  res->device_ms = ms;
+  b.last_trace_rows = res->trace_rows;
+  b.last_loss_samples = res->loss_samples < a.loss_cap ? res->loss_samples : a.loss_cap;
+  b.last_loss_every = sc->loss_every;
+  if (o.status == PS_E_TIMEOUT) return ps_fail(h, PS_E_TIMEOUT, "device watchdog fired in ps_sim_run");
+  if (o.status == PS_E_DIVERGED)
+    return ps_fail(h, PS_E_DIVERGED, "weights went non-finite on worker " + std::to_string(o.diverged_worker));
+  if (o.status == PS_E_BUDGET)
+    return ps_fail(h, PS_E_BUDGET, "event budget " + std::to_string(sc->max_events) + " exceeded");
+  if (o.status == PS_E_PROTOCOL) return ps_fail(h, PS_E_PROTOCOL, "protocol violation in device run");
+  if (o.unfinished) {
+    res->status = PS_E_DEADLOCK;
+    return ps_fail(h, PS_E_DEADLOCK, "simulation deadlocked");
+  }
+  return PS_OK;
+}
+
+int ps_sim_trace(ps_server* h, ps_trace_row* rows, int64_t cap, int64_t* n) {
+  DevGuard guard(h->dev);
+  const int64_t m = h->sim.last_trace_rows < cap ? h->sim.last_trace_rows : cap;
+  *n = h->sim.last_trace_rows;
+  if (m > 0) PS_CK(h, cudaMemcpy(rows, h->sim.trace, m * sizeof(ps_trace_row), cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, int64_t* n) {
+  DevGuard guard(h->dev);
+  const int64_t m = h->sim.last_loss_samples < cap ? h->sim.last_loss_samples : cap;
+  *n = h->sim.last_loss_samples;
+  if (m > 0) PS_CK(h, cudaMemcpy(losses, h->sim.losses, m * sizeof(double), cudaMemcpyDeviceToHost));
+  const int64_t le = h->sim.last_loss_every;
+  for (int64_t i = 0; i < m; ++i) versions[i] = (h->sim.last_base_version / le + i + 1) * le;
+  return PS_OK;
+}
+
+}  // extern "C"

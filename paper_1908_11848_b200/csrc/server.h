@@ -1,0 +1,51 @@
+// server.h -- host-side state of one single-GPU parameter server handle.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <string>
+#include "common.cuh"
+
+struct ps_sim_buffers {
+  size_t ops_cap = 0, slots_cap = 0, trace_cap = 0, loss_cap = 0, ctime_cap = 0;
+  int P = 0;
+  void* ops = nullptr;                 // Op[ops_cap]
+  unsigned long long* produced = nullptr;
+  unsigned* gcount = nullptr;          // [slots_cap]
+  unsigned* gbad = nullptr;            // [slots_cap]
+  float* rep = nullptr;                // [P][2][dpad] worker replicas
+  float* gbuf = nullptr;               // [P][dpad] worker gradients
+  float* center = nullptr;             // [dpad]
+  double* ctime = nullptr;             // [P][budget]
+  ps_trace_row* trace = nullptr;
+  double* losses = nullptr;
+  void* out = nullptr;                 // SimOut
+  int64_t last_trace_rows = 0, last_loss_samples = 0, last_loss_every = 0, last_base_version = 0;
+};
+
+struct ps_server {
+  ps_config cfg{};
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int64_t d = 0, nv = 0, dpad = 0;     // elements, float4 count, padded length
+  float* w[2] = {nullptr, nullptr};    // double-buffered fp32 weights (device)
+  dssp::Ctrl* ctrl = nullptr;          // device control block
+  dssp::Ctrl* hctrl = nullptr;         // pinned host mirror
+  int cur = 0;                         // host mirror of ctrl->cur
+  void* stage = nullptr;               // device staging for host-side gradients
+  void* hstage = nullptr;              // pinned host staging
+  size_t stage_bytes = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  int sm_count = 148;
+  std::string err;
+  ps_sim_buffers sim;
+};
+
+int ps_fail(ps_server* h, int code, const std::string& msg);
+int ps_cuda_fail(ps_server* h, cudaError_t e, const char* what);
+
+#define PS_CK(h, call)                                          \
+  do {                                                          \
+    cudaError_t _e = (call);                                    \
+    if (_e != cudaSuccess) return ps_cuda_fail((h), _e, #call); \
+  } while (0)

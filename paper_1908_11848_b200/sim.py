@@ -1,0 +1,121 @@
+"""Device-resident simulated runs: the reference simulator's schedule with the
+server hot path (pull, update, apply, gate) executed by one persistent kernel.
+
+``run_device_simulation(config)`` is the drop-in counterpart of
+``stalesync.simnet.run_simulation`` (simnet.py:211-218) for the server side
+of a run: same (time, seq) event order, same push aggregation, same trace
+(byte-identical once rendered with :func:`trace.format_trace`). Worker
+compute is replaced by an on-device update generator -- the quadratic bowl
+model (engine.py:46-60, g = w_local - c, closed loop) or resident synthetic
+N(0,1) buffers -- because the reference's numpy models are outside the hot
+path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .config import bowl_center, compute_time_table, initial_weights_f64, push_budget
+from .engine import Engine, raise_for
+from .errors import DeadlockError
+from .trace import rows_to_entries
+
+
+@dataclass
+class DeviceRunReport:
+    entries: list
+    events: int
+    pushes: int
+    applied: int
+    rejected: int
+    device_ms: float
+    version: int
+    loss_curve: list = field(default_factory=list)
+    final_weights: np.ndarray | None = None
+
+    @property
+    def updates_per_s(self) -> float:
+        return self.applied / (self.device_ms * 1e-3) if self.device_ms > 0 else 0.0
+
+
+class DeviceSimulation:
+    """Owns one engine and runs simulated schedules on it."""
+
+    def __init__(self, config, dimension=None, grad="bowl", device: int = 0, engine=None):
+        self.config = config
+        self.dimension = int(dimension if dimension is not None else config.dimension)
+        self.grad = grad
+        self.device = device
+        self.engine = engine or Engine(
+            config.paradigm, config.worker_count, config.staleness.s_lower,
+            config.staleness.r_max, config.learning_rate, self.dimension,
+            w0=initial_weights_f64(config, self.dimension), device=device)
+        self.budget = push_budget(config)
+        self.ctime = np.ascontiguousarray(compute_time_table(config, self.budget))
+        self._center = None
+        self._synthetic = None
+        self._synth_count = 0
+        if grad == "bowl":
+            self._center = np.ascontiguousarray(bowl_center(config, self.dimension))
+        elif grad != "synthetic":
+            raise ValueError("grad must be 'bowl' or 'synthetic'")
+
+    def set_synthetic(self, tensor, count):
+        """Resident updates: a CUDA fp32 tensor [P, count, round_up(d, 4)]."""
+        self._synthetic = tensor
+        self._synth_count = int(count)
+
+    def run(self, record_trace=True, loss_every=None, max_events=0, data_ctas=0,
+            read_weights=True):
+        sc = _lib.PSSimConfig()
+        sc.budget = self.budget
+        sc.grad_kind = _lib.GRAD_BOWL if self.grad == "bowl" else _lib.GRAD_SYNTHETIC
+        le = self.config.loss_every if loss_every is None else loss_every
+        sc.loss_every = int(le) if self.grad == "bowl" else 0
+        sc.n_synthetic = self._synth_count
+        sc.comm_delay = float(self.config.timing_model.comm_delay)
+        sc.compute_time = self.ctime.ctypes.data
+        if self._center is not None:
+            sc.center = self._center.ctypes.data
+            sc.center_dtype = _lib.F64
+        sc.record_trace = 1 if record_trace else 0
+        if self._synthetic is not None:
+            sc.synthetic = self._synthetic.data_ptr()
+        sc.max_events = int(max_events or 0)
+        sc.data_ctas = int(data_ctas)
+        res = _lib.PSSimResult()
+        lib = self.engine.lib
+        rc = lib.ps_sim_run(self.engine.handle, ctypes.byref(sc), ctypes.byref(res))
+        if rc == _lib.E_DEADLOCK:
+            raise DeadlockError([q for q in range(self.config.worker_count)
+                                 if (res.unfinished >> q) & 1])
+        raise_for(rc, self.engine.error())
+        entries = []
+        if record_trace:
+            n = res.trace_rows
+            rows = (_lib.PSTraceRow * max(n, 1))()
+            got = ctypes.c_int64(0)
+            self.engine.check(lib.ps_sim_trace(self.engine.handle, rows, n, ctypes.byref(got)))
+            entries = rows_to_entries(rows, n)
+        curve = []
+        if sc.loss_every > 0 and res.loss_samples > 0:
+            m = res.loss_samples
+            vs = (ctypes.c_int64 * m)()
+            ls = (ctypes.c_double * m)()
+            got = ctypes.c_int64(0)
+            self.engine.check(lib.ps_sim_losses(self.engine.handle, vs, ls, m, ctypes.byref(got)))
+            curve = [(int(vs[i]), float(ls[i])) for i in range(m)]
+        self.engine.refresh()
+        weights = self.engine.read()[0] if read_weights else None
+        return DeviceRunReport(entries=entries, events=res.events, pushes=res.pushes,
+                               applied=res.applied, rejected=res.rejected,
+                               device_ms=res.device_ms, version=int(self.engine.state.version),
+                               loss_curve=curve, final_weights=weights)
+
+
+def run_device_simulation(config, grad="bowl", device: int = 0, **kw):
+    return DeviceSimulation(config, grad=grad, device=device).run(**kw)
