@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark of the parameter-server hot path (push-apply, pull, DSSP gate).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+
+N=1 (default) measures BASELINE.json configs[1] ("C2"): a ResNet-20-sized
+server (d = 272,474 fp32) with P = 4 workers on the heterogeneous gtx-mix
+schedule (simnet.py:34-69; 2 fast + 2 workers 2.2x slower), one "step" being
+one complete simulated run of 250 iterations per worker (1,000 server
+updates: pull -> update -> push-apply -> gate decision) executed by the
+device-resident run loop. Updates are synthetic N(0,1) fp32 vectors resident
+in HBM (2 per worker), lr = 0.05. The headline paradigm is DSSP(3, 12); BSP,
+SSP(3) and ASP are reported beside it.
+
+N>1 (torchrun, one process per GPU) measures configs[2] ("C3"): a
+ResNet-50-sized server (d = 23,528,522 fp32) sharded by contiguous range
+across the N GPUs, one worker per GPU, homogeneous workers; each step every
+worker pushes its update to every shard owner over NVLink P2P, the owners
+apply all N updates in ticket order, the replicated device gate decides, and
+every worker pulls the full weights back over NVLink.
+
+The line also carries:
+  e2e          the same metric through the reference-facing API
+               (ParameterServer drop-in, host buffers, H2D/D2H per call);
+  roofline     the dominant kernel's achieved bytes/s vs the measured peak;
+  cpu_baseline the reference algorithm (oracle/ port, fp64 numpy, 1 core) on
+               a bounded sample of the same call sequence;
+  sweep        push-apply / pull kernels at 1 MB .. 1 GB (configs[4]).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback
+NVLINK_GBS = 770.0          # B200_PROFILING.md measured peer copy per direction
+C2_DIM = 272_474            # ResNet-20 (CIFAR-10) parameter count
+C3_DIM = 23_528_522         # ResNet-50 (torchvision layout, 10 classes)
+METRIC = "PS push+pull updates/sec (HBM/NVLink GB/s); iters/sec per paradigm at 1/2/4/8 B200"
+PARADIGMS = (("dssp", 3, 12), ("ssp", 3, 0), ("bsp", 0, 0), ("asp", 0, 0))
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                return
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 5 + i and s[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def c2_config(paradigm, s_lower, r_max):
+    import paper_1908_11848_b200 as ps
+    return ps.validate_config(ps.make_config(
+        paradigm=paradigm, worker_count=4, s_lower=s_lower, r_max=r_max,
+        timing_preset="gtx-mix", compute_base=1.0, comm_delay=0.05, model_kind="tiny_mlp",
+        dimension=3072, dataset_size=4000, batch_size=16, learning_rate=0.05, epochs=4, seed=0))
+
+
+def synthetic_host(P, K, d):
+    """N(0,1) fp32 updates from PCG64(seed*1000 + worker) per SURVEY.md 8(d)."""
+    out = np.zeros((P, K, (d + 3) // 4 * 4), dtype=np.float32)
+    for p in range(P):
+        rng = np.random.Generator(np.random.PCG64(0 * 1000 + p))
+        for k in range(K):
+            out[p, k, :d] = rng.standard_normal(d, dtype=np.float32)
+    return out
+
+
+def flush_l2(torch, buf):
+    buf.add_(1.0)  # 256 MiB write: larger than the 126 MB L2
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle port of the reference algorithm
+# ---------------------------------------------------------------------------
+
+def reference_sample(calls, synth, d, paradigm, s_lower, r_max, lr, max_updates):
+    """Time the reference algorithm (oracle.RefPortServer: fp64 numpy apply
+    with the reference's temporaries and frozen copies, Python gate) on the
+    first `max_updates` applies of the call sequence. Returns (updates, s)."""
+    import oracle
+    w0 = oracle.initial_weights_f64(0, d)
+    srv = oracle.RefPortServer(paradigm, synth.shape[0], s_lower, r_max, lr, w0)
+    g64 = [[np.array(synth[p, k, :d], dtype=np.float64) for k in range(synth.shape[1])]
+           for p in range(synth.shape[0])]
+    for row in g64:
+        for g in row:
+            g.flags.writeable = False
+    pushes = {}
+    updates = 0
+    t0 = time.perf_counter()
+    for call in calls:
+        if call[0] == "apply":
+            k = pushes.get(call[1], 0)
+            pushes[call[1]] = k + 1
+            srv.apply_gradient(g64[call[1]][k % len(g64[call[1]])])
+            updates += 1
+        elif call[0] == "decide":
+            srv.decide_push(call[1], call[2])
+        elif call[0] == "pull":
+            srv.handle_pull(call[1])
+        if updates >= max_updates and call[0] == "decide":
+            break
+    return updates, time.perf_counter() - t0
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import paper_1908_11848_b200 as ps
+    # the call sequence of the C2 schedule is fixed by the reference
+    # simulator semantics; replay it with the same synthetic updates
+    cfg = c2_config("dssp", 3, 12)
+    calls, _ = reference_calls("dssp")
+    synth = synthetic_host(4, 2, C2_DIM)
+    n_updates = sum(1 for c in calls if c[0] == "apply")
+    per_step = min(n_updates, 250)
+    for _ in range(args.warmup):
+        reference_sample(calls, synth, C2_DIM, "dssp", 3, 12, cfg.learning_rate, per_step)
+    times, ups = [], 0
+    for _ in range(args.steps):
+        u, s = reference_sample(calls, synth, C2_DIM, "dssp", 3, 12, cfg.learning_rate, per_step)
+        times.append(s)
+        ups += u
+    total = sum(times)
+    value = ups / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 call sequence (DSSP(3,12), P=4, gtx-mix), d=272474; "
+                               f"each step = the first {per_step} updates"},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": "port",
+                         "sample": f"{per_step} updates x {args.steps} steps of the C2 call sequence"},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def reference_calls(paradigm="dssp"):
+    """The C2 server-call sequence and trace recorded from the reference
+    simulator itself (tests/golden/c2_schedule.json.gz, made by
+    tests/golden/make_golden.py)."""
+    import oracle
+    for run in oracle.load_golden("c2_schedule.json.gz")["runs"]:
+        if run["name"] == f"c2_{paradigm}":
+            calls = [tuple(c[:2]) if c[0] != "decide" else ("decide", c[1], c[2])
+                     for c in run["calls"] if c[0] in ("pull", "apply", "decide")]
+            return calls, run["trace"]
+    raise KeyError(paradigm)
+
+
+# ---------------------------------------------------------------------------
+# engine arm, N = 1
+# ---------------------------------------------------------------------------
+
+def apply_sweep(torch, ps, hbm_peak):
+    """configs[4]: push-apply (12 B/param) and pull (8 B/param) kernels from
+    1 MB to 1 GB of fp32 parameters; L2 flushed before every timed launch."""
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    out = []
+    for mb in (1, 4, 16, 64, 256, 1024):
+        d = mb * (1 << 20) // 4
+        eng = ps.engine.Engine("asp", 1, 0, 0, 0.05, d, device=0)
+        g = torch.randn(d, device="cuda", dtype=torch.float32)
+        dst = torch.empty(d, device="cuda", dtype=torch.float32)
+        ap, pl = [], []
+        for it in range(8):
+            flush_l2(torch, flush)
+            torch.cuda.synchronize()
+            eng.apply(0, g)
+            if it >= 3:
+                ap.append(eng.last_kernel_ms())
+            flush_l2(torch, flush)
+            torch.cuda.synchronize()
+            eng.read(out=dst)
+            if it >= 3:
+                pl.append(eng.last_kernel_ms())
+        eng.close()
+        a_ms, p_ms = statistics.median(ap), statistics.median(pl)
+        out.append({"mbytes": mb, "d": d,
+                    "apply_ms": round(a_ms, 4), "apply_gbs": round(12 * d / a_ms / 1e6, 1),
+                    "apply_frac": round(12 * d / a_ms / 1e6 / hbm_peak, 3),
+                    "pull_ms": round(p_ms, 4), "pull_gbs": round(8 * d / p_ms / 1e6, 1),
+                    "pull_frac": round(8 * d / p_ms / 1e6 / hbm_peak, 3)})
+        del g, dst
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def e2e_drop_in(torch, ps, cfg, calls, synth_host, d):
+    """The same workload through the reference-facing API: ParameterServer
+    drop-in, gradients from pinned host memory (H2D per push), pulls into
+    pinned host memory (D2H per pull). Returns (updates/s, h2d, d2h bytes)."""
+    server = ps.ParameterServer(cfg, d)
+    P, K = synth_host.shape[0], synth_host.shape[1]
+    pinned = torch.from_numpy(np.ascontiguousarray(synth_host[:, :, :d])).pin_memory()
+    host_g = [[pinned[p, k].numpy() for k in range(K)] for p in range(P)]
+    pull_buf = torch.empty(d, dtype=torch.float32).pin_memory().numpy()
+    grads = {}
+    pushes = {}
+
+    def replay():
+        h2d = d2h = updates = 0
+        for call in calls:
+            if call[0] == "pull":
+                server.handle_pull(call[1], out=pull_buf)
+                d2h += 4 * d
+            elif call[0] == "apply":
+                p = call[1]
+                k = pushes.get(p, 0)
+                pushes[p] = k + 1
+                server.apply_gradient(ps.GradientVector(host_g[p][k % K], p, k))
+                h2d += 4 * d
+                updates += 1
+            else:
+                server.decide_push(call[1], call[2])
+        return updates, h2d, d2h
+
+    # warm-up pass on a fresh gate, then the timed pass on another fresh one
+    replay()
+    server = ps.ParameterServer(cfg, d)
+    pushes.clear()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    updates, h2d, d2h = replay()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    return updates / dt, h2d, d2h, updates
+
+
+def bench_single(args):
+    import torch
+    import paper_1908_11848_b200 as ps
+
+    hbm_peak, peak_kind = peaks()
+    d = C2_DIM
+    P, K = 4, 2
+    synth_host = synthetic_host(P, K, d)
+    synth = torch.from_numpy(synth_host).cuda()
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    per_paradigm = {}
+    sims = {}
+    for name, s, r in PARADIGMS:
+        cfg = c2_config(name, s, r)
+        sim = ps.DeviceSimulation(cfg, dimension=d, grad="synthetic")
+        sim.set_synthetic(synth, K)
+        sims[name] = (cfg, sim)
+        for _ in range(args.warmup):
+            sim.run(read_weights=False, reset_gate=True)
+    sampler = ClockSampler(0)
+    reports = {}
+    with sampler:
+        for name, s, r in PARADIGMS:
+            cfg, sim = sims[name]
+            times, applied, iters = [], 0, 0
+            rep = None
+            for _ in range(args.steps):
+                flush_l2(torch, flush)
+                torch.cuda.synchronize()
+                rep = sim.run(read_weights=False, reset_gate=True)
+                times.append(rep.device_ms)
+                applied += rep.applied
+                iters += rep.pushes
+            reports[name] = rep
+            total_ms = sum(times)
+            per_paradigm[name] = {
+                "updates_per_s": applied / (total_ms * 1e-3),
+                "iters_per_s": iters / (total_ms * 1e-3),
+                "ms_per_step": total_ms / args.steps,
+                "defers_per_step": sum(1 for e in rep.entries
+                                       if e.kind == "push_arrive" and e.decision == "defer"),
+                "virtual_duration_s": max(e.time for e in rep.entries),
+            }
+    head = per_paradigm["dssp"]
+    cfg, sim = sims["dssp"]
+    rep = reports["dssp"]
+    # roofline of the dominant kernel (k_sim): algorithmic bytes per launch =
+    # updates x 12 B/param (push-apply) + pulls x 8 B/param (read w, write replica)
+    pulls = sum(1 for e in rep.entries if e.kind == "pull_arrive")
+    alg_bytes = rep.applied * 12 * d + pulls * 8 * d
+    achieved = alg_bytes / (head["ms_per_step"] * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k_sim_dram_bytes.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    # parity inside the bench: every paradigm's device trace must equal the
+    # reference simulator's trace of the same schedule, byte for byte
+    parity = {}
+    for name, _, _ in PARADIGMS:
+        want_calls, want_trace = reference_calls(name)
+        parity[name] = ps.format_trace(reports[name].entries) == want_trace
+    calls, _ = reference_calls("dssp")
+    # e2e through the reference-facing API
+    e2e_value, h2d, d2h, e2e_updates = e2e_drop_in(torch, ps, cfg, calls, synth_host, d)
+    # cpu baseline: the oracle port of the reference on a bounded sample
+    cpu_updates, cpu_s = reference_sample(calls, synth_host, d, "dssp", 3, 12, cfg.learning_rate,
+                                          max_updates=args.cpu_updates)
+    sweep = apply_sweep(torch, ps, hbm_peak) if not args.no_sweep else None
+    clocks = sampler.summary()
+    line = {
+        "metric": METRIC,
+        "value": head["updates_per_s"],
+        "unit": "updates/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "C2 (BASELINE configs[1]): ResNet-20-sized server d=272474 fp32, "
+                               "P=4 workers, gtx-mix schedule, DSSP(3,12); step = one device-resident "
+                               "run of 250 iterations/worker (1000 updates + pulls + gate decisions)",
+                   "d": d, "workers": P, "paradigm": "dssp", "s_lower": 3, "r_max": 12,
+                   "updates_per_step": rep.applied, "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": "single GPU"},
+        "per_paradigm": per_paradigm,
+        "parity": {"trace_identical_to_reference": parity},
+        "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "api": "ParameterServer drop-in, pinned host buffers",
+                "updates_per_step": e2e_updates},
+        "gpu_launches": 2 * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_sim (device run loop)",
+                     "bytes_model": "12 B/param per update + 8 B/param per pull"},
+        "cpu_baseline": {"value": cpu_updates / cpu_s, "unit": "updates/s", "cores": 1,
+                         "kind": "port",
+                         "sample": f"first {cpu_updates} updates of the same C2 call sequence, "
+                                   "oracle.RefPortServer (fp64 numpy + Python gate)",
+                         "host_cpus": os.cpu_count()},
+        "sweep": sweep,
+        "clocks": clocks,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=("engine", "reference"))
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--cpu-updates", type=int, default=3000)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_1908_11848_b200 import sharded
+        return sharded.bench_main(args, METRIC)
+    return bench_single(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

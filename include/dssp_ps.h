@@ -139,10 +139,10 @@ typedef struct ps_sim_config {
   const void* center;          /* host [d] bowl center (PS_GRAD_BOWL) */
   int32_t center_dtype;
   int32_t record_trace;        /* 1: keep TraceEntry rows */
-  const float* synthetic;      /* device [P][n_synthetic][d] (PS_GRAD_SYNTHETIC) */
+  const float* synthetic;      /* device [P][n_synthetic][round_up(d,4)] (PS_GRAD_SYNTHETIC) */
   int64_t max_events;          /* 0: unbounded */
   int32_t data_ctas;           /* 0: one per SM minus the control CTA */
-  int32_t threads;             /* 0: default */
+  int32_t reset_gate;          /* 1: zero the gate tables first (a fresh run) */
 } ps_sim_config;
 
 typedef struct ps_sim_result {
@@ -175,6 +175,39 @@ int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, 
 
 /* Per-kernel device time of the last ps_* call that launched work, in ms. */
 int ps_last_kernel_ms(ps_server* h, double* ms);
+
+/* ------------------------------------------------------------------------
+ * Sharded server: G GPUs, one process (rank) per GPU, one worker per rank.
+ * Shard r owns [r*S, min(d,(r+1)*S)), S = ceil(d/G) rounded up to 4. Ranks
+ * exchange the opaque blobs of ps_shard_ipc_handles (any host transport --
+ * the Python side uses torch.distributed.all_gather_object) and call
+ * ps_shard_connect; afterwards every step moves data only over NVLink P2P
+ * and synchronizes only through device flags (no collective, no host).
+ * Replaces the same reference interfaces as the single-GPU server, for the
+ * sharded layout of SURVEY.md section 8(e).
+ * ---------------------------------------------------------------------- */
+typedef struct ps_shard_server ps_shard_server;
+
+int ps_shard_range(int64_t d, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
+/* w0: full-length initial weights; w0_flags bit 0 = device pointer, bit 1 = fp64. */
+int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const void* w0,
+                    int64_t w0_flags, ps_shard_server** out);
+void ps_shard_destroy(ps_shard_server* h);
+const char* ps_shard_last_error(const ps_shard_server* h);
+int ps_shard_ipc_handles(ps_shard_server* h, void* out, int64_t cap); /* returns blob size */
+int ps_shard_connect(ps_shard_server* h, const void* blobs, int64_t len);
+/* The worker's update buffer (device, fp32, padded_len >= d): push source. */
+int ps_shard_update_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len);
+/* Run `steps` push groups (tickets t0..t0+steps-1, one push per rank each,
+ * applied in rank order then decided in rank order at virtual time now[i]),
+ * each followed by this rank's pull into dst (device fp32, >= round_up(d,4)
+ * floats; NULL = internal replica). Blocks until done; *ms = device time. */
+int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, void* dst,
+                 double* ms);
+int ps_shard_read_shard(ps_shard_server* h, void* dst_host, int64_t* n);
+int ps_shard_read_replica(ps_shard_server* h, void* dst_host);
+int ps_shard_get_state(ps_shard_server* h, ps_gate_state* out);
+int ps_shard_trace(ps_shard_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus
 }

@@ -54,7 +54,7 @@ class PSSimConfig(ctypes.Structure):
                 ("center", ctypes.c_void_p), ("center_dtype", ctypes.c_int32),
                 ("record_trace", ctypes.c_int32), ("synthetic", ctypes.c_void_p),
                 ("max_events", ctypes.c_int64), ("data_ctas", ctypes.c_int32),
-                ("threads", ctypes.c_int32)]
+                ("reset_gate", ctypes.c_int32)]
 
 
 class PSSimResult(ctypes.Structure):
@@ -103,12 +103,13 @@ SIGNATURES = {
     "ps_shard_connect": (ctypes.c_int, [_P, _P, _I64]),
     "ps_shard_destroy": (None, [_P]),
     "ps_shard_last_error": (ctypes.c_char_p, [_P]),
-    "ps_shard_step": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _I64, _PD]),
+    "ps_shard_update_buffer": (ctypes.c_int, [_P, ctypes.POINTER(_P), _PI64]),
+    "ps_shard_run": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _PD]),
     "ps_shard_read_shard": (ctypes.c_int, [_P, _P, _PI64]),
+    "ps_shard_read_replica": (ctypes.c_int, [_P, _P]),
     "ps_shard_get_state": (ctypes.c_int, [_P, ctypes.POINTER(PSGateState)]),
     "ps_shard_trace": (ctypes.c_int, [_P, ctypes.POINTER(PSTraceRow), _I64, _PI64]),
     "ps_shard_range": (ctypes.c_int, [_I64, _I32, _I32, _PI64, _PI64]),
-    "ps_shard_bench": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _PD]),
 }
 
 _lib = None

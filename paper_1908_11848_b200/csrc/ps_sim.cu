@@ -55,7 +55,7 @@ struct SimOut {
 };
 
 struct SimArgs {
-  int P, budget, grad_kind, n_synth, loss_every, record_trace;
+  int P, budget, grad_kind, n_synth, loss_every, record_trace, reset_gate;
   long long nv, dpad, max_events, trace_cap, loss_cap, ops_cap;
   double comm_delay;
   float lr;
@@ -239,6 +239,13 @@ __device__ void control_warp(const SimArgs& a, CtlState& s) {
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
     s.gate = a.ctrl->gate;
+    if (a.reset_gate) {
+      for (int q = 0; q < kMaxP; ++q) {
+        s.gate.clocks[q] = 0; s.gate.latest[q] = 0.0; s.gate.previous[q] = 0.0;
+        s.gate.populated[q] = 0; s.gate.credits[q] = 0;
+      }
+      s.gate.deferred = 0ull;
+    }
     for (int q = 0; q < kMaxP; ++q) {
       s.ev_kind[q] = -1;
       s.iterations[q] = 0;
@@ -515,6 +522,7 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   a.n_synth = sc->n_synthetic > 0 ? sc->n_synthetic : 1;
   a.loss_every = sc->loss_every;
   a.record_trace = sc->record_trace;
+  a.reset_gate = sc->reset_gate;
   a.nv = h->nv;
   a.dpad = h->dpad;
   a.max_events = sc->max_events;

@@ -1,0 +1,284 @@
+"""The sharded parameter server: one process per GPU (torchrun), contiguous-range
+shards, push/pull over NVLink P2P, replicated device gate.
+
+torch.distributed is plumbing only: it exchanges the CUDA-IPC blobs once at
+start-up (all_gather_object), broadcasts the initial weights once over NCCL
+(the north star's only collective) and takes the max of the per-rank device
+times for the benchmark. Every step after that is three kernels per rank
+that talk to their peers through mapped device memory (csrc/ps_shard.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import time
+
+import numpy as np
+
+from . import _lib
+from .config import initial_weights_f64, make_config, validate_config
+from .engine import raise_for
+from .trace import rows_to_entries
+
+BLOB_BYTES = 512
+
+
+def shard_range(d, world, rank):
+    lib = _lib.load(require_gpu=False)
+    lo, hi = ctypes.c_int64(0), ctypes.c_int64(0)
+    lib.ps_shard_range(int(d), int(world), int(rank), ctypes.byref(lo), ctypes.byref(hi))
+    return lo.value, hi.value
+
+
+def homogeneous_push_times(compute_base, comm_delay, steps):
+    """Push instants of the homogeneous schedule, accumulated with the same
+    sequence of additions simnet.py performs (PULL_ARRIVE at comm, PULL_RETURN
+    +comm, COMPUTE_DONE +compute, PUSH_ARRIVE +comm, then GRANT_DELIVER +comm,
+    PULL_ARRIVE +comm, ...), so the gate sees bit-identical timestamps."""
+    at = comm_delay
+    at = at + comm_delay
+    at = at + compute_base
+    at = at + comm_delay
+    out = [at]
+    for _ in range(steps - 1):
+        at = at + comm_delay
+        at = at + comm_delay
+        at = at + comm_delay
+        at = at + compute_base
+        at = at + comm_delay
+        out.append(at)
+    return out
+
+
+def exchange_blobs(mine: bytes):
+    """All-gather every rank's IPC blob, ordered by rank (host plumbing)."""
+    import torch.distributed as dist
+    everyone = [None] * dist.get_world_size()
+    dist.all_gather_object(everyone, mine)
+    return everyone
+
+
+def max_over_ranks(value: float) -> float:
+    """Max of a per-rank scalar (device times are reported as max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class _CudaArray:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3}
+
+
+class ShardedServer:
+    """Rank-local handle of the G-GPU server. All ranks construct it
+    collectively (it all-gathers the IPC blobs)."""
+
+    def __init__(self, config, dimension, rank, world, device, w0_device=None, w0_host=None):
+        import torch
+        import torch.distributed as dist
+        self.lib = _lib.load()
+        self.config = config
+        self.dimension = int(dimension)
+        self.rank, self.world, self.device = int(rank), int(world), int(device)
+        cfg = _lib.PSConfig()
+        cfg.paradigm = _lib.PARADIGMS[config.paradigm]
+        cfg.worker_count = int(config.worker_count)
+        cfg.s_lower = int(config.staleness.s_lower)
+        cfg.r_max = int(config.staleness.r_max)
+        cfg.learning_rate = float(config.learning_rate)
+        cfg.dimension = self.dimension
+        cfg.device = self.device
+        self._h = ctypes.c_void_p()
+        if w0_device is not None:
+            ptr, flags = w0_device.data_ptr(), 1 | (2 if w0_device.dtype == torch.float64 else 0)
+        elif w0_host is not None:
+            w0_host = np.ascontiguousarray(w0_host)
+            ptr, flags = w0_host.ctypes.data, (2 if w0_host.dtype == np.float64 else 0)
+        else:
+            ptr, flags = None, 0
+        rc = self.lib.ps_shard_create(ctypes.byref(cfg), self.world, self.rank, ptr, flags,
+                                      ctypes.byref(self._h))
+        if rc:
+            raise_for(rc, self.lib.ps_shard_last_error(None).decode())
+        blob = (ctypes.c_char * BLOB_BYTES)()
+        n = self.lib.ps_shard_ipc_handles(self._h, blob, BLOB_BYTES)
+        if n <= 0:
+            self._check(n)
+        joined = b"".join(exchange_blobs(bytes(blob)[:n]))
+        self._check(self.lib.ps_shard_connect(self._h, joined, len(joined)))
+        p = ctypes.c_void_p()
+        padded = ctypes.c_int64(0)
+        self.lib.ps_shard_update_buffer(self._h, ctypes.byref(p), ctypes.byref(padded))
+        self.update = torch.as_tensor(_CudaArray(p.value, padded.value), device=f"cuda:{self.device}")
+        self.lo, self.hi = shard_range(self.dimension, self.world, self.rank)
+        self.ticket = 1
+
+    def _check(self, rc):
+        raise_for(rc, self.lib.ps_shard_last_error(self._h).decode())
+
+    def close(self):
+        if self._h and self._h.value:
+            self.lib.ps_shard_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def run(self, now_times, dst=None):
+        """Enqueue len(now_times) push groups (+ this rank's pulls); returns
+        the device time in ms. dst: CUDA fp32 tensor with >= round_up(d,4)
+        elements, or None for the internal replica."""
+        now = np.ascontiguousarray(now_times, dtype=np.float64)
+        ms = ctypes.c_double(0)
+        rc = self.lib.ps_shard_run(self._h, self.ticket, len(now), now.ctypes.data,
+                                   dst.data_ptr() if dst is not None else None, ctypes.byref(ms))
+        self._check(rc)
+        self.ticket += len(now)
+        return ms.value
+
+    def read_shard(self):
+        out = np.empty(max(self.hi - self.lo, 1), dtype=np.float32)
+        n = ctypes.c_int64(0)
+        self._check(self.lib.ps_shard_read_shard(self._h, out.ctypes.data, ctypes.byref(n)))
+        return out[:n.value]
+
+    def read_replica(self):
+        out = np.empty(self.dimension, dtype=np.float32)
+        self._check(self.lib.ps_shard_read_replica(self._h, out.ctypes.data))
+        return out
+
+    def state(self):
+        st = _lib.PSGateState()
+        self._check(self.lib.ps_shard_get_state(self._h, ctypes.byref(st)))
+        return st
+
+    def trace(self):
+        n = ctypes.c_int64(0)
+        self._check(self.lib.ps_shard_trace(self._h, None, 0, ctypes.byref(n)))
+        rows = (_lib.PSTraceRow * max(n.value, 1))()
+        got = ctypes.c_int64(0)
+        self._check(self.lib.ps_shard_trace(self._h, rows, n.value, ctypes.byref(got)))
+        return rows_to_entries(rows, n.value)
+
+
+# ---------------------------------------------------------------------------
+# benchmark at N > 1 (bench.py delegates here under torchrun)
+# ---------------------------------------------------------------------------
+
+C3_DIM = 23_528_522
+PARADIGMS = (("dssp", 3, 12), ("ssp", 3, 0), ("bsp", 0, 0), ("asp", 0, 0))
+
+
+def c3_config(paradigm, s_lower, r_max, world):
+    return validate_config(make_config(
+        paradigm=paradigm, worker_count=world, s_lower=s_lower, r_max=r_max,
+        timing_preset="homogeneous", compute_base=1.0, comm_delay=0.05,
+        learning_rate=0.05, seed=0, dimension=C3_DIM, batch_size=1, dataset_size=world))
+
+
+def bench_main(args, metric):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    d = C3_DIM
+    # initial weights: rank 0 draws them (server.py:24-26) and NCCL-broadcasts
+    w0 = torch.empty(d, dtype=torch.float32, device="cuda")
+    if rank == 0:
+        w0.copy_(torch.from_numpy(initial_weights_f64(c3_config("dssp", 3, 12, world), d)
+                                  .astype(np.float32)))
+    dist.broadcast(w0, 0)
+    steps, warm = args.steps, args.warmup
+    times = homogeneous_push_times(1.0, 0.05, warm + steps + 64)
+    S_lo, S_hi = shard_range(d, world, rank)
+    results = {}
+    sampler = None
+    if rank == 0:
+        from bench import ClockSampler
+        sampler = ClockSampler(local)
+        sampler.__enter__()
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1000 * 0 + rank)
+    for name, s, r in PARADIGMS:
+        cfg = c3_config(name, s, r, world)
+        srv = ShardedServer(cfg, d, rank, world, local, w0_device=w0)
+        srv.update[:d].normal_(generator=gen)
+        srv.run(times[:warm])
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms = srv.run(times[warm:warm + steps])
+        ms_max = max_over_ranks(ms)
+        entries = srv.trace()
+        decisions = [e.decision for e in entries]
+        results[name] = {"updates_per_s": steps * world / (ms_max * 1e-3),
+                         "iters_per_s": steps * world / (ms_max * 1e-3),
+                         "ms_per_step": ms_max / steps,
+                         "defers": sum(1 for x in decisions if x == "defer")}
+        dist.barrier()
+        if name == "dssp":
+            # e2e: the same step with the worker's update arriving from pinned
+            # host memory (H2D) and the pulled weights leaving to pinned host
+            # memory (D2H) inside the timed region
+            host_upd = srv.update[:d].cpu().pin_memory()
+            host_out = torch.empty(d, dtype=torch.float32).pin_memory()
+            rep = torch.empty((d + 3) // 4 * 4, dtype=torch.float32, device="cuda")
+            e2e_steps = max(3, min(steps, 10))
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            base = warm + steps
+            for i in range(e2e_steps):
+                srv.update[:d].copy_(host_upd, non_blocking=True)
+                torch.cuda.synchronize()
+                srv.run(times[base + i:base + i + 1], dst=rep)
+                host_out.copy_(rep[:d])
+            torch.cuda.synchronize()
+            e2e_s = time.perf_counter() - t0
+            results["_e2e"] = {"value": e2e_steps * world / max_over_ranks(e2e_s), "unit": "updates/s",
+                               "h2d_bytes_per_step": 4 * d, "d2h_bytes_per_step": 4 * d,
+                               "api": "ShardedServer.run with pinned-host update in, replica out"}
+        torch.cuda.synchronize()
+        dist.barrier()  # no peer may still be reading this rank's memory
+        srv.close()
+    if sampler is not None:
+        sampler.__exit__(None, None, None)
+    if rank == 0:
+        head = results["dssp"]
+        S = S_hi - S_lo
+        nv_bytes = 2 * (world - 1) * S * 4          # push slices in + pull shards in, per GPU
+        achieved = nv_bytes / (head["ms_per_step"] * 1e-3) / 1e9
+        line = {
+            "metric": metric, "value": head["updates_per_s"], "unit": "updates/s",
+            "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "C3 (BASELINE configs[2]): ResNet-50-sized server d=23528522 fp32 "
+                                   f"sharded {world} ways, {world} homogeneous workers (one per GPU), "
+                                   "DSSP(3,12); step = one push group (every worker pushes, owners "
+                                   "apply in ticket order, gate decides) + every worker's pull",
+                       "d": d, "workers": world, "parallelism": f"sharded server x{world}, P2P NVLink",
+                       "l2": "per-GPU working set > L2 (94 MB update + 94 MB replica + shard)"},
+            "per_paradigm": {k: v for k, v in results.items() if not k.startswith("_")},
+            "e2e": results["_e2e"],
+            "gpu_launches": 3 * steps,
+            "roofline": {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s",
+                         "frac": achieved / 770.0, "traffic": None,
+                         "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                         "kernel": "k_shard_apply + k_shard_pull (whole step)",
+                         "bytes_model": "2*(G-1)*S*4 B received over NVLink per GPU per step"},
+            "cpu_baseline": None,
+            "clocks": sampler.summary() if sampler else None,
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

@@ -70,7 +70,7 @@ class DeviceSimulation:
         self._synth_count = int(count)
 
     def run(self, record_trace=True, loss_every=None, max_events=0, data_ctas=0,
-            read_weights=True):
+            read_weights=True, reset_gate=False):
         sc = _lib.PSSimConfig()
         sc.budget = self.budget
         sc.grad_kind = _lib.GRAD_BOWL if self.grad == "bowl" else _lib.GRAD_SYNTHETIC
@@ -87,6 +87,7 @@ class DeviceSimulation:
             sc.synthetic = self._synthetic.data_ptr()
         sc.max_events = int(max_events or 0)
         sc.data_ctas = int(data_ctas)
+        sc.reset_gate = 1 if reset_gate else 0
         res = _lib.PSSimResult()
         lib = self.engine.lib
         rc = lib.ps_sim_run(self.engine.handle, ctypes.byref(sc), ctypes.byref(res))
@@ -119,3 +120,29 @@ class DeviceSimulation:
 
 def run_device_simulation(config, grad="bowl", device: int = 0, **kw):
     return DeviceSimulation(config, grad=grad, device=device).run(**kw)
+
+
+def calls_from_trace(entries):
+    """The server-call sequence a host driver makes for this trace, in the
+    reference's order (simnet.py:127-201): ("pull", w) at PULL_ARRIVE, and for
+    every same-instant push group all ("apply", w) first, then each
+    ("decide", w, t). Consecutive push_arrive rows at one instant are one
+    group (the loop records a group's decisions back to back)."""
+    calls = []
+    i, n = 0, len(entries)
+    while i < n:
+        e = entries[i]
+        if e.kind == "pull_arrive":
+            calls.append(("pull", e.worker))
+            i += 1
+        elif e.kind == "push_arrive":
+            j = i
+            while j < n and entries[j].kind == "push_arrive" and entries[j].time == e.time:
+                j += 1
+            group = entries[i:j]
+            calls.extend(("apply", g.worker) for g in group)
+            calls.extend(("decide", g.worker, g.time) for g in group)
+            i = j
+        else:
+            i += 1
+    return calls

@@ -1,0 +1,73 @@
+"""One rank of the multi-GPU parity check (launched by tests/test_gpu_sharded.py
+under torchrun). Replays reference homogeneous schedules (tests/golden) on
+the sharded server and writes this rank's verdict as JSON."""
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_1908_11848_b200 as ps  # noqa: E402
+from paper_1908_11848_b200.sharded import ShardedServer  # noqa: E402
+
+
+def main(out_dir):
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    verdict = {"rank": rank, "checks": []}
+    runs = [r for r in oracle.load_golden("sim_corpus.json.gz")["runs"]
+            if r["config"].get("timing_preset") == "homogeneous"
+            and r["normalized"]["worker_count"] == world]
+    for d in (5, 100_003):
+        for run in runs:
+            cfg = ps.validate_config(ps.make_config(**run["config"]))
+            rows = [line.split("\t") for line in run["trace"].splitlines()]
+            pushes = [r for r in rows if r[2] == "push_arrive"]
+            times = sorted({float(r[0]) for r in pushes})
+            w0 = oracle.initial_weights_f64(cfg.seed, d)
+            srv = ShardedServer(cfg, d, rank, world, local, w0_host=w0)
+            g = oracle.synthetic_update(0, rank, 0, d)
+            srv.update[:d].copy_(torch.from_numpy(g))
+            torch.cuda.synchronize()
+            dist.barrier()
+            srv.run(times)
+            got = [e.render().split("\t") for e in srv.trace()]
+            want = [[r[0], r[1], r[2], r[3], r[4]] for r in pushes]
+            # oracle: every group applies its updates in the reference's ticket
+            # order (the order of the group's push rows in the reference trace)
+            w = w0.astype(np.float32)
+            gs = [oracle.synthetic_update(0, p, 0, d) for p in range(world)]
+            for r in pushes:
+                w = oracle.apply_f32(w, gs[int(r[1])], cfg.learning_rate)
+            shard = srv.read_shard()
+            rep = srv.read_replica()
+            ok_trace = got == want
+            ok_shard = bool(np.array_equal(shard.view(np.uint32), w[srv.lo:srv.hi].view(np.uint32)))
+            ok_rep = bool(np.array_equal(rep.view(np.uint32), w.view(np.uint32)))
+            st = srv.state()
+            diff = [(a, b) for a, b in zip(got, want) if a != b][:3]
+            verdict["checks"].append({"run": run["name"], "d": d, "trace": ok_trace,
+                                      "diff": diff, "n_got": len(got), "n_want": len(want),
+                                      "shard": ok_shard, "replica": ok_rep,
+                                      "version": int(st.version), "steps": len(times)})
+            torch.cuda.synchronize()
+            dist.barrier()
+            srv.close()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
+        json.dump(verdict, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

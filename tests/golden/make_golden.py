@@ -380,8 +380,27 @@ def apply_vectors():
         "initial_weights_16": init})
 
 
+def c2_schedule():
+    """bench.py's N=1 workload (BASELINE configs[1]): P=4, gtx-mix, 250
+    iterations per worker, for each paradigm. The call log fixes the server
+    call sequence the reference arm replays and the trace the device run loop
+    must reproduce."""
+    out = []
+    for paradigm, s, r in (("dssp", 3, 12), ("ssp", 3, 0), ("bsp", 0, 0), ("asp", 0, 0)):
+        flat = dict(paradigm=paradigm, worker_count=4, s_lower=s, r_max=r,
+                    timing_preset="gtx-mix", compute_base=1.0, comm_delay=0.05,
+                    model_kind="tiny_mlp", dimension=3072, dataset_size=4000, batch_size=16,
+                    learning_rate=0.05, epochs=4, seed=0, loss_every=100000)
+        rec = _run_recorded(flat, False)
+        rec["name"] = f"c2_{paradigm}"
+        out.append(rec)
+    _dump("c2_schedule.json.gz", {"runs": out}, gz=True)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["controller", "gate", "sim", "apply"]
+    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2"]
+    if "c2" in which:
+        c2_schedule()
     if "controller" in which:
         controller_tables()
     if "gate" in which:

@@ -1,0 +1,41 @@
+"""Multi-GPU parity of the sharded server (needs >= 2 GPUs; run with
+`gpurun --gpus 2`). Each rank replays the reference's homogeneous schedules:
+decisions byte-identical to the reference trace, every shard and every
+pulled replica bit-exact against the fp32 oracle."""
+
+import glob
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_parity(tmp_path, world):
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(29400 + world), os.path.join(ROOT, "tests", "_sharded_worker.py"),
+           str(tmp_path)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    files = sorted(glob.glob(str(tmp_path / "rank*.json")))
+    assert len(files) == world
+    for f in files:
+        v = json.load(open(f))
+        assert v["checks"], v
+        for c in v["checks"]:
+            assert c["trace"] and c["shard"] and c["replica"], c
+            assert c["version"] == c["steps"] * world
