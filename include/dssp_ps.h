@@ -156,6 +156,8 @@ typedef struct ps_sim_result {
   int32_t status;              /* enum ps_status */
   int32_t diverged_worker;
   double device_ms;            /* kernel time, CUDA events on the launch stream */
+  double control_ms;           /* control warp: start -> last op emitted (%globaltimer) */
+  double data_ms;              /* start -> last data warp done (%globaltimer) */
 } ps_sim_result;
 
 typedef struct ps_trace_row {

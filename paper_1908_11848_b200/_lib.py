@@ -62,7 +62,8 @@ class PSSimResult(ctypes.Structure):
                 ("applied", ctypes.c_int64), ("rejected", ctypes.c_int64),
                 ("trace_rows", ctypes.c_int64), ("loss_samples", ctypes.c_int64),
                 ("unfinished", ctypes.c_uint64), ("status", ctypes.c_int32),
-                ("diverged_worker", ctypes.c_int32), ("device_ms", ctypes.c_double)]
+                ("diverged_worker", ctypes.c_int32), ("device_ms", ctypes.c_double),
+                ("control_ms", ctypes.c_double), ("data_ms", ctypes.c_double)]
 
 
 class PSTraceRow(ctypes.Structure):

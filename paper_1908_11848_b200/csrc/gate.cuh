@@ -43,13 +43,23 @@ __device__ __forceinline__ int controller_grid(double lp, double pp, double ls, 
   const double is = interval_of(ls, ps);
   double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
   int best_r = 0x7fffffff;
+  // slow(k) = ls + (k+1)*is is non-decreasing in k (is > 0 and round-to-
+  // nearest is monotone), so |slow(k) - cand| is minimized at the last k with
+  // slow(k) <= cand or the one after it: a binary search finds that pair and
+  // the per-r minimum equals the brute-force min over all k bit for bit.
   for (int r = lane; r <= r_max; r += 32) {
     const double cand = __dadd_rn(lp, __dmul_rn((double)r, ip));
+    int lo = -1, hi = r_max + 1;  // slow(lo) <= cand < slow(hi), virtual ends
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__dadd_rn(ls, __dmul_rn((double)(mid + 1), is)) <= cand) lo = mid;
+      else hi = mid;
+    }
     double m = __longlong_as_double(0x7ff0000000000000ll);
-    for (int k = 0; k <= r_max; ++k) {
-      const double slow = __dadd_rn(ls, __dmul_rn((double)(k + 1), is));
-      const double gap = fabs(__dsub_rn(slow, cand));
-      if (gap < m) m = gap;
+    if (lo >= 0) m = fabs(__dsub_rn(__dadd_rn(ls, __dmul_rn((double)(lo + 1), is)), cand));
+    if (hi <= r_max) {
+      const double gh = fabs(__dsub_rn(__dadd_rn(ls, __dmul_rn((double)(hi + 1), is)), cand));
+      if (gh < m) m = gh;
     }
     if (m < best) { best = m; best_r = r; }
   }

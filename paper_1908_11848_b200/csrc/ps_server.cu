@@ -363,7 +363,7 @@ void ps_destroy(ps_server* h) {
   cudaFree(h->stage);
   cudaFreeHost(h->hstage);
   ps_sim_buffers& s = h->sim;
-  cudaFree(s.ops); cudaFree(s.produced); cudaFree(s.gcount); cudaFree(s.gbad);
+  cudaFree(s.ops); cudaFree(s.gcount);
   cudaFree(s.rep); cudaFree(s.gbuf); cudaFree(s.center); cudaFree(s.ctime);
   cudaFree(s.trace); cudaFree(s.losses); cudaFree(s.out);
   if (h->ev0) cudaEventDestroy(h->ev0);

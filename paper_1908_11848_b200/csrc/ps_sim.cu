@@ -33,6 +33,7 @@
 
 #include "common.cuh"
 #include "gate.cuh"
+#include "ctl_regs.cuh"
 #include "server.h"
 
 using namespace dssp;
@@ -41,17 +42,38 @@ namespace {
 
 enum OpType : int32_t { OP_PULL = 1, OP_GRAD = 2, OP_APPLY = 3, OP_END = 4 };
 
-struct Op {
-  int32_t type;
-  int32_t worker;
-  int32_t buf;    // PULL: staging replica; GRAD: active replica (bowl) / synthetic index; APPLY: synthetic index
-  int32_t slot;   // update id (GRAD/APPLY)
-};
+// One op is a single 64-bit word, written once per run with one relaxed store
+// and self-validating through its run tag, so the control warp never fences
+// and the data warps never read a separate "produced" counter:
+//   [0,16) run tag   [16,19) type   [19,26) worker   [26,34) buf   [34,64) slot
+// buf -- PULL: staging replica; GRAD: active replica (bowl) or synthetic index;
+//        APPLY: synthetic index.  slot -- update id (GRAD/APPLY).
+typedef unsigned long long Op;
+__host__ __device__ __forceinline__ Op op_pack(unsigned tag, int type, int w, int buf, long long slot) {
+  return (unsigned long long)(tag & 0xffffu) | ((unsigned long long)(type & 7) << 16) |
+         ((unsigned long long)(w & 127) << 19) | ((unsigned long long)(buf & 255) << 26) |
+         ((unsigned long long)slot << 34);
+}
+__device__ __forceinline__ int op_type(Op o) { return (int)((o >> 16) & 7); }
+__device__ __forceinline__ int op_worker(Op o) { return (int)((o >> 19) & 127); }
+__device__ __forceinline__ int op_buf(Op o) { return (int)((o >> 26) & 255); }
+__device__ __forceinline__ long long op_slot(Op o) { return (long long)(o >> 34); }
+__device__ __forceinline__ unsigned op_tag(Op o) { return (unsigned)(o & 0xffffu); }
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 struct SimOut {
   long long events, pushes, trace_rows, applied, rejected;
   unsigned long long unfinished;
   int status, diverged_worker;
+  unsigned long long t_start, t_control_done, t_data_done;  // %globaltimer ns
 };
 
 struct SimArgs {
@@ -66,9 +88,7 @@ struct SimArgs {
   const float* synth;
   const double* ctime;
   Op* ops;
-  unsigned long long* produced;
-  unsigned* gcount;
-  unsigned* gbad;
+  unsigned* gword;   // per update: data CTAs done (low 16 bits) | non-finite CTAs << 16
   ps_trace_row* trace;
   double* losses;
   Ctrl* ctrl;
@@ -76,10 +96,13 @@ struct SimArgs {
   unsigned n_data_warps;
   unsigned long long timeout_ns;
   long long base_version;
+  unsigned tag;
+  unsigned n_ctas;
 };
 
 constexpr int kSimThreads = 256;
 constexpr int kMaxP = PS_MAX_WORKERS;
+constexpr int kRegP = 8;  // control state in registers up to this many workers
 
 struct CtlState {
   ps_gate_state gate;
@@ -122,18 +145,9 @@ __device__ __forceinline__ void ctl_schedule(CtlState& s, double at, int kind, i
 }
 
 __device__ __forceinline__ void ctl_emit(const SimArgs& a, CtlState& s, int type, int w, int buf,
-                                         int slot) {
-  Op op;
-  op.type = type;
-  op.worker = w;
-  op.buf = buf;
-  op.slot = slot;
-  a.ops[s.n_ops] = op;
+                                         long long slot) {
+  st_relaxed_u64(a.ops + s.n_ops, op_pack(a.tag, type, w, buf, slot));
   s.n_ops += 1;
-}
-
-__device__ __forceinline__ void ctl_publish(const SimArgs& a, CtlState& s) {
-  st_release_u64(a.produced, (unsigned long long)s.n_ops);
 }
 
 // Lane 0 only. Advances the event loop until a decision is needed (returns 1,
@@ -214,7 +228,6 @@ __device__ int ctl_advance(const SimArgs& a, CtlState& s, int* p, double* now) {
       s.group_pos = 0;
       s.group_at = at;
     }
-    ctl_publish(a, s);
   }
 }
 
@@ -260,6 +273,7 @@ __device__ void control_warp(const SimArgs& a, CtlState& s) {
     s.status = PS_OK;
     for (int q = 0; q < a.P; ++q) ctl_schedule(s, a.comm_delay, PS_EV_PULL_ARRIVE, q);
   }
+  if (lane == 0) a.out->t_start = globaltimer_ns();
   __syncwarp();
   for (;;) {
     int cmd = 0, p = 0;
@@ -275,7 +289,7 @@ __device__ void control_warp(const SimArgs& a, CtlState& s) {
   }
   if (lane == 0) {
     ctl_emit(a, s, OP_END, 0, 0, 0);
-    ctl_publish(a, s);
+    a.out->t_control_done = globaltimer_ns();
     unsigned long long unfinished = 0;
     for (int q = 0; q < a.P; ++q)
       if (!s.finished[q]) unfinished |= 1ull << q;
@@ -292,39 +306,239 @@ __device__ void control_warp(const SimArgs& a, CtlState& s) {
   }
 }
 
-__device__ void data_warp(const SimArgs& a, unsigned dw) {
+// Register-resident control warp for P <= PM (see ctl_regs.cuh): all lanes run
+// the identical event loop; lane 0 alone writes trace rows and op words.
+template <int PM>
+__device__ void control_warp_regs(const SimArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const bool w0 = lane == 0;
+  const int P = a.P, budget = a.budget, nsyn = a.n_synth;
+  const bool bowl = a.grad_kind == PS_GRAD_BOWL;
+  const double comm = a.comm_delay;
+  const unsigned tag = a.tag;
+  Op* const ops = a.ops;
+  ps_trace_row* const trace = a.trace;
+  const long long trace_cap = a.record_trace ? a.trace_cap : 0;
+  RegGate<PM> g;
+  g.load(a.ctrl->gate, a.reset_gate != 0);
+  double ev_time[PM], nct[PM];
+  int ev_seq[PM], ev_kind[PM], iters[PM], active[PM], staged[PM], gslot[PM], sidx[PM];
+#pragma unroll
+  for (int q = 0; q < PM; ++q) {
+    ev_kind[q] = -1; iters[q] = 0; active[q] = 0; staged[q] = 0; gslot[q] = 0; sidx[q] = 0;
+    ev_time[q] = 0.0; ev_seq[q] = 0;
+    nct[q] = (q < P && budget > 0) ? a.ctime[(long long)q * budget] : 0.0;  // next compute draw
+  }
+  unsigned finished = 0;
+  int seq = 0, status = PS_OK;
+  long long processed = 0, n_ops = 0, n_trace = 0, pushes = 0, next_slot = 0;
+  auto emit = [&](int type, int w, int buf, long long slot) {
+    if (w0) st_relaxed_u64(ops + n_ops, op_pack(tag, type, w, buf, slot));
+    n_ops += 1;
+  };
+  auto trace_row = [&](double t, int w, int kind, int decision, unsigned long long released) {
+    if (w0 && n_trace < trace_cap) {
+      ps_trace_row r;
+      r.time = t; r.worker = w; r.kind = kind; r.count = rget<PM>(g.clocks, w);
+      r.decision = decision; r._pad = 0; r.released = released;
+      trace[n_trace] = r;
+    }
+    n_trace += 1;
+  };
+  auto schedule = [&](double at, int kind, int w) {
+#pragma unroll
+    for (int q = 0; q < PM; ++q)
+      if (q == w) { ev_time[q] = at; ev_seq[q] = seq; ev_kind[q] = kind; }
+    seq += 1;
+  };
+#pragma unroll
+  for (int q = 0; q < PM; ++q)
+    if (q < P) schedule(comm, PS_EV_PULL_ARRIVE, q);
+  if (w0) a.out->t_start = globaltimer_ns();
+  for (;;) {
+    // pop the (time, seq)-minimum event
+    int w = -1;
+    double bt = 0.0;
+    int bs = 0;
+#pragma unroll
+    for (int q = 0; q < PM; ++q) {
+      if (q < P && ev_kind[q] >= 0 &&
+          (w < 0 || ev_time[q] < bt || (ev_time[q] == bt && ev_seq[q] < bs))) {
+        w = q; bt = ev_time[q]; bs = ev_seq[q];
+      }
+    }
+    if (w < 0) break;
+    if (a.max_events > 0 && processed >= a.max_events) { status = PS_E_BUDGET; break; }
+    const double at = bt;
+    const int kind = rget<PM>(ev_kind, w);
+    rset<PM>(ev_kind, w, -1);
+    processed += 1;
+    if (kind == PS_EV_PULL_ARRIVE) {
+      const int st = 1 - rget<PM>(active, w);
+      emit(OP_PULL, w, st, 0);
+      rset<PM>(staged, w, st);
+      trace_row(at, w, kind, -1, 0);
+      schedule(at + comm, PS_EV_PULL_RETURN, w);
+    } else if (kind == PS_EV_PULL_RETURN) {
+      rset<PM>(active, w, rget<PM>(staged, w));  // adopt (simnet.py:156-165)
+      trace_row(at, w, kind, -1, 0);
+      if (rget<PM>(iters, w) < budget) schedule(at + rget<PM>(nct, w), PS_EV_COMPUTE_DONE, w);
+      else finished |= 1u << w;
+    } else if (kind == PS_EV_COMPUTE_DONE) {
+      const int it = rget<PM>(iters, w) + 1;
+      rset<PM>(iters, w, it);
+      if (it < budget) rset<PM>(nct, w, a.ctime[(long long)w * budget + it]);  // prefetch the next draw
+      const long long slot = next_slot++;
+      rset<PM>(gslot, w, (int)slot);
+      emit(OP_GRAD, w, bowl ? rget<PM>(active, w) : rget<PM>(sidx, w) % nsyn, slot);
+      trace_row(at, w, kind, -1, 0);
+      schedule(at + comm, PS_EV_PUSH_ARRIVE, w);
+    } else if (kind == PS_EV_GRANT_DELIVER) {
+      trace_row(at, w, kind, -1, 0);
+      schedule(at + comm, PS_EV_PULL_ARRIVE, w);
+    } else {
+      // PUSH_ARRIVE: every push queued at the same instant joins the group
+      // (simnet.py:167-182); the popped one first, the rest by seq.
+      unsigned rest = 0;
+#pragma unroll
+      for (int q = 0; q < PM; ++q)
+        if (q < P && ev_kind[q] == PS_EV_PUSH_ARRIVE && ev_time[q] == at) {
+          rest |= 1u << q;
+          ev_kind[q] = -1;
+        }
+      int order[PM];
+      int n = 1;
+      order[0] = w;
+#pragma unroll
+      for (int i = 1; i < PM; ++i) {
+        int m = -1, ms = 0;
+#pragma unroll
+        for (int q = 0; q < PM; ++q)
+          if (((rest >> q) & 1u) && (m < 0 || ev_seq[q] < ms)) { m = q; ms = ev_seq[q]; }
+        order[i] = m;
+        if (m >= 0) { rest &= ~(1u << m); n = i + 1; }
+      }
+#pragma unroll
+      for (int i = 0; i < PM; ++i) {
+        if (i < n) {
+          const int m = order[i];
+          const int si = rget<PM>(sidx, m);
+          emit(OP_APPLY, m, bowl ? 0 : si % nsyn, rget<PM>(gslot, m));
+          rset<PM>(sidx, m, si + 1);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < PM; ++i) {
+        if (i < n && status == PS_OK) {
+          const int m = order[i];
+          const GateResult r = g.on_push(m, at);
+          pushes += 1;
+          if (r.status != PS_OK) {
+            status = r.status;
+          } else {
+            trace_row(at, m, PS_EV_PUSH_ARRIVE, r.outcome, r.released);
+            if (r.outcome == 0) {
+              schedule(at + comm, PS_EV_GRANT_DELIVER, m);
+#pragma unroll
+              for (int q = 0; q < PM; ++q)
+                if ((r.released >> q) & 1ull) schedule(at + comm, PS_EV_GRANT_DELIVER, q);
+            }
+          }
+        }
+      }
+      if (status != PS_OK) break;
+    }
+  }
+  emit(OP_END, 0, 0, 0);
+  if (w0) {
+    a.out->t_control_done = globaltimer_ns();
+    unsigned long long unfinished = 0;
+    for (int q = 0; q < P; ++q)
+      if (!((finished >> q) & 1u)) unfinished |= 1ull << q;
+    ps_gate_state& dst = a.ctrl->gate;
+    if (a.reset_gate) {
+      for (int q = 0; q < kMaxP; ++q) {
+        dst.clocks[q] = 0; dst.latest[q] = 0.0; dst.previous[q] = 0.0;
+        dst.populated[q] = 0; dst.credits[q] = 0;
+      }
+    }
+    g.store(dst);
+    a.out->events = processed;
+    a.out->pushes = pushes;
+    a.out->trace_rows = n_trace;
+    a.out->unfinished = status == PS_OK ? unfinished : 0ull;
+    if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
+  }
+}
+
+constexpr int kRing = 256;  // per-CTA finiteness aggregation ring (> max warp skew in updates)
+
+// Loads of one worker's update slice; V float4 per lane, element u at lo + lane + 32u.
+template <int V>
+__device__ __forceinline__ void load_slice(float4 (&r)[V], const float4* src, long long lo, long long hi,
+                                           int lane) {
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const long long j = lo + lane + 32ll * u;
+    r[u] = j < hi ? ld_stream(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// Data warp with its weight slice held in registers for the whole run (V
+// float4 per lane); V == 0 is the general path that keeps it in HBM.
+template <int V>
+__device__ void data_warp(const SimArgs& a, unsigned dw, unsigned* s_ring, int warps_here) {
   const int lane = threadIdx.x & 31;
   const long long per = (a.nv + a.n_data_warps - 1) / a.n_data_warps;
-  const long long lo = (long long)dw * per;
+  const long long lo = (long long)dw * per < a.nv ? (long long)dw * per : a.nv;
   const long long hi = lo + per < a.nv ? lo + per : a.nv;
   float4* W = reinterpret_cast<float4*>(a.W);
   const float4* C = reinterpret_cast<const float4*>(a.center);
-  long long avail = 0, applied = 0, rejected = 0;
-  const unsigned long long t0 = globaltimer_ns();
-  for (long long i = 0;; ++i) {
-    if (i >= avail) {
-      unsigned long long v = 0;
-      if (lane == 0) {
-        for (;;) {
-          v = ld_acquire_u64(a.produced);
-          if ((long long)v > i) break;
-          if (globaltimer_ns() - t0 > a.timeout_ns) { v = 0; break; }
-          __nanosleep(64);
-        }
-      }
-      v = __shfl_sync(kFull, v, 0);
-      if ((long long)v <= i) {  // watchdog: never hang the GPU
-        if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
-        return;
-      }
-      avail = (long long)v;
+  float4 wr[V > 0 ? V : 1];
+  if constexpr (V > 0) {
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const long long j = lo + lane + 32ll * u;
+      wr[u] = j < hi ? W[j] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const int4 raw = __ldcg(reinterpret_cast<const int4*>(a.ops) + i);
-    const int type = raw.x, w = raw.y, buf = raw.z, slot = raw.w;
+  }
+  long long applied = 0, rejected = 0;
+  const unsigned long long t0 = globaltimer_ns();
+  long long base = 0;
+  int have = 0;
+  Op batch = 0;
+  for (long long i = 0;; ++i) {
+    if (i >= base + have) {
+      // fetch up to 32 published ops at once (one coalesced 256 B load)
+      base = i;
+      for (;;) {
+        const long long k = base + lane;
+        batch = k < a.ops_cap ? ld_relaxed_u64(a.ops + k) : 0ull;
+        const unsigned valid = __ballot_sync(kFull, op_tag(batch) == (a.tag & 0xffffu));
+        have = valid == kFull ? 32 : __ffs(~valid) - 1;
+        if (have > 0) break;
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
+          return;
+        }
+        __nanosleep(32);
+      }
+    }
+    const Op op = __shfl_sync(kFull, batch, (int)(i - base));
+    const int type = op_type(op), w = op_worker(op), buf = op_buf(op);
+    const long long slot = op_slot(op);
     if (type == OP_END) break;
     if (type == OP_PULL) {
       float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)w * 2 + buf) * a.dpad);
-      for (long long j = lo + lane; j < hi; j += 32) dst[j] = W[j];
+      if constexpr (V > 0) {
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          const long long j = lo + lane + 32ll * u;
+          if (j < hi) dst[j] = wr[u];
+        }
+      } else {
+        for (long long j = lo + lane; j < hi; j += 32) dst[j] = W[j];
+      }
     } else if (type == OP_GRAD) {
       bool bad = false;
       if (a.grad_kind == PS_GRAD_BOWL) {
@@ -340,40 +554,72 @@ __device__ void data_warp(const SimArgs& a, unsigned dw) {
       } else {
         const float4* src =
             reinterpret_cast<const float4*>(a.synth + ((long long)w * a.n_synth + buf) * a.dpad);
-        for (long long j = lo + lane; j < hi; j += 32) bad |= nonfinite4(ld_stream(src + j));
+        if constexpr (V > 0) {
+          float4 r[V];
+          load_slice<V>(r, src, lo, hi, lane);
+#pragma unroll
+          for (int u = 0; u < V; ++u) bad |= nonfinite4(r[u]);
+        } else {
+          for (long long j = lo + lane; j < hi; j += 32) bad |= nonfinite4(ld_stream(src + j));
+        }
       }
       const bool any_bad = __any_sync(kFull, bad);
       if (lane == 0) {
-        if (any_bad) atomicOr(&a.gbad[slot], 1u);
-        __threadfence();
-        atomicAdd(&a.gcount[slot], 1u);
+        // CTA-level aggregation: the last warp of this CTA to flag the update
+        // adds one count (and a non-finite mark) to its global word
+        const unsigned inc = 1u + (any_bad ? 0x10000u : 0u);
+        const unsigned old = atomicAdd(&s_ring[slot & (kRing - 1)], inc);
+        if ((old & 0xffffu) == (unsigned)warps_here - 1) {
+          atomicExch(&s_ring[slot & (kRing - 1)], 0u);
+          const unsigned badc = (old >> 16) + (any_bad ? 1u : 0u);
+          atomicAdd(&a.gword[slot], 1u + (badc ? 0x10000u : 0u));
+        }
       }
     } else if (type == OP_APPLY) {
-      unsigned bad = 0;
-      if (lane == 0) {
-        while (ld_acquire_u32(&a.gcount[slot]) < a.n_data_warps) {
-          if (globaltimer_ns() - t0 > a.timeout_ns) { bad = 2; break; }
-          __nanosleep(32);
-        }
-        if (!bad) bad = ld_relaxed_u32(&a.gbad[slot]);
-      }
-      bad = __shfl_sync(kFull, bad, 0);
-      if (bad == 2) {
-        if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
-        return;
-      }
-      if (bad) {
-        rejected += 1;
-        continue;
-      }
       const float4* g = a.grad_kind == PS_GRAD_BOWL
                             ? reinterpret_cast<const float4*>(a.gbuf + (long long)w * a.dpad)
                             : reinterpret_cast<const float4*>(a.synth + ((long long)w * a.n_synth + buf) * a.dpad);
+      float4 gr[V > 0 ? V : 1];
+      if constexpr (V > 0) {
+        if (a.grad_kind == PS_GRAD_BOWL) {
+#pragma unroll
+          for (int u = 0; u < V; ++u) {
+            const long long j = lo + lane + 32ll * u;
+            gr[u] = j < hi ? g[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        } else {
+          load_slice<V>(gr, g, lo, hi, lane);  // in flight while we wait for the verdict
+        }
+      }
+      unsigned v = 0;
+      if (lane == 0) {
+        while (((v = ld_relaxed_u32(&a.gword[slot])) & 0xffffu) < a.n_ctas) {
+          if (globaltimer_ns() - t0 > a.timeout_ns) { v = 0xffffffffu; break; }
+          __nanosleep(20);
+        }
+      }
+      v = __shfl_sync(kFull, v, 0);
+      if (v == 0xffffffffu) {
+        if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
+        return;
+      }
+      if (v >> 16) {
+        rejected += 1;
+        continue;
+      }
       bool dbad = false;
-      for (long long j = lo + lane; j < hi; j += 32) {
-        const float4 r = apply4(W[j], a.lr, g[j]);
-        dbad |= nonfinite4(r);
-        W[j] = r;
+      if constexpr (V > 0) {
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          wr[u] = apply4(wr[u], a.lr, gr[u]);
+          dbad |= nonfinite4(wr[u]);
+        }
+      } else {
+        for (long long j = lo + lane; j < hi; j += 32) {
+          const float4 r = apply4(W[j], a.lr, g[j]);
+          dbad |= nonfinite4(r);
+          W[j] = r;
+        }
       }
       applied += 1;
       if (__any_sync(kFull, dbad) && lane == 0) {
@@ -381,11 +627,24 @@ __device__ void data_warp(const SimArgs& a, unsigned dw) {
       }
       if (a.loss_every > 0 && (a.base_version + applied) % a.loss_every == 0) {
         double acc = 0.0;
-        for (long long j = lo + lane; j < hi; j += 32) {
-          const float4 x = W[j], c = C[j];
-          const double d0 = (double)x.x - (double)c.x, d1 = (double)x.y - (double)c.y;
-          const double d2 = (double)x.z - (double)c.z, d3 = (double)x.w - (double)c.w;
-          acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+        if constexpr (V > 0) {
+#pragma unroll
+          for (int u = 0; u < V; ++u) {
+            const long long j = lo + lane + 32ll * u;
+            if (j < hi) {
+              const float4 x = wr[u], c = C[j];
+              const double d0 = (double)x.x - (double)c.x, d1 = (double)x.y - (double)c.y;
+              const double d2 = (double)x.z - (double)c.z, d3 = (double)x.w - (double)c.w;
+              acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+            }
+          }
+        } else {
+          for (long long j = lo + lane; j < hi; j += 32) {
+            const float4 x = W[j], c = C[j];
+            const double d0 = (double)x.x - (double)c.x, d1 = (double)x.y - (double)c.y;
+            const double d2 = (double)x.z - (double)c.z, d3 = (double)x.w - (double)c.w;
+            acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+          }
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
@@ -395,19 +654,35 @@ __device__ void data_warp(const SimArgs& a, unsigned dw) {
       }
     }
   }
+  if constexpr (V > 0) {
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const long long j = lo + lane + 32ll * u;
+      if (j < hi) W[j] = wr[u];
+    }
+  }
+  if (lane == 0) atomicMax(&a.out->t_data_done, globaltimer_ns());
   if (dw == 0 && lane == 0) {
     a.out->applied = applied;
     a.out->rejected = rejected;
   }
 }
 
+// V: float4 per lane of register-resident weights (0 = in HBM);
+// PM: register-resident control tables for P <= PM workers (0 = shared memory).
+template <int V, int PM>
 __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   __shared__ CtlState s;
+  __shared__ unsigned s_ring[kRing];
+  for (int i = threadIdx.x; i < kRing; i += blockDim.x) s_ring[i] = 0;
+  __syncthreads();
   const unsigned gw = (blockIdx.x * kSimThreads + threadIdx.x) >> 5;
+  const int warps_here = blockIdx.x == 0 ? kSimThreads / 32 - 1 : kSimThreads / 32;
   if (gw == 0) {
-    control_warp(a, s);
+    if constexpr (PM > 0) control_warp_regs<PM>(a);
+    else control_warp(a, s);
   } else {
-    data_warp(a, gw - 1);
+    data_warp<V>(a, gw - 1, s_ring, warps_here);
   }
 }
 
@@ -459,16 +734,26 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   const size_t ops = (size_t)P * (3 * budget + 2) + 8;
   int rc;
   size_t cap;
-  cap = b.ops_cap; if ((rc = grow(h, (Op**)&b.ops, &cap, ops))) return rc; b.ops_cap = cap;
+  if (b.ops_cap < ops || !b.ops) {
+    cudaFree(b.ops);
+    b.ops = nullptr;
+    PS_CK(h, cudaMalloc(&b.ops, ops * sizeof(Op)));
+    PS_CK(h, cudaMemsetAsync(b.ops, 0, ops * sizeof(Op), h->stream));  // tag 0 = never valid
+    b.ops_cap = ops;
+    b.tag = 0;
+  }
+  b.tag = (b.tag + 1) & 0xffffu;
+  if (b.tag == 0) {  // tag space wrapped: clear stale words once
+    PS_CK(h, cudaMemsetAsync(b.ops, 0, b.ops_cap * sizeof(Op), h->stream));
+    b.tag = 1;
+  }
   cap = b.slots_cap;
   if (cap < slots || !b.gcount) {
-    cudaFree(b.gcount); cudaFree(b.gbad);
-    b.gcount = nullptr; b.gbad = nullptr;
+    cudaFree(b.gcount);
+    b.gcount = nullptr;
     PS_CK(h, cudaMalloc(&b.gcount, slots * sizeof(unsigned)));
-    PS_CK(h, cudaMalloc(&b.gbad, slots * sizeof(unsigned)));
     b.slots_cap = slots;
   }
-  if (!b.produced) PS_CK(h, cudaMalloc(&b.produced, sizeof(unsigned long long)));
   if (!b.out) PS_CK(h, cudaMalloc(&b.out, sizeof(SimOut)));
   if (b.P != P || !b.rep) {
     cudaFree(b.rep); cudaFree(b.gbuf);
@@ -504,14 +789,27 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   const size_t loss_need = sc->loss_every > 0 ? (size_t)P * budget / sc->loss_every + 2 : 1;
   cap = b.loss_cap; if ((rc = grow(h, &b.losses, &cap, loss_need))) return rc; b.loss_cap = cap;
   PS_CK(h, cudaMemsetAsync(b.gcount, 0, slots * sizeof(unsigned), h->stream));
-  PS_CK(h, cudaMemsetAsync(b.gbad, 0, slots * sizeof(unsigned), h->stream));
-  PS_CK(h, cudaMemsetAsync(b.produced, 0, sizeof(unsigned long long), h->stream));
   PS_CK(h, cudaMemsetAsync(b.out, 0, sizeof(SimOut), h->stream));
   PS_CK(h, cudaMemsetAsync(b.losses, 0, loss_need * sizeof(double), h->stream));
 
+  // one CTA per SM; the weight slice of every data warp lives in registers
+  // when it fits V float4 per lane (V in {1,2,4,8,16}), else in HBM (V = 0)
+  int grid = sc->data_ctas > 0 ? sc->data_ctas : h->sm_count;
+  const long long dwarps = (long long)grid * (kSimThreads / 32) - 1;
+  const long long per = (h->nv + dwarps - 1) / dwarps;
+  const long long need_v = (per + 31) / 32;
+  const int vi = need_v <= 1 ? 0 : need_v <= 2 ? 1 : need_v <= 4 ? 2 : need_v <= 8 ? 3 : need_v <= 16 ? 4 : 5;
+  const int pi = P <= 2 ? 0 : P <= 4 ? 1 : P <= kRegP ? 2 : 3;
+  static const void* const table[6][4] = {
+      {(const void*)k_sim<1, 2>, (const void*)k_sim<1, 4>, (const void*)k_sim<1, 8>, (const void*)k_sim<1, 0>},
+      {(const void*)k_sim<2, 2>, (const void*)k_sim<2, 4>, (const void*)k_sim<2, 8>, (const void*)k_sim<2, 0>},
+      {(const void*)k_sim<4, 2>, (const void*)k_sim<4, 4>, (const void*)k_sim<4, 8>, (const void*)k_sim<4, 0>},
+      {(const void*)k_sim<8, 2>, (const void*)k_sim<8, 4>, (const void*)k_sim<8, 8>, (const void*)k_sim<8, 0>},
+      {(const void*)k_sim<16, 2>, (const void*)k_sim<16, 4>, (const void*)k_sim<16, 8>, (const void*)k_sim<16, 0>},
+      {(const void*)k_sim<0, 2>, (const void*)k_sim<0, 4>, (const void*)k_sim<0, 8>, (const void*)k_sim<0, 0>}};
+  const void* kern = table[vi][pi];
   int per_sm = 0;
-  PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sim, kSimThreads, 0));
-  int grid = sc->data_ctas > 0 ? sc->data_ctas + 1 : h->sm_count;
+  PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimThreads, 0));
   if (grid > per_sm * h->sm_count) grid = per_sm * h->sm_count;
   if (grid < 1) return ps_fail(h, PS_E_CUDA, "k_sim cannot be resident");
 
@@ -538,9 +836,9 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   a.synth = sc->synthetic;
   a.ctime = b.ctime;
   a.ops = (Op*)b.ops;
-  a.produced = b.produced;
-  a.gcount = b.gcount;
-  a.gbad = b.gbad;
+  a.gword = b.gcount;
+  a.tag = b.tag;
+  a.n_ctas = (unsigned)grid;
   a.trace = b.trace;
   a.losses = b.losses;
   a.ctrl = h->ctrl;
@@ -551,8 +849,7 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   b.last_base_version = a.base_version;
   void* args[] = {&a};
   PS_CK(h, cudaEventRecord(h->ev0, h->stream));
-  PS_CK(h, cudaLaunchCooperativeKernel((const void*)k_sim, dim3(grid), dim3(kSimThreads), args, 0,
-                                       h->stream));
+  PS_CK(h, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSimThreads), args, 0, h->stream));
   PS_CK(h, cudaEventRecord(h->ev1, h->stream));
   k_sim_finish<<<1, 1, 0, h->stream>>>(h->ctrl, (SimOut*)b.out);
   PS_CK(h, cudaGetLastError());
@@ -574,6 +871,8 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   res->status = o.status;
   res->diverged_worker = o.diverged_worker;
   res->device_ms = ms;
+  res->control_ms = o.t_control_done > o.t_start ? (o.t_control_done - o.t_start) * 1e-6 : 0.0;
+  res->data_ms = o.t_data_done > o.t_start ? (o.t_data_done - o.t_start) * 1e-6 : 0.0;
   b.last_trace_rows = res->trace_rows;
   b.last_loss_samples = res->loss_samples < a.loss_cap ? res->loss_samples : a.loss_cap;
   b.last_loss_every = sc->loss_every;

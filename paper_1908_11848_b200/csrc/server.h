@@ -8,10 +8,9 @@
 struct ps_sim_buffers {
   size_t ops_cap = 0, slots_cap = 0, trace_cap = 0, loss_cap = 0, ctime_cap = 0;
   int P = 0;
-  void* ops = nullptr;                 // Op[ops_cap]
-  unsigned long long* produced = nullptr;
-  unsigned* gcount = nullptr;          // [slots_cap]
-  unsigned* gbad = nullptr;            // [slots_cap]
+  void* ops = nullptr;                 // Op[ops_cap] (tagged 64-bit words)
+  unsigned tag = 0;                    // run tag of the op words
+  unsigned* gcount = nullptr;          // [slots_cap] per-update finiteness words
   float* rep = nullptr;                // [P][2][dpad] worker replicas
   float* gbuf = nullptr;               // [P][dpad] worker gradients
   float* center = nullptr;             // [dpad]

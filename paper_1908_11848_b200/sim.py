@@ -36,6 +36,8 @@ class DeviceRunReport:
     version: int
     loss_curve: list = field(default_factory=list)
     final_weights: np.ndarray | None = None
+    control_ms: float = 0.0
+    data_ms: float = 0.0
 
     @property
     def updates_per_s(self) -> float:
@@ -115,7 +117,8 @@ class DeviceSimulation:
         return DeviceRunReport(entries=entries, events=res.events, pushes=res.pushes,
                                applied=res.applied, rejected=res.rejected,
                                device_ms=res.device_ms, version=int(self.engine.state.version),
-                               loss_curve=curve, final_weights=weights)
+                               loss_curve=curve, final_weights=weights,
+                               control_ms=res.control_ms, data_ms=res.data_ms)
 
 
 def run_device_simulation(config, grad="bowl", device: int = 0, **kw):
