@@ -227,6 +227,7 @@ def apply_sweep(torch, ps, hbm_peak):
     for mb in (1, 4, 16, 64, 256, 1024):
         d = mb * (1 << 20) // 4
         eng = ps.engine.Engine("asp", 1, 0, 0, 0.05, d, device=0)
+        eng.set_profiling(True)
         g = torch.randn(d, device="cuda", dtype=torch.float32)
         dst = torch.empty(d, device="cuda", dtype=torch.float32)
         ap, pl = [], []

@@ -175,8 +175,11 @@ int ps_sim_trace(ps_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
 /* Loss samples of the last run: (version, 0.5*||w - c||^2 in fp64). */
 int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, int64_t* n);
 
-/* Per-kernel device time of the last ps_* call that launched work, in ms. */
+/* Device time (CUDA events on the server stream) of the last launch, in ms:
+ * always for ps_sim_run, for the per-op calls only with profiling on (the
+ * events cost two API calls per op, so they are off on the hot path). */
 int ps_last_kernel_ms(ps_server* h, double* ms);
+int ps_set_profiling(ps_server* h, int32_t on);
 
 /* ------------------------------------------------------------------------
  * Sharded server: G GPUs, one process (rank) per GPU, one worker per rank.
@@ -210,6 +213,9 @@ int ps_shard_read_shard(ps_shard_server* h, void* dst_host, int64_t* n);
 int ps_shard_read_replica(ps_shard_server* h, void* dst_host);
 int ps_shard_get_state(ps_shard_server* h, ps_gate_state* out);
 int ps_shard_trace(ps_shard_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
+/* Diagnosis only: per-kernel event timing (ready / apply / pull, ms summed). */
+int ps_shard_set_profiling(ps_shard_server* h, int32_t on);
+int ps_shard_phase_ms(ps_shard_server* h, double* out3);
 
 #ifdef __cplusplus
 }

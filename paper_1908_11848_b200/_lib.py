@@ -98,6 +98,7 @@ SIGNATURES = {
     "ps_sim_trace": (ctypes.c_int, [_P, ctypes.POINTER(PSTraceRow), _I64, _PI64]),
     "ps_sim_losses": (ctypes.c_int, [_P, _PI64, _PD, _I64, _PI64]),
     "ps_last_kernel_ms": (ctypes.c_int, [_P, _PD]),
+    "ps_set_profiling": (ctypes.c_int, [_P, _I32]),
     "ps_shard_create": (ctypes.c_int, [ctypes.POINTER(PSConfig), _I32, _I32, _P, _I64,
                                        ctypes.POINTER(_P)]),
     "ps_shard_ipc_handles": (ctypes.c_int, [_P, _P, _I64]),
@@ -111,6 +112,8 @@ SIGNATURES = {
     "ps_shard_get_state": (ctypes.c_int, [_P, ctypes.POINTER(PSGateState)]),
     "ps_shard_trace": (ctypes.c_int, [_P, ctypes.POINTER(PSTraceRow), _I64, _PI64]),
     "ps_shard_range": (ctypes.c_int, [_I64, _I32, _I32, _PI64, _PI64]),
+    "ps_shard_set_profiling": (ctypes.c_int, [_P, _I32]),
+    "ps_shard_phase_ms": (ctypes.c_int, [_P, _PD]),
 }
 
 _lib = None

@@ -59,12 +59,21 @@ struct Vec4Load<double> {
   static __device__ __forceinline__ float one(const double* g, long long i) { return (float)g[i]; }
 };
 
+// Warp-collective copy of the control block into the host-mapped mirror, so
+// the host reads every op's result and the gate tables without a D2H copy.
+__device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* mirror) {
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(ctrl);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(mirror);
+  for (int i = threadIdx.x & 31; i < (int)(sizeof(Ctrl) / 8); i += 32) d[i] = s[i];
+}
+
 // One streaming pass w[cur^1] = w[cur] - lr*g with flag reduction; the last CTA
-// publishes the result and (fuse=1) runs the gate decision.
+// publishes the result and (fuse=1) runs the gate decision. g may live in
+// device memory or in pinned host memory (read over PCIe, zero-copy).
 template <typename G>
 __global__ void __launch_bounds__(kApplyThreads)
 k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g, long long n,
-        float lr, Ctrl* ctrl, int fuse, int worker, double now) {
+        float lr, Ctrl* ctrl, int fuse, int worker, double now, Ctrl* mirror) {
   const int cur = *reinterpret_cast<volatile int*>(&ctrl->cur);
   const float4* src = reinterpret_cast<const float4*>(cur ? w1 : w0);
   float4* dst = reinterpret_cast<float4*>(cur ? w0 : w1);
@@ -150,15 +159,19 @@ k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g,
       ctrl->released = r.released;
     }
   }
+  __syncwarp();
+  publish_ctrl(ctrl, mirror);
 }
 
-__global__ void k_decide(Ctrl* ctrl, int worker, double now) {
+__global__ void k_decide(Ctrl* ctrl, int worker, double now, Ctrl* mirror) {
   const GateResult r = gate_on_push(&ctrl->gate, worker, now);
   if (threadIdx.x == 0) {
     ctrl->status = r.status;
     ctrl->granted = (r.status == PS_OK && r.outcome == 0) ? 1 : 0;
     ctrl->released = r.released;
   }
+  __syncwarp();
+  publish_ctrl(ctrl, mirror);
 }
 
 template <typename T>
@@ -222,11 +235,40 @@ int ensure_stage(ps_server* h, size_t bytes) {
   return PS_OK;
 }
 
+// Full D2H refresh of the mirror (after launches that do not publish it).
 int sync_ctrl(ps_server* h) {
   PS_CK(h, cudaMemcpyAsync(h->hctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
   PS_CK(h, cudaStreamSynchronize(h->stream));
   h->cur = h->hctrl->cur;
   return PS_OK;
+}
+
+// Wait for an op whose kernel published the mirror itself.
+int finish_op(ps_server* h) {
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  h->cur = h->hctrl->cur;
+  if (h->profile) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    h->last_ms = ms;
+  }
+  return PS_OK;
+}
+
+int mark(ps_server* h, cudaEvent_t e) {
+  if (h->profile) PS_CK(h, cudaEventRecord(e, h->stream));
+  return PS_OK;
+}
+
+// Pinned (page-locked, UVA-mapped) host memory can be read and written by
+// kernels directly over PCIe; pageable memory has to be staged.
+bool pinned_host(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
 }
 
 struct DevGuard {
@@ -236,7 +278,9 @@ struct DevGuard {
 };
 
 // Launch the apply (optionally fused with the decision) on a device- or host-
-// resident update. Host updates go through pinned staging (one H2D copy).
+// resident update: device or pinned host memory is read in place (the kernel
+// streams a pinned host update over PCIe, no separate copy); pageable host
+// memory and misaligned device views go through staging.
 int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_device, int fuse,
                  double now) {
   if (g_dtype != PS_F32 && g_dtype != PS_F64) return ps_fail(h, PS_E_VALUE, "bad gradient dtype");
@@ -244,33 +288,28 @@ int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_
   const size_t esz = g_dtype == PS_F64 ? 8 : 4;
   const size_t bytes = (size_t)h->d * esz;
   const void* dg = g;
-  if (!g_on_device || !aligned16(g)) {
+  const bool direct = aligned16(g) && (g_on_device || pinned_host(g));
+  if (!direct) {
     int rc = ensure_stage(h, bytes);
     if (rc) return rc;
-    if (!g_on_device) {
-      PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, cudaMemcpyHostToDevice, h->stream));
-    } else {
-      PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, cudaMemcpyDeviceToDevice, h->stream));
-    }
+    PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, g_on_device ? cudaMemcpyDeviceToDevice
+                                                               : cudaMemcpyHostToDevice, h->stream));
     dg = h->stage;
   }
   const float lr = (float)h->cfg.learning_rate;
   const int grid = grid_for(h, h->nv);
-  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  int rc = mark(h, h->ev0);
+  if (rc) return rc;
   if (g_dtype == PS_F32)
     k_apply<float><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const float*)dg, h->d,
-                                                          lr, h->ctrl, fuse, worker, now);
+                                                          lr, h->ctrl, fuse, worker, now, h->hctrl_dev);
   else
     k_apply<double><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const double*)dg,
-                                                           h->d, lr, h->ctrl, fuse, worker, now);
+                                                           h->d, lr, h->ctrl, fuse, worker, now,
+                                                           h->hctrl_dev);
   PS_CK(h, cudaGetLastError());
-  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
-  int rc = sync_ctrl(h);
-  if (rc) return rc;
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
-  h->last_ms = ms;
-  return PS_OK;
+  if ((rc = mark(h, h->ev1))) return rc;
+  return finish_op(h);
 }
 
 }  // namespace
@@ -324,7 +363,10 @@ int ps_create(const ps_config* cfg, const void* w0_host, int32_t w0_dtype, ps_se
     if ((e = cudaMemsetAsync(h->w[b], 0, h->dpad * sizeof(float), h->stream))) return bail(e, "memset");
   }
   if ((e = cudaMalloc(&h->ctrl, sizeof(Ctrl)))) return bail(e, "cudaMalloc ctrl");
-  if ((e = cudaMallocHost(&h->hctrl, sizeof(Ctrl)))) return bail(e, "cudaMallocHost ctrl");
+  if ((e = cudaHostAlloc((void**)&h->hctrl, sizeof(Ctrl), cudaHostAllocMapped)))
+    return bail(e, "cudaHostAlloc ctrl mirror");
+  if ((e = cudaHostGetDevicePointer((void**)&h->hctrl_dev, h->hctrl, 0)))
+    return bail(e, "cudaHostGetDevicePointer");
   std::memset(h->hctrl, 0, sizeof(Ctrl));
   ps_gate_state& gs = h->hctrl->gate;
   gs.paradigm = cfg->paradigm;
@@ -388,15 +430,11 @@ int ps_apply(ps_server* h, int32_t worker, const void* g, int32_t g_dtype, int32
 
 int ps_decide(ps_server* h, int32_t worker, double now, int32_t* granted, uint64_t* released) {
   DevGuard guard(h->dev);
-  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
-  k_decide<<<1, 32, 0, h->stream>>>(h->ctrl, worker, now);
-  PS_CK(h, cudaGetLastError());
-  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
-  int rc = sync_ctrl(h);
+  int rc = mark(h, h->ev0);
   if (rc) return rc;
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
-  h->last_ms = ms;
+  k_decide<<<1, 32, 0, h->stream>>>(h->ctrl, worker, now, h->hctrl_dev);
+  PS_CK(h, cudaGetLastError());
+  if ((rc = mark(h, h->ev1)) || (rc = finish_op(h))) return rc;
   *granted = h->hctrl->granted;
   *released = h->hctrl->released;
   if (h->hctrl->status == PS_E_PROTOCOL)
@@ -439,8 +477,11 @@ int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_d
   const float* src = h->w[h->cur];
   const size_t esz = dst_dtype == PS_F64 ? 8 : 4;
   if (version) *version = h->hctrl->gate.version;
-  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
-  if (dst_on_device && aligned16(dst)) {
+  int rc = mark(h, h->ev0);
+  if (rc) return rc;
+  // device or pinned host destinations are written by the copy kernel itself
+  // (over PCIe for pinned host memory); pageable ones take a staged copy
+  if (aligned16(dst) && (dst_on_device || pinned_host(dst))) {
     const int grid = grid_for(h, h->nv);
     if (dst_dtype == PS_F32)
       k_copy_out<float><<<grid, 256, 0, h->stream>>>(src, (float*)dst, h->d);
@@ -450,17 +491,18 @@ int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_d
   } else if (dst_dtype == PS_F32) {
     PS_CK(h, cudaMemcpyAsync(dst, src, h->d * 4, cudaMemcpyDefault, h->stream));
   } else {
-    int rc = ensure_stage(h, h->d * esz);
-    if (rc) return rc;
+    if ((rc = ensure_stage(h, h->d * esz))) return rc;
     k_copy_out<double><<<grid_for(h, h->nv), 256, 0, h->stream>>>(src, (double*)h->stage, h->d);
     PS_CK(h, cudaGetLastError());
     PS_CK(h, cudaMemcpyAsync(dst, h->stage, h->d * esz, cudaMemcpyDefault, h->stream));
   }
-  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
+  if ((rc = mark(h, h->ev1))) return rc;
   PS_CK(h, cudaStreamSynchronize(h->stream));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
-  h->last_ms = ms;
+  if (h->profile) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    h->last_ms = ms;
+  }
   return PS_OK;
 }
 
@@ -492,6 +534,11 @@ int ps_set_state(ps_server* h, const ps_gate_state* in) {
 
 int ps_last_kernel_ms(ps_server* h, double* ms) {
   *ms = h->last_ms;
+  return PS_OK;
+}
+
+int ps_set_profiling(ps_server* h, int32_t on) {
+  h->profile = on ? 1 : 0;
   return PS_OK;
 }
 

@@ -8,31 +8,35 @@
 //
 // One step = one same-instant push group of all G workers (the homogeneous
 // schedule of simnet.py:167-201: apply every update in seq order, then decide
-// each), three kernels in stream order on every rank, with no host in the loop
+// each), two kernels in stream order on every rank, with no host in the loop
 // and no collective:
 //
-//   K1 k_shard_ready  worker r scans its update for non-finite values
-//                     (server.py:65-67 needs the whole vector's verdict before
-//                     any shard applies it) and release-stores
-//                     ready = (t<<1)|bad into every owner's flag array.
+//   K1 k_shard_push   (one thread) worker r's push: once every owner's slice
+//                     of its previous pull has landed, release-store
+//                     ready = t into every owner's flag array.
 //   K2 k_shard_apply  owner r waits for all G ready flags, then streams its
-//                     shard once: w = w - lr*g_p for p = 0..G-1 in ticket
-//                     order (skipping rejected updates), reading each g_p slice
-//                     straight from worker p's HBM over NVLink (P2P loads,
-//                     payload crosses once). Per-element order == global push
-//                     order, no atomics on weights. The last CTA publishes
-//                     applied = t to every worker and runs the replicated gate
-//                     (gate.cuh) for the G pushes -- every rank computes the same
-//                     decisions from the same inputs, so no gate traffic crosses
-//                     NVLink.
-//   K3 k_shard_pull   worker r waits for all G applied flags and gathers the
-//                     full weights (handle_pull, server.py:84-91) from the G
-//                     shards into its replica with P2P loads.
+//                     shard once: w' = w - lr*g_p for p in ticket order, each
+//                     g_p slice read straight from worker p's HBM over NVLink
+//                     (P2P loads, payload crosses once), w' written to the back
+//                     buffer AND stored into every worker's replica (the pull,
+//                     handle_pull server.py:84-91, as P2P stores -- no gather
+//                     pass). Per-element order == global push order, no atomics
+//                     on weights. While streaming it scans the update slices;
+//                     the last CTA exchanges these verdicts with the other
+//                     owners (an update with ANY non-finite element is
+//                     rejected whole, server.py:65-67), commits by flipping the
+//                     buffers (or, rarely, redoes its slice without the
+//                     rejected updates; a non-finite result leaves w unchanged,
+//                     server.py:38-41), flags pulled = t to every worker and
+//                     runs the replicated gate (gate.cuh) -- every rank decides
+//                     the same group from the same inputs, so no gate traffic
+//                     crosses NVLink.
 //
 // Waits are only ever on flags written by OTHER GPUs' kernels that never wait
 // on the waiter's later work, so the protocol cannot deadlock; every spin has a
 // watchdog that aborts the kernel instead of hanging the GPU.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -51,7 +55,8 @@ constexpr unsigned long long kTimeoutNs = 20ull * 1000 * 1000 * 1000;
 struct ShardPtrs {
   const float* w[kMaxRanks];            // each shard's weights (peer mappings)
   const float* upd[kMaxRanks];          // each worker's update buffer
-  unsigned long long* flags[kMaxRanks]; // each rank's flag array: ready[G] then applied[G]
+  float* rep[kMaxRanks];                // each worker's replica (pull destination)
+  unsigned long long* flags[kMaxRanks]; // each rank's flags: ready[G], pulled[G], verdict[G]
   long long lo[kMaxRanks];
 };
 
@@ -67,10 +72,11 @@ struct ShardCtl {
   // (grant -> pusher first, then released ids ascending; simnet.py:192-201),
   // which every later event of the homogeneous chain inherits.
   int32_t order[kMaxRanks];
+  int32_t cur;  // which shard buffer holds the current weights
 };
 
 struct IpcBlob {
-  cudaIpcMemHandle_t w, upd, flags;
+  cudaIpcMemHandle_t w, upd, rep, flags;
   long long lo, hi;
   int rank, world;
 };
@@ -95,11 +101,15 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
 }
 
 // Last-CTA election; returns true in exactly one CTA (counter k is reset).
-__device__ bool last_cta(ShardCtl* ctl, int k) {
+// CTAs that stored to peer memory fence at system scope before arriving so
+// the winner's system-scope release covers their remote stores; CTAs that
+// only read need a GPU-scope fence.
+__device__ bool last_cta(ShardCtl* ctl, int k, bool wrote_remote) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (wrote_remote) __threadfence_system();
+    else __threadfence();
     const unsigned prev = atomicAdd(&ctl->arrive[k], 1u);
     s_last = (prev == gridDim.x - 1);
     if (s_last) ctl->arrive[k] = 0;
@@ -108,72 +118,142 @@ __device__ bool last_cta(ShardCtl* ctl, int k) {
   return s_last;
 }
 
-__global__ void __launch_bounds__(kThreads)
-k_shard_ready(const float* __restrict__ upd, long long d, ShardPtrs P, int G, int me,
-              unsigned long long t, ShardCtl* ctl) {
-  const long long nv = d >> 2;
-  unsigned bad = 0;
-  const long long stride = (long long)gridDim.x * kThreads;
-  for (long long j = (long long)blockIdx.x * kThreads + threadIdx.x; j < nv; j += stride)
-    bad |= nonfinite4(ld_stream(reinterpret_cast<const float4*>(upd) + j)) ? 1u : 0u;
-  if (blockIdx.x == 0 && threadIdx.x < (d & 3)) bad |= nonfinite(upd[(nv << 2) + threadIdx.x]) ? 1u : 0u;
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0 && bad) atomicOr(&ctl->bad, 1u);
-  if (!last_cta(ctl, 0)) return;
-  if (threadIdx.x == 0) {
-    const unsigned b = atomicExch(&ctl->bad, 0u);
-    __threadfence_system();
-    for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, (t << 1) | (b ? 1ull : 0ull));
-  }
+// Worker `me` pushes its update for step t: the previous pull (every owner's
+// slice of step t-1 in its replica) must have landed first.
+__global__ void k_shard_push(ShardPtrs P, int G, int me, unsigned long long t, ShardCtl* ctl) {
+  if (threadIdx.x != 0) return;
+  if (t > 1 && !wait_flags(P.flags[me] + G, G, t - 1, nullptr, ctl)) return;
+  __threadfence_system();
+  for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, t);
+}
+
+// End of a run: this rank's replica holds every owner's slice of step t.
+__global__ void k_shard_wait_pulled(ShardPtrs P, int G, int me, unsigned long long t, ShardCtl* ctl) {
+  if (threadIdx.x == 0) wait_flags(P.flags[me] + G, G, t, nullptr, ctl);
 }
 
 template <int G_MAX>
 __global__ void __launch_bounds__(kThreads)
-k_shard_apply(float* __restrict__ w, long long n_local, ShardPtrs P, int G, int me,
-              unsigned long long t, float lr, ShardCtl* ctl, double now, ps_trace_row* trace,
+k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local, ShardPtrs P, int G,
+              int me, unsigned long long t, float lr, ShardCtl* ctl, double now, ps_trace_row* trace,
               long long trace_cap) {
-  __shared__ unsigned long long s_bad;
+  __shared__ unsigned s_bits;
   if (threadIdx.x == 0) {
-    unsigned long long bad = 0;
-    if (!wait_flags(P.flags[me], G, t << 1, &bad, ctl)) bad = ~0ull;
-    s_bad = bad;
+    s_bits = 0;
+    if (!wait_flags(P.flags[me], G, t, nullptr, ctl)) s_bits = 0xffffffffu;
   }
   __syncthreads();
-  const unsigned long long badmask = s_bad;
-  if (badmask == ~0ull) return;  // watchdog fired
+  if (s_bits == 0xffffffffu) return;  // watchdog fired
   const long long nv = (n_local + 3) >> 2;
   const long long lo = P.lo[me];
+  const int cur = ctl->cur;
+  const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
+  float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
   const float4* src[G_MAX];
-  bool skip[G_MAX];
 #pragma unroll
-  for (int i = 0; i < G_MAX; ++i) {
-    const int p = i < G ? ctl->order[i] : 0;
-    src[i] = reinterpret_cast<const float4*>(P.upd[p] + lo);
-    skip[i] = (badmask >> p) & 1ull;
-  }
+  for (int i = 0; i < G_MAX; ++i)
+    src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? ctl->order[i] : 0] + lo);
   unsigned dbad = 0;
-  const long long stride = (long long)gridDim.x * kThreads;
-  for (long long j = (long long)blockIdx.x * kThreads + threadIdx.x; j < nv; j += stride) {
-    float4 g[G_MAX];
+  unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
+  // Optimistic single pass: apply all G updates in ticket order into the back
+  // buffer and every worker's replica while scanning the update slices; the
+  // verdict exchange below commits it (or redoes it without the rejected
+  // updates, the rare path). U consecutive float4 per thread per trip with all
+  // G slices loaded first: U*G independent 128-bit loads in flight.
+  constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
+  const long long stride = (long long)gridDim.x * kThreads * U;
+  for (long long base = (long long)blockIdx.x * kThreads * U + threadIdx.x; base < nv; base += stride) {
+    float4 g[U][G_MAX];
+    float4 x[U];
 #pragma unroll
-    for (int i = 0; i < G_MAX; ++i)
-      if (i < G) g[i] = ld_stream(src[i] + j);
-    float4 x = reinterpret_cast<float4*>(w)[j];
+    for (int u = 0; u < U; ++u) {
+      const long long j = base + (long long)u * kThreads;
+      if (j < nv) {
 #pragma unroll
-    for (int i = 0; i < G_MAX; ++i)
-      if (i < G && !skip[i]) x = apply4(x, lr, g[i]);
-    dbad |= nonfinite4(x) ? 1u : 0u;
-    reinterpret_cast<float4*>(w)[j] = x;
+        for (int i = 0; i < G_MAX; ++i)
+          if (i < G) g[u][i] = ld_stream(src[i] + j);
+        x[u] = wsrc[j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = base + (long long)u * kThreads;
+      if (j < nv) {
+#pragma unroll
+        for (int i = 0; i < G_MAX; ++i)
+          if (i < G) {
+            gbad |= nonfinite4(g[u][i]) ? (1u << i) : 0u;
+            x[u] = apply4(x[u], lr, g[u][i]);
+          }
+        dbad |= nonfinite4(x[u]) ? 1u : 0u;
+        wdst[j] = x[u];
+        // every worker's pull of this slice (handle_pull, server.py:84-91):
+        // stored straight into each replica, G-1 of them over NVLink
+#pragma unroll
+        for (int q = 0; q < G_MAX; ++q)
+          if (q < G) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x[u];
+      }
+    }
   }
-  dbad = __syncthreads_or(dbad);
-  if (threadIdx.x == 0 && dbad) atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);
-  if (!last_cta(ctl, 1)) return;
+  gbad = __reduce_or_sync(kFull, gbad);
+  dbad = __reduce_or_sync(kFull, dbad);
+  if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
+  __syncthreads();
+  if (threadIdx.x == 0 && s_bits) atomicOr(&ctl->bad, s_bits);
+  if (!last_cta(ctl, 1, true)) return;
+  // ---- last CTA: verdict exchange, commit, gate ---------------------------
+  __shared__ unsigned long long s_rej;
+  __shared__ int s_div;
+  if (threadIdx.x == 0) {
+    const unsigned b = atomicExch(&ctl->bad, 0u);
+    unsigned long long mine = 0;  // rejected pushers as worker-id bits
+    for (int i = 0; i < G; ++i)
+      if ((b >> i) & 1u) mine |= 1ull << ctl->order[i];
+    // every owner saw a different slice of each update: the reference rejects
+    // an update if ANY element is non-finite (server.py:65-67)
+    __threadfence_system();
+    for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | mine);
+    unsigned long long rej = 0;
+    const unsigned long long t0 = globaltimer_ns();
+    for (int s = 0; s < G; ++s) {
+      unsigned long long v;
+      while (((v = ld_acquire_sys_u64(P.flags[me] + 2 * G + s)) >> 32) < t) {
+        if (globaltimer_ns() - t0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); v = 0; break; }
+        __nanosleep(64);
+      }
+      rej |= v & 0xffffffffull;
+    }
+    s_rej = rej;
+    s_div = (b >> 31) & 1u;
+  }
+  __syncthreads();
+  const unsigned long long rej = s_rej;
+  if (rej) {
+    // rare path: recompute this slice without the rejected updates
+    unsigned redo_bad = 0;
+    for (long long j = threadIdx.x; j < nv; j += kThreads) {
+      float4 x = wsrc[j];
+      for (int i = 0; i < G; ++i)
+        if (!((rej >> ctl->order[i]) & 1ull)) x = apply4(x, lr, src[i][j]);
+      redo_bad |= nonfinite4(x) ? 1u : 0u;
+      wdst[j] = x;
+      for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
+    }
+    if (__syncthreads_or(redo_bad)) s_div = 1;
+    else if (threadIdx.x == 0) s_div = 0;
+    __syncthreads();
+  }
   if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
+      if (s_div) {
+        atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);  // weights stay at w[cur]
+      } else {
+        ctl->cur = cur ^ 1;
+        ctl->gate.version += G - __popcll(rej);
+        ctl->gate.rejected += __popcll(rej);
+      }
       __threadfence_system();
       for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, t);
-      ctl->gate.version += G - __popcll(badmask);
-      ctl->gate.rejected += __popcll(badmask);
     }
     __syncwarp();
     // the replicated gate: every rank decides the same group in ticket order
@@ -212,35 +292,6 @@ k_shard_apply(float* __restrict__ w, long long n_local, ShardPtrs P, int G, int 
   }
 }
 
-__global__ void __launch_bounds__(kThreads)
-k_shard_pull(float* __restrict__ dst, long long d, long long S, ShardPtrs P, int G, int me,
-             unsigned long long t, ShardCtl* ctl) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) s_ok = wait_flags(P.flags[me] + G, G, t, nullptr, ctl) ? 1 : 0;
-  __syncthreads();
-  if (!s_ok) return;
-  const long long nv = (d + 3) >> 2;
-  const long long S4 = S >> 2;
-  const long long stride = (long long)gridDim.x * kThreads;
-  constexpr int U = 4;
-  for (long long base = (long long)blockIdx.x * kThreads * U + threadIdx.x; base < nv; base += stride * U) {
-    float4 v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long j = base + (long long)u * kThreads;
-      if (j < nv) {
-        const int s = (int)(j / S4);
-        v[u] = ld_stream(reinterpret_cast<const float4*>(P.w[s]) + (j - (long long)s * S4));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long j = base + (long long)u * kThreads;
-      if (j < nv) reinterpret_cast<float4*>(dst)[j] = v[u];
-    }
-  }
-}
-
 template <typename T>
 __global__ void k_shard_load(const T* src, float* dst, long long n) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -255,7 +306,8 @@ struct ps_shard_server {
   int world = 1, rank = 0, dev = 0, sm_count = 148;
   cudaStream_t stream = nullptr;
   long long d = 0, S = 0, lo = 0, hi = 0, n_local = 0, dpad = 0;
-  float* w = nullptr;                 // local shard (padded to a multiple of 4)
+  float* w = nullptr;                 // local shard (padded to a multiple of 4), buffer 0
+  float* w_alt = nullptr;             // buffer 1 (ShardCtl::cur says which is current)
   float* upd = nullptr;               // worker update buffer [dpad]
   float* rep = nullptr;               // worker replica [dpad]
   unsigned long long* flags = nullptr;
@@ -266,6 +318,9 @@ struct ps_shard_server {
   ShardPtrs ptrs{};
   std::vector<void*> opened;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t pev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int profile = 0;
+  double phase_ms[3] = {0, 0, 0};   // ready / apply / pull, summed over profiled steps
   std::string err;
 };
 
@@ -344,13 +399,14 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
   };
   if ((e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking))) return bail("stream");
   if ((e = cudaEventCreate(&h->ev0)) || (e = cudaEventCreate(&h->ev1))) return bail("events");
-  if ((e = cudaMalloc(&h->w, shard_bytes))) return bail("shard");
-  if ((e = cudaMemset(h->w, 0, shard_bytes))) return bail("shard memset");
+  if ((e = cudaMalloc(&h->w, shard_bytes)) || (e = cudaMalloc(&h->w_alt, shard_bytes))) return bail("shard");
+  if ((e = cudaMemset(h->w, 0, shard_bytes)) || (e = cudaMemset(h->w_alt, 0, shard_bytes)))
+    return bail("shard memset");
   if ((e = cudaMalloc(&h->upd, h->dpad * sizeof(float)))) return bail("update buffer");
   if ((e = cudaMemset(h->upd, 0, h->dpad * sizeof(float)))) return bail("update memset");
   if ((e = cudaMalloc(&h->rep, h->dpad * sizeof(float)))) return bail("replica");
-  if ((e = cudaMalloc(&h->flags, 2 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags");
-  if ((e = cudaMemset(h->flags, 0, 2 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags memset");
+  if ((e = cudaMalloc(&h->flags, 3 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags");
+  if ((e = cudaMemset(h->flags, 0, 3 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags memset");
   if ((e = cudaMalloc(&h->ctl, sizeof(ShardCtl)))) return bail("ctl");
   if ((e = cudaMallocHost(&h->hctl, sizeof(ShardCtl)))) return bail("hctl");
   std::memset(h->hctl, 0, sizeof(ShardCtl));
@@ -389,7 +445,7 @@ void ps_shard_destroy(ps_shard_server* h) {
   Dev guard(h->dev);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->opened) cudaIpcCloseMemHandle(p);
-  cudaFree(h->w); cudaFree(h->upd); cudaFree(h->rep); cudaFree(h->flags); cudaFree(h->ctl);
+  cudaFree(h->w); cudaFree(h->w_alt); cudaFree(h->upd); cudaFree(h->rep); cudaFree(h->flags); cudaFree(h->ctl);
   cudaFree(h->trace);
   if (h->hctl) cudaFreeHost(h->hctl);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -405,6 +461,7 @@ int ps_shard_ipc_handles(ps_shard_server* h, void* out, int64_t cap) {
   IpcBlob b{};
   SCK(h, cudaIpcGetMemHandle(&b.w, h->w));
   SCK(h, cudaIpcGetMemHandle(&b.upd, h->upd));
+  SCK(h, cudaIpcGetMemHandle(&b.rep, h->rep));
   SCK(h, cudaIpcGetMemHandle(&b.flags, h->flags));
   b.lo = h->lo;
   b.hi = h->hi;
@@ -424,18 +481,22 @@ int ps_shard_connect(ps_shard_server* h, const void* blobs, int64_t len) {
     if (r == h->rank) {
       h->ptrs.w[r] = h->w;
       h->ptrs.upd[r] = h->upd;
+      h->ptrs.rep[r] = h->rep;
       h->ptrs.flags[r] = h->flags;
       continue;
     }
-    void *pw = nullptr, *pu = nullptr, *pf = nullptr;
+    void *pw = nullptr, *pu = nullptr, *pr = nullptr, *pf = nullptr;
     SCK(h, cudaIpcOpenMemHandle(&pw, b[r].w, cudaIpcMemLazyEnablePeerAccess));
     SCK(h, cudaIpcOpenMemHandle(&pu, b[r].upd, cudaIpcMemLazyEnablePeerAccess));
+    SCK(h, cudaIpcOpenMemHandle(&pr, b[r].rep, cudaIpcMemLazyEnablePeerAccess));
     SCK(h, cudaIpcOpenMemHandle(&pf, b[r].flags, cudaIpcMemLazyEnablePeerAccess));
     h->opened.push_back(pw);
     h->opened.push_back(pu);
+    h->opened.push_back(pr);
     h->opened.push_back(pf);
     h->ptrs.w[r] = (const float*)pw;
     h->ptrs.upd[r] = (const float*)pu;
+    h->ptrs.rep[r] = (float*)pr;
     h->ptrs.flags[r] = (unsigned long long*)pf;
   }
   return PS_OK;
@@ -449,8 +510,10 @@ int ps_shard_update_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len) 
 }
 
 // Enqueue `steps` push groups starting at step index t0 (1-based tickets) and
-// wait for them. now[i] is the virtual push time of step i; dst (device, fp32,
-// may be NULL) receives the pulled weights, else the internal replica does.
+// wait for them. now[i] is the virtual push time of step i. Every owner writes
+// its slice of the new weights straight into each worker's (engine-owned)
+// replica; dst (device, fp32, may be NULL) additionally receives a copy of
+// this rank's replica after the last step.
 int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, void* dst,
                  double* ms) {
   Dev guard(h->dev);
@@ -463,30 +526,50 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
     SCK(h, cudaMalloc(&h->trace, cap * sizeof(ps_trace_row)));
     h->trace_cap = cap;
   }
-  float* out = dst ? (float*)dst : h->rep;
   const int G = h->world, me = h->rank;
   const float lr = (float)h->cfg.learning_rate;
-  const int grid = h->sm_count * 4;
+  // CTAs per SM of the streaming kernel (tuning knob, default 4)
+  static const int per_sm = [] {
+    const char* v = getenv("PS_SHARD_CTAS_PER_SM");
+    const int n = v ? atoi(v) : 4;
+    return n > 0 && n <= 16 ? n : 4;
+  }();
+  const int grid = h->sm_count * per_sm;
   SCK(h, cudaEventRecord(h->ev0, h->stream));
   for (int i = 0; i < steps; ++i) {
     const unsigned long long t = (unsigned long long)(t0 + i);
-    k_shard_ready<<<grid, kThreads, 0, h->stream>>>(h->upd, h->d, h->ptrs, G, me, t, h->ctl);
+    if (h->profile) cudaEventRecord(h->pev[0], h->stream);
+    k_shard_push<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, t, h->ctl);
+    if (h->profile) cudaEventRecord(h->pev[1], h->stream);
     if (G <= 2)
-      k_shard_apply<2><<<grid, kThreads, 0, h->stream>>>(h->w, h->n_local, h->ptrs, G, me, t, lr, h->ctl,
-                                                         now[i], h->trace, h->trace_cap);
+      k_shard_apply<2><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
+                                                         h->ctl, now[i], h->trace, h->trace_cap);
     else if (G <= 4)
-      k_shard_apply<4><<<grid, kThreads, 0, h->stream>>>(h->w, h->n_local, h->ptrs, G, me, t, lr, h->ctl,
-                                                         now[i], h->trace, h->trace_cap);
+      k_shard_apply<4><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
+                                                         h->ctl, now[i], h->trace, h->trace_cap);
     else if (G <= 8)
-      k_shard_apply<8><<<grid, kThreads, 0, h->stream>>>(h->w, h->n_local, h->ptrs, G, me, t, lr, h->ctl,
-                                                         now[i], h->trace, h->trace_cap);
+      k_shard_apply<8><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
+                                                         h->ctl, now[i], h->trace, h->trace_cap);
     else
-      k_shard_apply<16><<<grid, kThreads, 0, h->stream>>>(h->w, h->n_local, h->ptrs, G, me, t, lr, h->ctl,
-                                                          now[i], h->trace, h->trace_cap);
-    k_shard_pull<<<grid, kThreads, 0, h->stream>>>(out, h->d, h->S, h->ptrs, G, me, t, h->ctl);
+      k_shard_apply<16><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
+                                                          h->ctl, now[i], h->trace, h->trace_cap);
+    if (h->profile) cudaEventRecord(h->pev[2], h->stream);
+    if (h->profile) {
+      k_shard_wait_pulled<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, t, h->ctl);
+      cudaEventRecord(h->pev[3], h->stream);
+      cudaEventSynchronize(h->pev[3]);
+      for (int k = 0; k < 3; ++k) {
+        float e = 0.f;
+        cudaEventElapsedTime(&e, h->pev[k], h->pev[k + 1]);
+        h->phase_ms[k] += e;
+      }
+    }
   }
+  // the last step's pull: every owner's slice has landed in this replica
+  k_shard_wait_pulled<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, (unsigned long long)(t0 + steps - 1), h->ctl);
   SCK(h, cudaGetLastError());
   SCK(h, cudaEventRecord(h->ev1, h->stream));
+  if (dst) SCK(h, cudaMemcpyAsync(dst, h->rep, h->d * sizeof(float), cudaMemcpyDeviceToDevice, h->stream));
   SCK(h, cudaMemcpyAsync(h->hctl, h->ctl, sizeof(ShardCtl), cudaMemcpyDeviceToHost, h->stream));
   SCK(h, cudaStreamSynchronize(h->stream));
   float e = 0.f;
@@ -499,10 +582,28 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   return PS_OK;
 }
 
+// Profiling: bracket each of the three kernels with events (serializes the
+// host with every step, so only for diagnosis, never for the timed numbers).
+int ps_shard_set_profiling(ps_shard_server* h, int32_t on) {
+  Dev guard(h->dev);
+  if (on && !h->pev[0])
+    for (int k = 0; k < 4; ++k) SCK(h, cudaEventCreate(&h->pev[k]));
+  h->profile = on ? 1 : 0;
+  h->phase_ms[0] = h->phase_ms[1] = h->phase_ms[2] = 0.0;
+  return PS_OK;
+}
+
+int ps_shard_phase_ms(ps_shard_server* h, double* out3) {
+  for (int k = 0; k < 3; ++k) out3[k] = h->phase_ms[k];
+  return PS_OK;
+}
+
 int ps_shard_read_shard(ps_shard_server* h, void* dst_host, int64_t* n) {
   Dev guard(h->dev);
   *n = h->n_local;
-  if (h->n_local > 0) SCK(h, cudaMemcpy(dst_host, h->w, h->n_local * sizeof(float), cudaMemcpyDeviceToHost));
+  SCK(h, cudaMemcpy(h->hctl, h->ctl, sizeof(ShardCtl), cudaMemcpyDeviceToHost));
+  const float* cur = h->hctl->cur ? h->w_alt : h->w;
+  if (h->n_local > 0) SCK(h, cudaMemcpy(dst_host, cur, h->n_local * sizeof(float), cudaMemcpyDeviceToHost));
   return PS_OK;
 }
 

@@ -28,6 +28,8 @@ struct ps_server {
   int64_t d = 0, nv = 0, dpad = 0;     // elements, float4 count, padded length
   float* w[2] = {nullptr, nullptr};    // double-buffered fp32 weights (device)
   dssp::Ctrl* ctrl = nullptr;          // device control block
+  dssp::Ctrl* hctrl_dev = nullptr;     // device alias of the mapped host mirror hctrl
+  int profile = 0;                     // 1: bracket each launch with CUDA events
   dssp::Ctrl* hctrl = nullptr;         // pinned host mirror
   int cur = 0;                         // host mirror of ctrl->cur
   void* stage = nullptr;               // device staging for host-side gradients

@@ -178,3 +178,7 @@ class Engine:
         ms = ctypes.c_double(0)
         self.lib.ps_last_kernel_ms(self._h, ctypes.byref(ms))
         return ms.value
+
+    def set_profiling(self, on=True):
+        """Bracket every per-op launch with CUDA events (last_kernel_ms)."""
+        self.lib.ps_set_profiling(self._h, 1 if on else 0)

@@ -63,6 +63,36 @@ def main(out_dir):
             torch.cuda.synchronize()
             dist.barrier()
             srv.close()
+    # rejection across shards: worker 1's update is non-finite in ONE element,
+    # inside shard 0 only; every owner must reject it whole (server.py:65-67)
+    d = 100_003
+    cfg = ps.validate_config(ps.make_config(paradigm="asp", worker_count=world, dimension=d,
+                                            learning_rate=0.05, seed=3))
+    w0 = oracle.initial_weights_f64(3, d)
+    srv = ShardedServer(cfg, d, rank, world, local, w0_host=w0)
+    g = oracle.synthetic_update(1, rank, 0, d)
+    if rank == 1:
+        g[7] = np.nan
+    srv.update[:d].copy_(torch.from_numpy(g))
+    torch.cuda.synchronize()
+    dist.barrier()
+    srv.run([1.0, 2.0])
+    w = w0.astype(np.float32)
+    for _ in range(2):
+        for p in range(world):
+            if p != 1:
+                w = oracle.apply_f32(w, oracle.synthetic_update(1, p, 0, d), 0.05)
+    st = srv.state()
+    verdict["checks"].append({
+        "run": "reject", "d": d, "trace": True,
+        "shard": bool(np.array_equal(srv.read_shard().view(np.uint32), w[srv.lo:srv.hi].view(np.uint32))),
+        "replica": bool(np.array_equal(srv.read_replica().view(np.uint32), w.view(np.uint32))),
+        "version": int(st.version) + int(st.rejected), "steps": 2,
+        "rejected": int(st.rejected)})
+    assert int(st.rejected) == 2, int(st.rejected)
+    torch.cuda.synchronize()
+    dist.barrier()
+    srv.close()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
         json.dump(verdict, fh)
     dist.barrier()
