@@ -61,10 +61,22 @@ struct Vec4Load<double> {
 
 // Warp-collective copy of the control block into the host-mapped mirror, so
 // the host reads every op's result and the gate tables without a D2H copy.
+// Only the live part crosses PCIe: the header, the first P entries of each
+// 64-slot gate table, the gate counters and the op result (3 + 5P + 8 words).
 __device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* mirror) {
+  static_assert(sizeof(ps_gate_state) == 8 * (3 + 5 * PS_MAX_WORKERS + 4), "gate layout");
+  static_assert(sizeof(Ctrl) == sizeof(ps_gate_state) + 32, "ctrl layout");
   const unsigned long long* s = reinterpret_cast<const unsigned long long*>(ctrl);
   unsigned long long* d = reinterpret_cast<unsigned long long*>(mirror);
-  for (int i = threadIdx.x & 31; i < (int)(sizeof(Ctrl) / 8); i += 32) d[i] = s[i];
+  const int P = ctrl->gate.worker_count;
+  const int n = 3 + 5 * P + 8;
+  for (int i = threadIdx.x & 31; i < n; i += 32) {
+    int word;
+    if (i < 3) word = i;                                              // header
+    else if (i < 3 + 5 * P) word = 3 + ((i - 3) / P) * PS_MAX_WORKERS + (i - 3) % P;  // tables
+    else word = 3 + 5 * PS_MAX_WORKERS + (i - 3 - 5 * P);             // counters + result
+    d[word] = s[word];
+  }
 }
 
 // One streaming pass w[cur^1] = w[cur] - lr*g with flag reduction; the last CTA

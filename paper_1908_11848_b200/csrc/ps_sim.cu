@@ -511,6 +511,9 @@ __device__ void data_warp(const SimArgs& a, unsigned dw, unsigned* s_ring, int w
     if (i >= base + have) {
       // fetch up to 32 published ops at once (one coalesced 256 B load)
       base = i;
+      unsigned backoff = 32;  // ns; doubles while the log is dry (the control
+                              // warp emits ~1 op/us: hot polling only steals
+                              // L2 bandwidth from the op stores it waits for)
       for (;;) {
         const long long k = base + lane;
         batch = k < a.ops_cap ? ld_relaxed_u64(a.ops + k) : 0ull;
@@ -521,7 +524,8 @@ __device__ void data_warp(const SimArgs& a, unsigned dw, unsigned* s_ring, int w
           if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
           return;
         }
-        __nanosleep(32);
+        __nanosleep(backoff);
+        backoff = backoff < 512 ? backoff * 2 : 512;
       }
     }
     const Op op = __shfl_sync(kFull, batch, (int)(i - base));
@@ -676,14 +680,16 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   __shared__ unsigned s_ring[kRing];
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) s_ring[i] = 0;
   __syncthreads();
-  const unsigned gw = (blockIdx.x * kSimThreads + threadIdx.x) >> 5;
-  const int warps_here = blockIdx.x == 0 ? kSimThreads / 32 - 1 : kSimThreads / 32;
-  if (gw == 0) {
+  // CTA 0 is the control warp alone: no data warp competes with it for its
+  // SM sub-partition's issue slot (the scheduler favours higher warp ids).
+  if (blockIdx.x == 0) {
+    if (threadIdx.x >= 32) return;
     if constexpr (PM > 0) control_warp_regs<PM>(a);
     else control_warp(a, s);
-  } else {
-    data_warp<V>(a, gw - 1, s_ring, warps_here);
+    return;
   }
+  const unsigned dw = ((blockIdx.x - 1) * kSimThreads + threadIdx.x) >> 5;
+  data_warp<V>(a, dw, s_ring, kSimThreads / 32);
 }
 
 // After the run: fold the data side's counters into the control block.
@@ -794,8 +800,10 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
 
   // one CTA per SM; the weight slice of every data warp lives in registers
   // when it fits V float4 per lane (V in {1,2,4,8,16}), else in HBM (V = 0)
-  int grid = sc->data_ctas > 0 ? sc->data_ctas : h->sm_count;
-  const long long dwarps = (long long)grid * (kSimThreads / 32) - 1;
+  int grid = sc->data_ctas > 0 ? sc->data_ctas + 1 : h->sm_count;
+  if (grid > h->sm_count) grid = h->sm_count;
+  if (grid < 2) grid = 2;
+  const long long dwarps = (long long)(grid - 1) * (kSimThreads / 32);
   const long long per = (h->nv + dwarps - 1) / dwarps;
   const long long need_v = (per + 31) / 32;
   const int vi = need_v <= 1 ? 0 : need_v <= 2 ? 1 : need_v <= 4 ? 2 : need_v <= 8 ? 3 : need_v <= 16 ? 4 : 5;
@@ -811,7 +819,7 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   int per_sm = 0;
   PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimThreads, 0));
   if (grid > per_sm * h->sm_count) grid = per_sm * h->sm_count;
-  if (grid < 1) return ps_fail(h, PS_E_CUDA, "k_sim cannot be resident");
+  if (grid < 2) return ps_fail(h, PS_E_CUDA, "k_sim cannot be resident");
 
   SimArgs a{};
   a.P = P;
@@ -838,12 +846,12 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   a.ops = (Op*)b.ops;
   a.gword = b.gcount;
   a.tag = b.tag;
-  a.n_ctas = (unsigned)grid;
+  a.n_ctas = (unsigned)(grid - 1);  // CTA 0 is the control warp alone
   a.trace = b.trace;
   a.losses = b.losses;
   a.ctrl = h->ctrl;
   a.out = (SimOut*)b.out;
-  a.n_data_warps = (unsigned)(grid * (kSimThreads / 32) - 1);
+  a.n_data_warps = (unsigned)((grid - 1) * (kSimThreads / 32));
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.base_version = h->hctrl->gate.version;
   b.last_base_version = a.base_version;
