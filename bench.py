@@ -255,6 +255,96 @@ def apply_sweep(torch, ps, hbm_peak):
     return out
 
 
+C4_DIM = 1_730_714  # ResNet-110 (CIFAR)
+
+
+def c4_config(paradigm, s_lower, r_max):
+    """BASELINE configs[3]: three workers throttled 1x / 2x / 4x."""
+    import paper_1908_11848_b200 as ps
+    return ps.validate_config(ps.make_config(
+        paradigm=paradigm, worker_count=3, s_lower=s_lower, r_max=r_max,
+        timing_preset="homogeneous", compute_base=1.0, comm_delay=0.05, throttle=(1, 2, 4),
+        model_kind="tiny_mlp", dimension=3072, dataset_size=3 * 1600, batch_size=16,
+        learning_rate=0.05, epochs=1, seed=0))
+
+
+def c4_throttled(torch, ps, reps=3):
+    """configs[3]: DSSP threshold adaptation vs fixed SSP on a 1x/2x/4x
+    cluster, ResNet-110-sized server, device run loop; reports device
+    throughput and the schedule's virtual-time outcome per paradigm."""
+    from paper_1908_11848_b200.metrics import per_worker, staleness_histogram
+    d = C4_DIM
+    synth = torch.from_numpy(synthetic_host(3, 2, d)).cuda()
+    out = {}
+    for name, s, r in PARADIGMS:
+        cfg = c4_config(name, s, r)
+        sim = ps.DeviceSimulation(cfg, dimension=d, grad="synthetic")
+        sim.set_synthetic(synth, 2)
+        sim.run(read_weights=False, reset_gate=True)
+        times = []
+        for _ in range(reps):
+            rep = sim.run(read_weights=False, reset_gate=True)
+            times.append(rep.device_ms)
+        pw = per_worker(rep.entries)
+        hist = staleness_histogram(rep.entries)
+        out[name] = {"updates_per_s": rep.applied / (statistics.median(times) * 1e-3),
+                     "updates": rep.applied,
+                     "virtual_duration_s": max(e.time for e in rep.entries),
+                     "fast_worker_wait_s": pw[0].wait_s,
+                     "total_wait_s": sum(w.wait_s for w in pw.values()),
+                     "max_staleness": max(hist) if hist else 0}
+        sim.engine.close()
+    del synth
+    return out
+
+
+def torch_workers(torch, ps, iters=48, batch=128):
+    """Real ResNet-20 workers (PyTorch fwd/bwd) on one GPU,
+    round-robin, pushing .grad views and pulling into parameter views through
+    the drop-in. Reports iterations/s per paradigm and the share of wall time
+    spent in the server calls."""
+    from paper_1908_11848_b200.workers import CifarResNet, TorchWorker, synthetic_cifar
+    out = {}
+    for name, s, r in PARADIGMS:
+        cfg = ps.validate_config(ps.make_config(paradigm=name, worker_count=4, s_lower=s,
+                                                r_max=r, learning_rate=0.01, seed=0))
+        torch.manual_seed(0)
+        workers = [TorchWorker(p, CifarResNet(20), synthetic_cifar(2, batch, seed=p))
+                   for p in range(4)]
+        server = ps.ParameterServer(cfg, workers[0].dimension)
+        for wk in workers:
+            wk.adopt_from(server)
+        pending, done, ps_s = set(), 0, 0.0
+        # warm-up (cuDNN autotuning), then the timed iterations
+        for phase, n in (("warm", 8), ("timed", iters)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ps_s, done, it, now = 0.0, 0, 0, 0.0
+            while done < n:
+                p = it % 4
+                it += 1
+                if p in pending:
+                    continue
+                g = workers[p].begin_iteration()
+                now += 1.0 + 0.5 * p
+                t1 = time.perf_counter()
+                dec = server.handle_push(g, now)
+                if dec.granted:
+                    for q in dec.released:
+                        pending.discard(q)
+                        workers[q].adopt_from(server)
+                    workers[p].adopt_from(server)
+                else:
+                    pending.add(p)
+                ps_s += time.perf_counter() - t1
+                done += 1
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+        out[name] = {"iters_per_s": done / wall, "ps_share_of_wall": ps_s / wall,
+                     "model": "CIFAR ResNet-20 (272,474 params)", "batch": batch, "workers": 4}
+    return out
+
+
 def e2e_drop_in(torch, ps, cfg, calls, synth_host, d):
     """The same workload through the reference-facing API: ParameterServer
     drop-in, gradients from pinned host memory (H2D per push), pulls into
@@ -367,6 +457,8 @@ def bench_single(args):
     cpu_updates, cpu_s = reference_sample(calls, synth_host, d, "dssp", 3, 12, cfg.learning_rate,
                                           max_updates=args.cpu_updates)
     sweep = apply_sweep(torch, ps, hbm_peak) if not args.no_sweep else None
+    c4 = c4_throttled(torch, ps) if not args.no_sweep else None
+    tw = torch_workers(torch, ps) if not args.no_sweep else None
     clocks = sampler.summary()
     line = {
         "metric": METRIC,
@@ -403,6 +495,8 @@ def bench_single(args):
                                    "oracle.RefPortServer (fp64 numpy + Python gate)",
                          "host_cpus": os.cpu_count()},
         "sweep": sweep,
+        "c4_throttled": c4,
+        "torch_workers": tw,
         "clocks": clocks,
     }
     print(json.dumps(line))

@@ -181,6 +181,12 @@ int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, 
 int ps_last_kernel_ms(ps_server* h, double* ms);
 int ps_set_profiling(ps_server* h, int32_t on);
 
+/* Device-pointer updates and pull destinations are usually produced/consumed
+ * on the caller's own CUDA stream (a cudaStream_t passed as an opaque
+ * pointer; NULL = none). Every later push/pull is stream-ordered after the
+ * work already enqueued there (an event edge, no host synchronization). */
+int ps_set_producer_stream(ps_server* h, void* cuda_stream);
+
 /* ------------------------------------------------------------------------
  * Sharded server: G GPUs, one process (rank) per GPU, one worker per rank.
  * Shard r owns [r*S, min(d,(r+1)*S)), S = ceil(d/G) rounded up to 4. Ranks

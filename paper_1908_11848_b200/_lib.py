@@ -99,6 +99,7 @@ SIGNATURES = {
     "ps_sim_losses": (ctypes.c_int, [_P, _PI64, _PD, _I64, _PI64]),
     "ps_last_kernel_ms": (ctypes.c_int, [_P, _PD]),
     "ps_set_profiling": (ctypes.c_int, [_P, _I32]),
+    "ps_set_producer_stream": (ctypes.c_int, [_P, _P]),
     "ps_shard_create": (ctypes.c_int, [ctypes.POINTER(PSConfig), _I32, _I32, _P, _I64,
                                        ctypes.POINTER(_P)]),
     "ps_shard_ipc_handles": (ctypes.c_int, [_P, _P, _I64]),

@@ -272,6 +272,17 @@ int mark(ps_server* h, cudaEvent_t e) {
   return PS_OK;
 }
 
+// Stream-order the server after the caller's producer stream (e.g. the
+// PyTorch stream whose backward wrote the update, or that will read a pull):
+// an event edge, no host synchronization.
+int after_producer(ps_server* h) {
+  if (!h->producer) return PS_OK;
+  if (!h->ev_in) PS_CK(h, cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+  PS_CK(h, cudaEventRecord(h->ev_in, h->producer));
+  PS_CK(h, cudaStreamWaitEvent(h->stream, h->ev_in, 0));
+  return PS_OK;
+}
+
 // Pinned (page-locked, UVA-mapped) host memory can be read and written by
 // kernels directly over PCIe; pageable memory has to be staged.
 bool pinned_host(const void* p) {
@@ -300,18 +311,18 @@ int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_
   const size_t esz = g_dtype == PS_F64 ? 8 : 4;
   const size_t bytes = (size_t)h->d * esz;
   const void* dg = g;
+  int rc = after_producer(h);
+  if (rc) return rc;
   const bool direct = aligned16(g) && (g_on_device || pinned_host(g));
   if (!direct) {
-    int rc = ensure_stage(h, bytes);
-    if (rc) return rc;
+    if ((rc = ensure_stage(h, bytes))) return rc;
     PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, g_on_device ? cudaMemcpyDeviceToDevice
                                                                : cudaMemcpyHostToDevice, h->stream));
     dg = h->stage;
   }
   const float lr = (float)h->cfg.learning_rate;
   const int grid = grid_for(h, h->nv);
-  int rc = mark(h, h->ev0);
-  if (rc) return rc;
+  if ((rc = mark(h, h->ev0))) return rc;
   if (g_dtype == PS_F32)
     k_apply<float><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const float*)dg, h->d,
                                                           lr, h->ctrl, fuse, worker, now, h->hctrl_dev);
@@ -422,6 +433,7 @@ void ps_destroy(ps_server* h) {
   cudaFree(s.trace); cudaFree(s.losses); cudaFree(s.out);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -493,6 +505,7 @@ int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_d
   if (rc) return rc;
   // device or pinned host destinations are written by the copy kernel itself
   // (over PCIe for pinned host memory); pageable ones take a staged copy
+  if ((rc = after_producer(h))) return rc;  // the destination may still be in use there
   if (aligned16(dst) && (dst_on_device || pinned_host(dst))) {
     const int grid = grid_for(h, h->nv);
     if (dst_dtype == PS_F32)
@@ -551,6 +564,11 @@ int ps_last_kernel_ms(ps_server* h, double* ms) {
 
 int ps_set_profiling(ps_server* h, int32_t on) {
   h->profile = on ? 1 : 0;
+  return PS_OK;
+}
+
+int ps_set_producer_stream(ps_server* h, void* cuda_stream) {
+  h->producer = (cudaStream_t)cuda_stream;
   return PS_OK;
 }
 

@@ -119,10 +119,24 @@ class Engine:
         self.refresh(sync=False)
 
     # -- hot path -----------------------------------------------------------
+    def _order_after(self, tensor):
+        """Device tensors come from (or go to) the caller's current CUDA
+        stream: order the server's stream after it (no host sync)."""
+        if tensor is None:
+            ptr = None
+        else:
+            import torch
+            ptr = torch.cuda.current_stream(tensor.device).cuda_stream
+        if ptr != getattr(self, "_producer", None):
+            self.lib.ps_set_producer_stream(self._h, ptr)
+            self._producer = ptr
+
     def _gradient_args(self, values):
         dev = device_pointer(values)
         if dev is not None:
+            self._order_after(values)
             return dev[0], dev[1], 1, values
+        self._order_after(None)
         arr, dt = as_f32_host(values)
         return arr.ctypes.data, dt, 0, arr
 
@@ -162,7 +176,9 @@ class Engine:
         dev = device_pointer(out)
         if dev is not None:
             ptr, dt, on_dev = dev[0], dev[1], 1
+            self._order_after(out)
         else:
+            self._order_after(None)
             if not (out.flags.c_contiguous and out.dtype in (np.float32, np.float64)):
                 raise ValueError("pull destination must be a contiguous fp32/fp64 array")
             ptr, dt, on_dev = out.ctypes.data, (_lib.F64 if out.dtype == np.float64 else _lib.F32), 0
