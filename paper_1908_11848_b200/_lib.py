@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdssp_ps.so")
+LIB_PATH = os.environ.get("DSSP_PS_LIB") or os.path.join(HERE, "libdssp_ps.so")  # env: profiling builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "dssp_ps.h")
 
 MAX_WORKERS = 64

@@ -3,13 +3,15 @@
 // One cooperative persistent kernel executes a whole simulated cluster run
 // (simnet.py:127-201) with the host out of the loop:
 //
-//   * warp 0 of CTA 0 is the CONTROL warp. Lane 0 runs the reference's event
-//     loop -- (time, seq) ordered events, one in flight per worker, same-instant
-//     push aggregation (simnet.py:167-201: apply every gradient of the group in
-//     seq order, then decide each) -- and the whole warp runs each gate
-//     decision (gate.cuh). It appends TraceEntry rows (trace.py:28-37) and emits
-//     data operations into an in-HBM op log that it publishes with a release
-//     store. It never waits for the data side.
+//   * CTA 0 is a single CONTROL warp. It runs the reference's event loop --
+//     (time, seq) ordered events, one in flight per worker, same-instant push
+//     aggregation (simnet.py:167-201: apply every gradient of the group in seq
+//     order, then decide each) -- and every gate decision, with all tables in
+//     registers: replicated scalars for P <= 8 (ctl_regs.cuh), one worker per
+//     lane for P <= 32 (ctl_lanes.cuh), shared memory beyond (CtlState). It
+//     appends TraceEntry rows (trace.py:28-37) and emits data operations into
+//     an HBM op log as self-tagged 64-bit words. It never waits for the data
+//     side; it is the run's critical path (~3 us per worker iteration).
 //   * every other warp is a DATA warp that owns a fixed contiguous slice of
 //     the parameter vector and replays the op log in order over its slice:
 //       PULL  (handle_pull, server.py:84-91)  copy the weights into the
@@ -33,6 +35,7 @@
 
 #include "common.cuh"
 #include "gate.cuh"
+#include "ctl_lanes.cuh"
 #include "ctl_regs.cuh"
 #include "server.h"
 
@@ -100,9 +103,25 @@ struct SimArgs {
   unsigned n_ctas;
 };
 
+// Cycle accounting of the control warp, compiled in with -DPS_SIM_PROFILE.
+#ifdef PS_SIM_PROFILE
+#define PROF_DECL() long long c_pop = 0, c_push = 0, c_other = 0, c_gate = 0
+#define PROF_MARK(t) const long long t = clock64()
+#define PROF_ADD(acc, t) acc += clock64() - (t)
+#define PROF_PRINT()                                                                         \
+  if ((threadIdx.x & 31) == 0)                                                               \
+  printf("PROF P=%d events=%lld pop=%lld push=%lld (gate=%lld) other=%lld\n", a.P, processed, \
+         c_pop, c_push, c_gate, c_other)
+#else
+#define PROF_DECL() do {} while (0)
+#define PROF_MARK(t) do {} while (0)
+#define PROF_ADD(acc, t) do {} while (0)
+#define PROF_PRINT() do {} while (0)
+#endif
+
 constexpr int kSimThreads = 256;
 constexpr int kMaxP = PS_MAX_WORKERS;
-constexpr int kRegP = 8;  // control state in registers up to this many workers
+constexpr int kLaneP = 32;  // one worker per control-warp lane up to this many workers
 
 struct CtlState {
   ps_gate_state gate;
@@ -355,7 +374,9 @@ __device__ void control_warp_regs(const SimArgs& a) {
   for (int q = 0; q < PM; ++q)
     if (q < P) schedule(comm, PS_EV_PULL_ARRIVE, q);
   if (w0) a.out->t_start = globaltimer_ns();
+  PROF_DECL();
   for (;;) {
+    PROF_MARK(t_a);
     // pop the (time, seq)-minimum event
     int w = -1;
     double bt = 0.0;
@@ -368,6 +389,8 @@ __device__ void control_warp_regs(const SimArgs& a) {
       }
     }
     if (w < 0) break;
+    PROF_MARK(t_b);
+    PROF_ADD(c_pop, t_a);
     if (a.max_events > 0 && processed >= a.max_events) { status = PS_E_BUDGET; break; }
     const double at = bt;
     const int kind = rget<PM>(ev_kind, w);
@@ -431,7 +454,9 @@ __device__ void control_warp_regs(const SimArgs& a) {
       for (int i = 0; i < PM; ++i) {
         if (i < n && status == PS_OK) {
           const int m = order[i];
+          PROF_MARK(t_g);
           const GateResult r = g.on_push(m, at);
+          PROF_ADD(c_gate, t_g);
           pushes += 1;
           if (r.status != PS_OK) {
             status = r.status;
@@ -448,7 +473,9 @@ __device__ void control_warp_regs(const SimArgs& a) {
       }
       if (status != PS_OK) break;
     }
+    PROF_ADD(kind == PS_EV_PUSH_ARRIVE ? c_push : c_other, t_b);
   }
+  PROF_PRINT();
   emit(OP_END, 0, 0, 0);
   if (w0) {
     a.out->t_control_done = globaltimer_ns();
@@ -467,6 +494,161 @@ __device__ void control_warp_regs(const SimArgs& a) {
     a.out->pushes = pushes;
     a.out->trace_rows = n_trace;
     a.out->unfinished = status == PS_OK ? unfinished : 0ull;
+    if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
+  }
+}
+
+// Control warp for P <= 32 (ctl_lanes.cuh): lane q owns worker q; the event
+// loop is warp-uniform; lane 0 stores op words, lanes 0-4 one trace row each.
+__device__ void control_warp_lanes(const SimArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const int P = a.P, budget = a.budget, nsyn = a.n_synth;
+  const bool bowl = a.grad_kind == PS_GRAD_BOWL;
+  const bool mine = lane < P;
+  const double comm = a.comm_delay;
+  const unsigned tag = a.tag;
+  Op* const ops = a.ops;
+  unsigned long long* const trace = reinterpret_cast<unsigned long long*>(a.trace);
+  const long long trace_cap = a.record_trace ? a.trace_cap : 0;
+  LaneGate g;
+  {
+    const ps_gate_state& s = a.ctrl->gate;
+    const bool z = a.reset_gate || !mine;
+    g.paradigm = s.paradigm; g.P = P; g.s_lower = s.s_lower; g.r_max = s.r_max;
+    g.threshold = s.threshold;
+    g.deferred = a.reset_gate ? 0u : (unsigned)s.deferred;
+    g.decisions = s.decisions;
+    g.clock = z ? 0 : (int)s.clocks[lane];
+    g.latest = z ? 0.0 : s.latest[lane];
+    g.previous = z ? 0.0 : s.previous[lane];
+    g.populated = z ? 0 : (int)s.populated[lane];
+    g.credits = z ? 0 : (int)s.credits[lane];
+  }
+  // this lane's worker
+  double ev_time = 0.0;
+  int ev_seq = 0x7fffffff, ev_kind = -1;
+  int iters = 0, active = 0, staged = 0, gslot = 0, sidx = 0, order_i = 0;
+  bool finished = false;
+  double nct = (mine && budget > 0) ? a.ctime[(long long)lane * budget] : 0.0;  // next compute draw
+  int seq = 0, status = PS_OK;
+  long long processed = 0, n_ops = 0, n_trace = 0, pushes = 0, next_slot = 0;
+
+  auto emit = [&](int type, int w, int buf, long long slot) {
+    if (lane == 0) st_relaxed_u64(ops + n_ops, op_pack(tag, type, w, buf, slot));
+    n_ops += 1;
+  };
+  // ps_trace_row as five 8-byte words, one per lane 0..4, one store
+  auto trace_row = [&](double t, int w, int kind, int decision, unsigned long long released) {
+    if (n_trace < trace_cap) {
+      const long long count = from_lane(g.clock, w);
+      unsigned long long v = 0;
+      if (lane == 0) v = dbits(t);
+      else if (lane == 1) v = ((unsigned long long)(unsigned)kind << 32) | (unsigned)w;
+      else if (lane == 2) v = (unsigned long long)count;
+      else if (lane == 3) v = (unsigned)decision;
+      else if (lane == 4) v = released;
+      if (lane < 5) trace[n_trace * 5 + lane] = v;
+    }
+    n_trace += 1;
+  };
+  auto schedule = [&](double at, int kind, int w) {
+    if (lane == w) { ev_time = at; ev_seq = seq; ev_kind = kind; }
+    seq += 1;
+  };
+  for (int q = 0; q < P; ++q) schedule(comm, PS_EV_PULL_ARRIVE, q);
+  if (lane == 0) a.out->t_start = globaltimer_ns();
+  for (;;) {
+    // pop the (time, seq)-minimum event: time bits, then seq
+    const bool cand = mine && ev_kind >= 0;
+    const unsigned long long tb = dbits(ev_time);
+    const unsigned hi = __reduce_min_sync(kFull, cand ? (unsigned)(tb >> 32) : 0xffffffffu);
+    const bool c1 = cand && (unsigned)(tb >> 32) == hi;
+    const unsigned lo = __reduce_min_sync(kFull, c1 ? (unsigned)tb : 0xffffffffu);
+    const bool c2 = c1 && (unsigned)tb == lo;
+    const int ms = __reduce_min_sync(kFull, c2 ? ev_seq : 0x7fffffff);
+    const unsigned who = __ballot_sync(kFull, c2 && ev_seq == ms);
+    if (!who) break;
+    const int w = __ffs(who) - 1;
+    if (a.max_events > 0 && processed >= a.max_events) { status = PS_E_BUDGET; break; }
+    const double at = from_lane(ev_time, w);
+    const int kind = from_lane(ev_kind, w);
+    if (lane == w) ev_kind = -1;
+    processed += 1;
+    if (kind == PS_EV_PULL_ARRIVE) {
+      const int st = 1 - from_lane(active, w);
+      emit(OP_PULL, w, st, 0);
+      if (lane == w) staged = st;
+      trace_row(at, w, kind, -1, 0);
+      schedule(at + comm, PS_EV_PULL_RETURN, w);
+    } else if (kind == PS_EV_PULL_RETURN) {
+      if (lane == w) active = staged;  // adopt (simnet.py:156-165)
+      trace_row(at, w, kind, -1, 0);
+      if (from_lane(iters, w) < budget) schedule(at + from_lane(nct, w), PS_EV_COMPUTE_DONE, w);
+      else if (lane == w) finished = true;
+    } else if (kind == PS_EV_COMPUTE_DONE) {
+      if (lane == w) {
+        iters += 1;
+        if (iters < budget) nct = a.ctime[(long long)w * budget + iters];  // prefetch the next draw
+        gslot = (int)next_slot;
+      }
+      const long long slot = next_slot++;
+      emit(OP_GRAD, w, bowl ? from_lane(active, w) : from_lane(sidx, w) % nsyn, slot);
+      trace_row(at, w, kind, -1, 0);
+      schedule(at + comm, PS_EV_PUSH_ARRIVE, w);
+    } else if (kind == PS_EV_GRANT_DELIVER) {
+      trace_row(at, w, kind, -1, 0);
+      schedule(at + comm, PS_EV_PULL_ARRIVE, w);
+    } else {
+      // PUSH_ARRIVE: every push queued at the same instant joins the group
+      // (simnet.py:167-182); the popped one first, the rest by seq.
+      const bool join = mine && ev_kind == PS_EV_PUSH_ARRIVE && dbits(ev_time) == dbits(at);
+      unsigned rest = __ballot_sync(kFull, join);
+      if (join) ev_kind = -1;
+      int n = 1;
+      if (lane == 0) order_i = w;
+      while (rest) {
+        const int sm = __reduce_min_sync(kFull, ((rest >> lane) & 1u) ? ev_seq : 0x7fffffff);
+        const int m = __ffs(__ballot_sync(kFull, ((rest >> lane) & 1u) && ev_seq == sm)) - 1;
+        if (lane == n) order_i = m;
+        rest &= ~(1u << m);
+        n += 1;
+      }
+      for (int i = 0; i < n; ++i) {
+        const int m = from_lane(order_i, i);
+        emit(OP_APPLY, m, bowl ? 0 : from_lane(sidx, m) % nsyn, from_lane(gslot, m));
+        if (lane == m) sidx += 1;
+      }
+      for (int i = 0; i < n && status == PS_OK; ++i) {
+        const int m = from_lane(order_i, i);
+        const GateResult r = g.on_push(lane, m, at);
+        pushes += 1;
+        if (r.status != PS_OK) { status = r.status; break; }
+        trace_row(at, m, PS_EV_PUSH_ARRIVE, r.outcome, r.released);
+        if (r.outcome == 0) {
+          schedule(at + comm, PS_EV_GRANT_DELIVER, m);
+          for (unsigned rel = (unsigned)r.released; rel; rel &= rel - 1)
+            schedule(at + comm, PS_EV_GRANT_DELIVER, __ffs(rel) - 1);
+        }
+      }
+      if (status != PS_OK) break;
+    }
+  }
+  emit(OP_END, 0, 0, 0);
+  const unsigned done = __ballot_sync(kFull, mine && finished);
+  ps_gate_state& dst = a.ctrl->gate;
+  if (mine) {
+    dst.clocks[lane] = g.clock; dst.latest[lane] = g.latest; dst.previous[lane] = g.previous;
+    dst.populated[lane] = g.populated; dst.credits[lane] = g.credits;
+  }
+  if (lane == 0) {
+    a.out->t_control_done = globaltimer_ns();
+    const unsigned all = P == 32 ? 0xffffffffu : ((1u << P) - 1u);
+    dst.deferred = g.deferred;
+    dst.decisions = g.decisions;
+    a.out->events = processed;
+    a.out->pushes = pushes;
+    a.out->trace_rows = n_trace;
+    a.out->unfinished = status == PS_OK ? (unsigned long long)(all & ~done) : 0ull;
     if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
   }
 }
@@ -673,8 +855,10 @@ __device__ void data_warp(const SimArgs& a, unsigned dw, unsigned* s_ring, int w
 }
 
 // V: float4 per lane of register-resident weights (0 = in HBM);
-// PM: register-resident control tables for P <= PM workers (0 = shared memory).
-template <int V, int PM>
+// CTL: control tables in registers -- 2/4/8: scalar, replicated in every lane
+// (fastest for few workers, ctl_regs.cuh); 32: one worker per lane
+// (ctl_lanes.cuh); 0: shared memory (any P <= 64).
+template <int V, int CTL>
 __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   __shared__ CtlState s;
   __shared__ unsigned s_ring[kRing];
@@ -684,7 +868,8 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   // SM sub-partition's issue slot (the scheduler favours higher warp ids).
   if (blockIdx.x == 0) {
     if (threadIdx.x >= 32) return;
-    if constexpr (PM > 0) control_warp_regs<PM>(a);
+    if constexpr (CTL == 32) control_warp_lanes(a);
+    else if constexpr (CTL > 0) control_warp_regs<CTL>(a);
     else control_warp(a, s);
     return;
   }
@@ -807,14 +992,14 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   const long long per = (h->nv + dwarps - 1) / dwarps;
   const long long need_v = (per + 31) / 32;
   const int vi = need_v <= 1 ? 0 : need_v <= 2 ? 1 : need_v <= 4 ? 2 : need_v <= 8 ? 3 : need_v <= 16 ? 4 : 5;
-  const int pi = P <= 2 ? 0 : P <= 4 ? 1 : P <= kRegP ? 2 : 3;
-  static const void* const table[6][4] = {
-      {(const void*)k_sim<1, 2>, (const void*)k_sim<1, 4>, (const void*)k_sim<1, 8>, (const void*)k_sim<1, 0>},
-      {(const void*)k_sim<2, 2>, (const void*)k_sim<2, 4>, (const void*)k_sim<2, 8>, (const void*)k_sim<2, 0>},
-      {(const void*)k_sim<4, 2>, (const void*)k_sim<4, 4>, (const void*)k_sim<4, 8>, (const void*)k_sim<4, 0>},
-      {(const void*)k_sim<8, 2>, (const void*)k_sim<8, 4>, (const void*)k_sim<8, 8>, (const void*)k_sim<8, 0>},
-      {(const void*)k_sim<16, 2>, (const void*)k_sim<16, 4>, (const void*)k_sim<16, 8>, (const void*)k_sim<16, 0>},
-      {(const void*)k_sim<0, 2>, (const void*)k_sim<0, 4>, (const void*)k_sim<0, 8>, (const void*)k_sim<0, 0>}};
+  const int pi = P <= 2 ? 0 : P <= 4 ? 1 : P <= 8 ? 2 : P <= kLaneP ? 3 : 4;
+  static const void* const table[6][5] = {
+      {(const void*)k_sim<1, 2>, (const void*)k_sim<1, 4>, (const void*)k_sim<1, 8>, (const void*)k_sim<1, 32>, (const void*)k_sim<1, 0>},
+      {(const void*)k_sim<2, 2>, (const void*)k_sim<2, 4>, (const void*)k_sim<2, 8>, (const void*)k_sim<2, 32>, (const void*)k_sim<2, 0>},
+      {(const void*)k_sim<4, 2>, (const void*)k_sim<4, 4>, (const void*)k_sim<4, 8>, (const void*)k_sim<4, 32>, (const void*)k_sim<4, 0>},
+      {(const void*)k_sim<8, 2>, (const void*)k_sim<8, 4>, (const void*)k_sim<8, 8>, (const void*)k_sim<8, 32>, (const void*)k_sim<8, 0>},
+      {(const void*)k_sim<16, 2>, (const void*)k_sim<16, 4>, (const void*)k_sim<16, 8>, (const void*)k_sim<16, 32>, (const void*)k_sim<16, 0>},
+      {(const void*)k_sim<0, 2>, (const void*)k_sim<0, 4>, (const void*)k_sim<0, 8>, (const void*)k_sim<0, 32>, (const void*)k_sim<0, 0>}};
   const void* kern = table[vi][pi];
   int per_sm = 0;
   PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimThreads, 0));
