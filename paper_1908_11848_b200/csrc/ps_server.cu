@@ -14,6 +14,7 @@
 // decision, so apply + clock increment + decision is one launch.
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -283,6 +284,16 @@ int after_producer(ps_server* h) {
   return PS_OK;
 }
 
+// Host transfers through the copy engines instead of zero-copy kernel access
+// (PS_HOST_DMA=1; an A/B switch for the e2e path).
+bool host_dma() {
+  static const bool on = [] {
+    const char* v = getenv("PS_HOST_DMA");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 // Pinned (page-locked, UVA-mapped) host memory can be read and written by
 // kernels directly over PCIe; pageable memory has to be staged.
 bool pinned_host(const void* p) {
@@ -313,7 +324,7 @@ int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_
   const void* dg = g;
   int rc = after_producer(h);
   if (rc) return rc;
-  const bool direct = aligned16(g) && (g_on_device || pinned_host(g));
+  const bool direct = aligned16(g) && (g_on_device || (!host_dma() && pinned_host(g)));
   if (!direct) {
     if ((rc = ensure_stage(h, bytes))) return rc;
     PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, g_on_device ? cudaMemcpyDeviceToDevice
@@ -506,7 +517,10 @@ int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_d
   // device or pinned host destinations are written by the copy kernel itself
   // (over PCIe for pinned host memory); pageable ones take a staged copy
   if ((rc = after_producer(h))) return rc;  // the destination may still be in use there
-  if (aligned16(dst) && (dst_on_device || pinned_host(dst))) {
+  // f32 to host: the copy engine (measured faster than kernel stores over
+  // PCIe); f64 to pinned host: the conversion kernel writes it in place
+  const bool kernel_dst = dst_on_device || (dst_dtype == PS_F64 && !host_dma() && pinned_host(dst));
+  if (aligned16(dst) && kernel_dst) {
     const int grid = grid_for(h, h->nv);
     if (dst_dtype == PS_F32)
       k_copy_out<float><<<grid, 256, 0, h->stream>>>(src, (float*)dst, h->d);
