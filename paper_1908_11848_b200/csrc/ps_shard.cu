@@ -8,13 +8,13 @@
 //
 // One step = one same-instant push group of all G workers (the homogeneous
 // schedule of simnet.py:167-201: apply every update in seq order, then decide
-// each), two kernels in stream order on every rank, with no host in the loop
-// and no collective:
+// each), ONE kernel per step on every rank, with no host in the loop and no
+// collective (all of its CTAs are co-resident by construction):
 //
-//   K1 k_shard_push   (one thread) worker r's push: once every owner's slice
-//                     of its previous pull has landed, release-store
+//   push              CTA 0 of rank r's kernel: once every owner's slice of
+//                     worker r's previous pull has landed, release-store
 //                     ready = t into every owner's flag array.
-//   K2 k_shard_apply  owner r waits for all G ready flags, then streams its
+//   k_shard_apply     owner r waits for all G ready flags, then streams its
 //                     shard once: w' = w - lr*g_p for p in ticket order, each
 //                     g_p slice read straight from worker p's HBM over NVLink
 //                     (P2P loads, payload crosses once), w' written to the back
@@ -27,10 +27,11 @@
 //                     rejected whole, server.py:65-67), commits by flipping the
 //                     buffers (or, rarely, redoes its slice without the
 //                     rejected updates; a non-finite result leaves w unchanged,
-//                     server.py:38-41), flags pulled = t to every worker and
-//                     runs the replicated gate (gate.cuh) -- every rank decides
-//                     the same group from the same inputs, so no gate traffic
-//                     crosses NVLink.
+//                     server.py:38-41) and flags pulled = t to every worker.
+//   gate CTA          one extra CTA runs the replicated gate (gate.cuh) for the
+//                     group from shared memory while the data CTAs stream --
+//                     every rank decides the same group from the same inputs,
+//                     so no gate traffic crosses NVLink.
 //
 // Waits are only ever on flags written by OTHER GPUs' kernels that never wait
 // on the waiter's later work, so the protocol cannot deadlock; every spin has a
@@ -71,7 +72,7 @@ struct ShardCtl {
   // previous group's decisions scheduled the workers' GRANT_DELIVER events
   // (grant -> pusher first, then released ids ascending; simnet.py:192-201),
   // which every later event of the homogeneous chain inherits.
-  int32_t order[kMaxRanks];
+  int32_t order[2][kMaxRanks];  // [step parity]: this group's order, the next one's
   int32_t cur;  // which shard buffer holds the current weights
 };
 
@@ -92,7 +93,7 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
         atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT);
         return false;
       }
-      __nanosleep(100);
+      __nanosleep(20);
     }
     if (acc_bad && (v & 1ull)) bad |= 1ull << q;
   }
@@ -104,27 +105,18 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
 // CTAs that stored to peer memory fence at system scope before arriving so
 // the winner's system-scope release covers their remote stores; CTAs that
 // only read need a GPU-scope fence.
-__device__ bool last_cta(ShardCtl* ctl, int k, bool wrote_remote) {
+__device__ bool last_cta(ShardCtl* ctl, int k, bool wrote_remote, int participants) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     if (wrote_remote) __threadfence_system();
     else __threadfence();
     const unsigned prev = atomicAdd(&ctl->arrive[k], 1u);
-    s_last = (prev == gridDim.x - 1);
+    s_last = (prev == (unsigned)participants - 1);
     if (s_last) ctl->arrive[k] = 0;
   }
   __syncthreads();
   return s_last;
-}
-
-// Worker `me` pushes its update for step t: the previous pull (every owner's
-// slice of step t-1 in its replica) must have landed first.
-__global__ void k_shard_push(ShardPtrs P, int G, int me, unsigned long long t, ShardCtl* ctl) {
-  if (threadIdx.x != 0) return;
-  if (t > 1 && !wait_flags(P.flags[me] + G, G, t - 1, nullptr, ctl)) return;
-  __threadfence_system();
-  for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, t);
 }
 
 // End of a run: this rank's replica holds every owner's slice of step t.
@@ -137,10 +129,83 @@ __global__ void __launch_bounds__(kThreads)
 k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local, ShardPtrs P, int G,
               int me, unsigned long long t, float lr, ShardCtl* ctl, double now, ps_trace_row* trace,
               long long trace_cap) {
+  const int cur_order = (int)(t & 1);
+  // ---- the gate CTA: the replicated decisions for this group ------------
+  // They depend only on (worker, now) and the gate tables, never on the data,
+  // so one extra CTA runs them from shared memory while the others stream.
+  if (blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x >= 32) return;
+    __shared__ ps_gate_state sg;
+    {
+      const unsigned long long* s = reinterpret_cast<const unsigned long long*>(&ctl->gate);
+      unsigned long long* d = reinterpret_cast<unsigned long long*>(&sg);
+      for (int i = threadIdx.x; i < (int)(sizeof(ps_gate_state) / 8); i += 32) d[i] = s[i];
+    }
+    __syncwarp();
+    int next[kMaxRanks];
+    int n_next = 0;
+    int status = PS_OK;
+    for (int i = 0; i < G; ++i) {
+      const int p = ctl->order[cur_order][i];
+      const GateResult r = gate_on_push(&sg, p, now);
+      if (threadIdx.x == 0) {
+        if (r.status != PS_OK) status = r.status;
+        if (r.status == PS_OK && r.outcome == 0) {
+          next[n_next++] = p;
+          for (int q = 0; q < G; ++q)
+            if ((r.released >> q) & 1ull) next[n_next++] = q;
+        }
+        const unsigned long long n = ctl->trace_n++;
+        if ((long long)n < trace_cap) {
+          ps_trace_row row;
+          row.time = now;
+          row.worker = p;
+          row.kind = PS_EV_PUSH_ARRIVE;
+          row.count = sg.clocks[p];
+          row.decision = r.outcome;
+          row._pad = 0;
+          row.released = r.released;
+          trace[n] = row;
+        }
+      }
+      __syncwarp();
+    }
+    if (threadIdx.x == 0) {
+      // every worker must be back for the next group (homogeneous schedule)
+      if (status == PS_OK && n_next != G) status = PS_E_PROTOCOL;
+      if (status != PS_OK) atomicCAS(&ctl->status, PS_OK, status);
+      for (int i = 0; i < n_next && i < G; ++i) ctl->order[cur_order ^ 1][i] = next[i];
+    }
+    __syncwarp();
+    // tables back (version / rejected belong to the committing CTA)
+    for (int q = threadIdx.x; q < G; q += 32) {
+      ctl->gate.clocks[q] = sg.clocks[q];
+      ctl->gate.latest[q] = sg.latest[q];
+      ctl->gate.previous[q] = sg.previous[q];
+      ctl->gate.populated[q] = sg.populated[q];
+      ctl->gate.credits[q] = sg.credits[q];
+    }
+    if (threadIdx.x == 0) {
+      ctl->gate.deferred = sg.deferred;
+      ctl->gate.decisions = sg.decisions;
+    }
+    return;
+  }
+  // ---- data CTAs ----------------------------------------------------------
   __shared__ unsigned s_bits;
   if (threadIdx.x == 0) {
     s_bits = 0;
-    if (!wait_flags(P.flags[me], G, t, nullptr, ctl)) s_bits = 0xffffffffu;
+    // worker `me` pushes its update for step t once every owner's slice of
+    // its previous pull has landed (CTA 0 publishes for the whole rank)
+    bool ok = true;
+    if (blockIdx.x == 0) {
+      ok = t <= 1 || wait_flags(P.flags[me] + G, G, t - 1, nullptr, ctl);
+      if (ok) {
+        __threadfence_system();
+        for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, t);
+      }
+    }
+    if (!ok || !wait_flags(P.flags[me], G, t, nullptr, ctl)) s_bits = 0xffffffffu;
   }
   __syncthreads();
   if (s_bits == 0xffffffffu) return;  // watchdog fired
@@ -152,7 +217,7 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
   const float4* src[G_MAX];
 #pragma unroll
   for (int i = 0; i < G_MAX; ++i)
-    src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? ctl->order[i] : 0] + lo);
+    src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? ctl->order[cur_order][i] : 0] + lo);
   unsigned dbad = 0;
   unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
   // Optimistic single pass: apply all G updates in ticket order into the back
@@ -161,7 +226,8 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
   // updates, the rare path). U consecutive float4 per thread per trip with all
   // G slices loaded first: U*G independent 128-bit loads in flight.
   constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
-  const long long stride = (long long)gridDim.x * kThreads * U;
+  const int ndata = gridDim.x - 1;
+  const long long stride = (long long)ndata * kThreads * U;
   for (long long base = (long long)blockIdx.x * kThreads * U + threadIdx.x; base < nv; base += stride) {
     float4 g[U][G_MAX];
     float4 x[U];
@@ -200,15 +266,15 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
   if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
   __syncthreads();
   if (threadIdx.x == 0 && s_bits) atomicOr(&ctl->bad, s_bits);
-  if (!last_cta(ctl, 1, true)) return;
-  // ---- last CTA: verdict exchange, commit, gate ---------------------------
+  if (!last_cta(ctl, 1, true, ndata)) return;
+  // ---- last data CTA: verdict exchange, commit ----------------------------
   __shared__ unsigned long long s_rej;
   __shared__ int s_div;
   if (threadIdx.x == 0) {
     const unsigned b = atomicExch(&ctl->bad, 0u);
     unsigned long long mine = 0;  // rejected pushers as worker-id bits
     for (int i = 0; i < G; ++i)
-      if ((b >> i) & 1u) mine |= 1ull << ctl->order[i];
+      if ((b >> i) & 1u) mine |= 1ull << ctl->order[cur_order][i];
     // every owner saw a different slice of each update: the reference rejects
     // an update if ANY element is non-finite (server.py:65-67)
     __threadfence_system();
@@ -219,7 +285,7 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
       unsigned long long v;
       while (((v = ld_acquire_sys_u64(P.flags[me] + 2 * G + s)) >> 32) < t) {
         if (globaltimer_ns() - t0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); v = 0; break; }
-        __nanosleep(64);
+        __nanosleep(20);
       }
       rej |= v & 0xffffffffull;
     }
@@ -234,7 +300,7 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
     for (long long j = threadIdx.x; j < nv; j += kThreads) {
       float4 x = wsrc[j];
       for (int i = 0; i < G; ++i)
-        if (!((rej >> ctl->order[i]) & 1ull)) x = apply4(x, lr, src[i][j]);
+        if (!((rej >> ctl->order[cur_order][i]) & 1ull)) x = apply4(x, lr, src[i][j]);
       redo_bad |= nonfinite4(x) ? 1u : 0u;
       wdst[j] = x;
       for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
@@ -243,52 +309,16 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
     else if (threadIdx.x == 0) s_div = 0;
     __syncthreads();
   }
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      if (s_div) {
-        atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);  // weights stay at w[cur]
-      } else {
-        ctl->cur = cur ^ 1;
-        ctl->gate.version += G - __popcll(rej);
-        ctl->gate.rejected += __popcll(rej);
-      }
-      __threadfence_system();
-      for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, t);
+  if (threadIdx.x == 0) {
+    if (s_div) {
+      atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);  // weights stay at w[cur]
+    } else {
+      ctl->cur = cur ^ 1;
+      ctl->gate.version += G - __popcll(rej);
+      ctl->gate.rejected += __popcll(rej);
     }
-    __syncwarp();
-    // the replicated gate: every rank decides the same group in ticket order
-    int next[kMaxRanks];
-    int n_next = 0;
-    for (int i = 0; i < G; ++i) {
-      const int p = ctl->order[i];
-      const GateResult r = gate_on_push(&ctl->gate, p, now);
-      if (threadIdx.x == 0) {
-        if (r.status != PS_OK) atomicCAS(&ctl->status, PS_OK, r.status);
-        if (r.status == PS_OK && r.outcome == 0) {
-          next[n_next++] = p;
-          for (int q = 0; q < G; ++q)
-            if ((r.released >> q) & 1ull) next[n_next++] = q;
-        }
-        const unsigned long long n = ctl->trace_n++;
-        if ((long long)n < trace_cap) {
-          ps_trace_row row;
-          row.time = now;
-          row.worker = p;
-          row.kind = PS_EV_PUSH_ARRIVE;
-          row.count = ctl->gate.clocks[p];
-          row.decision = r.outcome;
-          row._pad = 0;
-          row.released = r.released;
-          trace[n] = row;
-        }
-      }
-      __syncwarp();
-    }
-    if (threadIdx.x == 0) {
-      // every worker must be back for the next group (homogeneous schedule)
-      if (n_next != G) atomicCAS(&ctl->status, PS_OK, PS_E_PROTOCOL);
-      for (int i = 0; i < n_next && i < G; ++i) ctl->order[i] = next[i];
-    }
+    __threadfence_system();
+    for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, t);
   }
 }
 
@@ -416,7 +446,7 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
   gs.s_lower = cfg->s_lower;
   gs.r_max = cfg->r_max;
   gs.threshold = cfg->paradigm == PS_BSP ? 0 : cfg->s_lower;
-  for (int r = 0; r < kMaxRanks; ++r) h->hctl->order[r] = r;  // initial pulls arrive in worker order
+  for (int r = 0; r < kMaxRanks; ++r) h->hctl->order[1][r] = r;  // step 1: initial pulls arrive in worker order
   if ((e = cudaMemcpy(h->ctl, h->hctl, sizeof(ShardCtl), cudaMemcpyHostToDevice))) return bail("ctl upload");
   // w0: full-length initial weights; bit 0 of w0_flags = on device, bit 1 = fp64
   if (w0) {
@@ -528,37 +558,43 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   }
   const int G = h->world, me = h->rank;
   const float lr = (float)h->cfg.learning_rate;
-  // CTAs per SM of the streaming kernel (tuning knob, default 4)
-  static const int per_sm = [] {
+  // CTAs per SM of the streaming kernel (tuning knob, default 4), clamped so
+  // every CTA is co-resident (CTA 0 publishes this rank's push that the other
+  // CTAs -- and the peers -- wait for), plus one gate CTA
+  static const int per_sm_env = [] {
     const char* v = getenv("PS_SHARD_CTAS_PER_SM");
     const int n = v ? atoi(v) : 4;
     return n > 0 && n <= 16 ? n : 4;
   }();
-  const int grid = h->sm_count * per_sm;
+  const void* kern = G <= 2 ? (const void*)k_shard_apply<2> : G <= 4 ? (const void*)k_shard_apply<4>
+                   : G <= 8 ? (const void*)k_shard_apply<8> : (const void*)k_shard_apply<16>;
+  int resident = 0;
+  SCK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kThreads, 0));
+  int data_ctas = h->sm_count * (per_sm_env < resident ? per_sm_env : resident) - 1;
+  if (data_ctas < 1) return sfail(h, PS_E_CUDA, "k_shard_apply cannot be resident");
+  const dim3 grid(data_ctas + 1), block(kThreads);
+  float* w0p = h->w;
+  float* w1p = h->w_alt;
+  long long nl = h->n_local;
+  ShardPtrs ptrs = h->ptrs;
+  ShardCtl* ctl = h->ctl;
+  ps_trace_row* trace = h->trace;
+  long long tcap = h->trace_cap;
+  int Gv = G, mev = me;
+  float lrv = lr;
   SCK(h, cudaEventRecord(h->ev0, h->stream));
   for (int i = 0; i < steps; ++i) {
-    const unsigned long long t = (unsigned long long)(t0 + i);
+    unsigned long long t = (unsigned long long)(t0 + i);
+    double nowv = now[i];
+    void* args[] = {&w0p, &w1p, &nl, &ptrs, &Gv, &mev, &t, &lrv, &ctl, &nowv, &trace, &tcap};
     if (h->profile) cudaEventRecord(h->pev[0], h->stream);
-    k_shard_push<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, t, h->ctl);
-    if (h->profile) cudaEventRecord(h->pev[1], h->stream);
-    if (G <= 2)
-      k_shard_apply<2><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
-                                                         h->ctl, now[i], h->trace, h->trace_cap);
-    else if (G <= 4)
-      k_shard_apply<4><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
-                                                         h->ctl, now[i], h->trace, h->trace_cap);
-    else if (G <= 8)
-      k_shard_apply<8><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
-                                                         h->ctl, now[i], h->trace, h->trace_cap);
-    else
-      k_shard_apply<16><<<grid, kThreads, 0, h->stream>>>(h->w, h->w_alt, h->n_local, h->ptrs, G, me, t, lr,
-                                                          h->ctl, now[i], h->trace, h->trace_cap);
-    if (h->profile) cudaEventRecord(h->pev[2], h->stream);
+    SCK(h, cudaLaunchKernel(kern, grid, block, args, 0, h->stream));
     if (h->profile) {
+      cudaEventRecord(h->pev[1], h->stream);
       k_shard_wait_pulled<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, t, h->ctl);
-      cudaEventRecord(h->pev[3], h->stream);
-      cudaEventSynchronize(h->pev[3]);
-      for (int k = 0; k < 3; ++k) {
+      cudaEventRecord(h->pev[2], h->stream);
+      cudaEventSynchronize(h->pev[2]);
+      for (int k = 0; k < 2; ++k) {
         float e = 0.f;
         cudaEventElapsedTime(&e, h->pev[k], h->pev[k + 1]);
         h->phase_ms[k] += e;

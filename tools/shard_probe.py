@@ -21,7 +21,7 @@ srv.run(times[25:45])
 ph = (ctypes.c_double * 3)()
 srv.lib.ps_shard_phase_ms(srv._h, ph)
 if rank == 0:
-    print(f"world={world} d={d} step_ms={ms/20:.4f} profiled ready={ph[0]/20:.4f} apply={ph[1]/20:.4f} pull={ph[2]/20:.4f}")
+    print(f"world={world} d={d} step_ms={ms/20:.4f} profiled apply_kernel={ph[0]/20:.4f} then_wait_pull={ph[1]/20:.4f}")
 dist.barrier()
 srv.close()
 dist.destroy_process_group()
