@@ -5,11 +5,15 @@
 
 N=1 (default) measures BASELINE.json configs[1] ("C2"): a ResNet-20-sized
 server (d = 272,474 fp32) with P = 4 workers on the heterogeneous gtx-mix
-schedule (simnet.py:34-69; 2 fast + 2 workers 2.2x slower), one "step" being
-one complete simulated run of 250 iterations per worker (1,000 server
-updates: pull -> update -> push-apply -> gate decision) executed by the
-device-resident run loop. Updates are synthetic N(0,1) fp32 vectors resident
-in HBM (2 per worker), lr = 0.05. The headline paradigm is DSSP(3, 12); BSP,
+schedule (simnet.py:34-69; 2 fast + 2 workers 2.2x slower). One "step" is the
+server serving the request stream of one complete run (250 iterations per
+worker: 1,000 push-applies, 1,004 pulls, 1,000 gate decisions) in the order
+the reference simulator issues them (tests/golden/c2_schedule.json.gz,
+recorded from stalesync itself), in one device-resident kernel; every
+decision is checked against the recorded one. The closed-loop variant (the
+simulator's whole event loop on the device, trace byte-identical) is reported
+as device_simulation. Updates are synthetic N(0,1) fp32 vectors resident in
+HBM (2 per worker), lr = 0.05. The headline paradigm is DSSP(3, 12); BSP,
 SSP(3) and ASP are reported beside it.
 
 N>1 (torchrun, one process per GPU) measures configs[2] ("C3"): a
@@ -389,6 +393,8 @@ def e2e_drop_in(torch, ps, cfg, calls, synth_host, d):
 def bench_single(args):
     import torch
     import paper_1908_11848_b200 as ps
+    from paper_1908_11848_b200.engine import Engine
+    from paper_1908_11848_b200.sim import DeviceReplay
 
     hbm_peak, peak_kind = peaks()
     d = C2_DIM
@@ -396,21 +402,48 @@ def bench_single(args):
     synth_host = synthetic_host(P, K, d)
     synth = torch.from_numpy(synth_host).cuda()
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-    per_paradigm = {}
-    sims = {}
+    import oracle
+    w0 = oracle.initial_weights_f64(0, d)
+    # (1) headline: the device serving the recorded C2 request stream
+    #     (pull / apply / decide, reference order), decisions by the device gate
+    replays, sims, recorded = {}, {}, {}
     for name, s, r in PARADIGMS:
+        calls, trace = reference_calls(name)
+        recorded[name] = trace
+        eng = Engine(name, P, s, r, 0.05, d, w0=w0)
+        replays[name] = DeviceReplay(eng, calls, synth, K)
         cfg = c2_config(name, s, r)
         sim = ps.DeviceSimulation(cfg, dimension=d, grad="synthetic")
         sim.set_synthetic(synth, K)
         sims[name] = (cfg, sim)
         for _ in range(args.warmup):
+            replays[name].run(decisions=False)
             sim.run(read_weights=False, reset_gate=True)
     sampler = ClockSampler(0)
-    reports = {}
+    per_paradigm, device_sim, parity, reports = {}, {}, {}, {}
     with sampler:
         for name, s, r in PARADIGMS:
+            times, applied = [], 0
+            for _ in range(args.steps):
+                flush_l2(torch, flush)
+                torch.cuda.synchronize()
+                rr = replays[name].run(decisions=False)
+                times.append(rr.device_ms)
+                applied += rr.applied
+            total_ms = sum(times)
+            check = replays[name].run()
+            want = [(ln.split("\t")[4]) for ln in recorded[name].splitlines()
+                    if ln.split("\t")[2] == "push_arrive"]
+            got = [ps.decision_token(o == "grant", rel) for o, rel in check.decisions]
+            per_paradigm[name] = {"updates_per_s": applied / (total_ms * 1e-3),
+                                  "iters_per_s": applied / (total_ms * 1e-3),
+                                  "ms_per_step": total_ms / args.steps,
+                                  "defers_per_step": sum(1 for o, _ in check.decisions if o == "defer")}
+            parity.setdefault("replay_decisions_identical_to_reference", {})[name] = got == want
+        # (2) the closed loop: the simulator's whole event loop on the device
+        for name, s, r in PARADIGMS:
             cfg, sim = sims[name]
-            times, applied, iters = [], 0, 0
+            times, applied = [], 0
             rep = None
             for _ in range(args.steps):
                 flush_l2(torch, flush)
@@ -418,24 +451,20 @@ def bench_single(args):
                 rep = sim.run(read_weights=False, reset_gate=True)
                 times.append(rep.device_ms)
                 applied += rep.applied
-                iters += rep.pushes
             reports[name] = rep
             total_ms = sum(times)
-            per_paradigm[name] = {
-                "updates_per_s": applied / (total_ms * 1e-3),
-                "iters_per_s": iters / (total_ms * 1e-3),
-                "ms_per_step": total_ms / args.steps,
-                "defers_per_step": sum(1 for e in rep.entries
-                                       if e.kind == "push_arrive" and e.decision == "defer"),
-                "virtual_duration_s": max(e.time for e in rep.entries),
-            }
+            device_sim[name] = {"updates_per_s": applied / (total_ms * 1e-3),
+                                "ms_per_step": total_ms / args.steps,
+                                "virtual_duration_s": max(e.time for e in rep.entries)}
+            parity.setdefault("simulation_trace_identical_to_reference", {})[name] = \
+                ps.format_trace(rep.entries) == recorded[name]
     head = per_paradigm["dssp"]
-    cfg, sim = sims["dssp"]
-    rep = reports["dssp"]
-    # roofline of the dominant kernel (k_sim): algorithmic bytes per launch =
-    # updates x 12 B/param (push-apply) + pulls x 8 B/param (read w, write replica)
-    pulls = sum(1 for e in rep.entries if e.kind == "pull_arrive")
-    alg_bytes = rep.applied * 12 * d + pulls * 8 * d
+    calls, _ = reference_calls("dssp")
+    n_apply = sum(1 for c in calls if c[0] == "apply")
+    n_pull = sum(1 for c in calls if c[0] == "pull")
+    # roofline of the dominant kernel (k_sim, replay mode): algorithmic bytes
+    # per launch = updates x 12 B/param (push-apply) + pulls x 8 B/param
+    alg_bytes = n_apply * 12 * d + n_pull * 8 * d
     achieved = alg_bytes / (head["ms_per_step"] * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k_sim_dram_bytes.json")
@@ -444,16 +473,8 @@ def bench_single(args):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    # parity inside the bench: every paradigm's device trace must equal the
-    # reference simulator's trace of the same schedule, byte for byte
-    parity = {}
-    for name, _, _ in PARADIGMS:
-        want_calls, want_trace = reference_calls(name)
-        parity[name] = ps.format_trace(reports[name].entries) == want_trace
-    calls, _ = reference_calls("dssp")
-    # e2e through the reference-facing API
+    cfg = c2_config("dssp", 3, 12)
     e2e_value, h2d, d2h, e2e_updates = e2e_drop_in(torch, ps, cfg, calls, synth_host, d)
-    # cpu baseline: the oracle port of the reference on a bounded sample
     cpu_updates, cpu_s = reference_sample(calls, synth_host, d, "dssp", 3, 12, cfg.learning_rate,
                                           max_updates=args.cpu_updates)
     sweep = apply_sweep(torch, ps, hbm_peak) if not args.no_sweep else None
@@ -474,24 +495,27 @@ def bench_single(args):
         "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": "C2 (BASELINE configs[1]): ResNet-20-sized server d=272474 fp32, "
-                               "P=4 workers, gtx-mix schedule, DSSP(3,12); step = one device-resident "
-                               "run of 250 iterations/worker (1000 updates + pulls + gate decisions)",
+                               "P=4 workers, gtx-mix schedule, DSSP(3,12); step = the server "
+                               "serving the reference's recorded request stream of one run "
+                               f"({n_apply} pushes, {n_pull} pulls, {n_apply} gate decisions) "
+                               "in one device-resident kernel",
                    "d": d, "workers": P, "paradigm": "dssp", "s_lower": 3, "r_max": 12,
-                   "updates_per_step": rep.applied, "l2": "flushed between timed steps (256 MiB write)",
+                   "updates_per_step": n_apply, "l2": "flushed between timed steps (256 MiB write)",
                    "parallelism": "single GPU"},
         "per_paradigm": per_paradigm,
-        "parity": {"trace_identical_to_reference": parity},
+        "device_simulation": device_sim,
+        "parity": parity,
         "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": "ParameterServer drop-in, pinned host buffers",
                 "updates_per_step": e2e_updates},
         "gpu_launches": 2 * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_sim (device run loop)",
-                     "bytes_model": "12 B/param per update + 8 B/param per pull"},
+                     "kernel": "k_sim (replay mode)",
+                     "bytes_model": "12 B/param per push-apply + 8 B/param per pull"},
         "cpu_baseline": {"value": cpu_updates / cpu_s, "unit": "updates/s", "cores": 1,
                          "kind": "port",
-                         "sample": f"first {cpu_updates} updates of the same C2 call sequence, "
+                         "sample": f"first {cpu_updates} updates of the same C2 request stream, "
                                    "oracle.RefPortServer (fp64 numpy + Python gate)",
                          "host_cpus": os.cpu_count()},
         "sweep": sweep,

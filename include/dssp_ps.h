@@ -171,6 +171,22 @@ typedef struct ps_trace_row {
 } ps_trace_row;
 
 int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* out);
+
+/* Replay: the server serving a recorded request stream -- the reference's
+ * boundary call sequence (handle_pull / apply_gradient / decide_push, in the
+ * order the simulator issues them) executed in one persistent kernel: pulls
+ * and applies as data ops, every decide through the device gate (decisions
+ * retrievable with ps_replay_decisions as (released << 8) | outcome). Updates
+ * are resident: apply k of worker p uses synthetic[p][k % n_synthetic]. */
+enum { PS_CALL_PULL = 0, PS_CALL_APPLY = 1, PS_CALL_DECIDE = 2 };
+typedef struct ps_replay_call {
+  double now;       /* PS_CALL_DECIDE: the push instant */
+  int32_t kind;
+  int32_t worker;
+} ps_replay_call;
+int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const float* synthetic,
+                  int32_t n_synthetic, int32_t reset_gate, int32_t data_ctas, ps_sim_result* out);
+int ps_replay_decisions(ps_server* h, int64_t* out, int64_t cap, int64_t* n);
 int ps_sim_trace(ps_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
 /* Loss samples of the last run: (version, 0.5*||w - c||^2 in fp64). */
 int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, int64_t* n);

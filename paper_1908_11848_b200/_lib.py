@@ -96,6 +96,8 @@ SIGNATURES = {
     "ps_apply_vectors": (ctypes.c_int, [_I32, _P, _P, _I32, _I64, _D, _P, _PI32]),
     "ps_sim_run": (ctypes.c_int, [_P, ctypes.POINTER(PSSimConfig), ctypes.POINTER(PSSimResult)]),
     "ps_sim_trace": (ctypes.c_int, [_P, ctypes.POINTER(PSTraceRow), _I64, _PI64]),
+    "ps_replay_run": (ctypes.c_int, [_P, _P, _I64, _P, _I32, _I32, _I32, ctypes.POINTER(PSSimResult)]),
+    "ps_replay_decisions": (ctypes.c_int, [_P, _PI64, _I64, _PI64]),
     "ps_sim_losses": (ctypes.c_int, [_P, _PI64, _PD, _I64, _PI64]),
     "ps_last_kernel_ms": (ctypes.c_int, [_P, _PD]),
     "ps_set_profiling": (ctypes.c_int, [_P, _I32]),

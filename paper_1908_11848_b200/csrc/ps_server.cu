@@ -442,6 +442,7 @@ void ps_destroy(ps_server* h) {
   cudaFree(s.ops); cudaFree(s.gcount);
   cudaFree(s.rep); cudaFree(s.gbuf); cudaFree(s.center); cudaFree(s.ctime);
   cudaFree(s.trace); cudaFree(s.losses); cudaFree(s.out);
+  cudaFree(s.calls); cudaFree(s.decisions);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev_in) cudaEventDestroy(h->ev_in);

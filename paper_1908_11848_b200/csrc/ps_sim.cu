@@ -72,6 +72,13 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+struct ReplayCall {  // ps_replay_call
+  double now;
+  int kind;    // kCallPull / kCallApply / kCallDecide
+  int worker;
+};
+constexpr int kCallPull = 0, kCallApply = 1, kCallDecide = 2;
+
 struct SimOut {
   long long events, pushes, trace_rows, applied, rejected;
   unsigned long long unfinished;
@@ -99,6 +106,10 @@ struct SimArgs {
   unsigned n_data_warps;
   unsigned long long timeout_ns;
   long long base_version;
+  int mode;                   // 0: simulated run, 1: replay of a recorded call stream
+  const struct ReplayCall* calls;
+  long long n_calls;
+  long long* decisions;       // replay: (released << 8) | outcome per decide
   unsigned tag;
   unsigned n_ctas;
 };
@@ -653,6 +664,149 @@ __device__ void control_warp_lanes(const SimArgs& a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Replay mode: the server serving a recorded request stream.
+//
+// The control warp reads the reference's boundary call sequence (pull /
+// apply / decide, in the order simnet.py:127-201 issues them) from HBM and
+// executes it: pulls and applies become data ops exactly as in the simulated
+// run, every decide runs the gate on the device. It is what a parameter
+// server does with the requests its workers send, without simulating the
+// workers -- the same work the reference arm times on the CPU
+// (ParameterServer.apply_gradient / decide_push / handle_pull).
+// Each update's finiteness scan (GRAD op) is emitted one 32-call chunk
+// ahead of its apply, so the apply rarely waits for it.
+// ---------------------------------------------------------------------------
+
+template <int PM>
+struct ReplayGate {  // scalar register tables (ctl_regs.cuh), P <= PM
+  RegGate<PM> g;
+  __device__ __forceinline__ void load(const ps_gate_state& s, bool reset, ps_gate_state*) { g.load(s, reset); }
+  __device__ __forceinline__ void store(ps_gate_state& d) { g.store(d); }
+  __device__ __forceinline__ bool deferred(int q) const { return (g.deferred >> q) & 1ull; }
+  __device__ __forceinline__ GateResult on_push(int p, double now) { return g.on_push(p, now); }
+};
+
+template <>
+struct ReplayGate<0> {  // shared-memory tables (gate.cuh), any P <= 64
+  ps_gate_state* s;
+  __device__ __forceinline__ void load(const ps_gate_state& src, bool reset, ps_gate_state* smem) {
+    s = smem;
+    if ((threadIdx.x & 31) == 0) {
+      *s = src;
+      if (reset) {
+        for (int q = 0; q < kMaxP; ++q) {
+          s->clocks[q] = 0; s->latest[q] = 0.0; s->previous[q] = 0.0;
+          s->populated[q] = 0; s->credits[q] = 0;
+        }
+        s->deferred = 0ull;
+      }
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void store(ps_gate_state& d) {
+    if ((threadIdx.x & 31) == 0) {
+      const long long v = d.version, r = d.rejected;
+      d = *s;
+      d.version = v;
+      d.rejected = r;
+    }
+  }
+  __device__ __forceinline__ bool deferred(int q) const { return (s->deferred >> q) & 1ull; }
+  __device__ __forceinline__ GateResult on_push(int p, double now) {
+    const GateResult r = gate_on_push(s, p, now);
+    __syncwarp();
+    return r;
+  }
+};
+
+template <int PM>
+__device__ void control_warp_replay(const SimArgs& a, ps_gate_state* sgate, int* s_staged, int* s_sidx) {
+  const int lane = threadIdx.x & 31;
+  const int P = a.P, nsyn = a.n_synth;
+  const unsigned tag = a.tag;
+  Op* const ops = a.ops;
+  ReplayGate<PM> g;
+  g.load(a.ctrl->gate, a.reset_gate != 0, sgate);
+  for (int q = lane; q < P; q += 32) { s_staged[q] = 0; s_sidx[q] = 0; }
+  __syncwarp();
+  long long n_ops = 0, next_slot = 0, n_dec = 0, pushes = 0;
+  int status = PS_OK;
+  auto emit = [&](int type, int w, int buf, long long slot) {
+    if (lane == 0) st_relaxed_u64(ops + n_ops, op_pack(tag, type, w, buf, slot));
+    n_ops += 1;
+  };
+  const long long n = a.n_calls;
+  // lane l holds call (base + l) of the current chunk and its (slot, buf)
+  auto load_chunk = [&](long long base, ReplayCall& c) {
+    const long long i = base + lane;
+    if (i < n) c = a.calls[i];
+    else { c.now = 0.0; c.kind = -1; c.worker = 0; }
+  };
+  auto emit_grads = [&](const ReplayCall& c, long long& slot_l, int& buf_l) {
+    for (int l = 0; l < 32; ++l) {
+      const int kind = __shfl_sync(kFull, c.kind, l);
+      if (kind != kCallApply) continue;
+      const int p = __shfl_sync(kFull, c.worker, l);
+      const int si = s_sidx[p];
+      const int buf = si % nsyn;
+      const long long slot = next_slot++;
+      __syncwarp();
+      if (lane == 0) s_sidx[p] = si + 1;
+      __syncwarp();
+      if (lane == l) { slot_l = slot; buf_l = buf; }
+      emit(OP_GRAD, p, buf, slot);
+    }
+  };
+  ReplayCall cur, nxt;
+  long long cur_slot = 0, nxt_slot = 0;
+  int cur_buf = 0, nxt_buf = 0;
+  if (lane == 0) a.out->t_start = globaltimer_ns();
+  load_chunk(0, cur);
+  emit_grads(cur, cur_slot, cur_buf);
+  for (long long base = 0; base < n && status == PS_OK; base += 32) {
+    load_chunk(base + 32, nxt);
+    emit_grads(nxt, nxt_slot, nxt_buf);  // one chunk of lookahead for the scans
+    const int m = n - base < 32 ? (int)(n - base) : 32;
+    for (int i = 0; i < m; ++i) {
+      const int kind = __shfl_sync(kFull, cur.kind, i);
+      const int w = __shfl_sync(kFull, cur.worker, i);
+      if (w < 0 || w >= P) { status = PS_E_PROTOCOL; break; }
+      if (kind == kCallPull) {
+        if (g.deferred(w)) { status = PS_E_PROTOCOL; break; }  // pulled while deferred
+        const int st = s_staged[w] ^ 1;
+        __syncwarp();
+        if (lane == 0) s_staged[w] = st;
+        __syncwarp();
+        emit(OP_PULL, w, st, 0);
+      } else if (kind == kCallApply) {
+        emit(OP_APPLY, w, __shfl_sync(kFull, cur_buf, i), __shfl_sync(kFull, cur_slot, i));
+      } else {
+        const double now = __shfl_sync(kFull, cur.now, i);
+        const GateResult r = g.on_push(w, now);
+        pushes += 1;
+        if (r.status != PS_OK) { status = r.status; break; }
+        if (lane == 0 && n_dec < a.trace_cap)
+          a.decisions[n_dec] = (long long)((r.released << 8) | (unsigned)r.outcome);
+        n_dec += 1;
+      }
+    }
+    cur = nxt;
+    cur_slot = nxt_slot;
+    cur_buf = nxt_buf;
+  }
+  emit(OP_END, 0, 0, 0);
+  g.store(a.ctrl->gate);
+  if (lane == 0) {
+    a.out->t_control_done = globaltimer_ns();
+    a.out->events = n;
+    a.out->pushes = pushes;
+    a.out->trace_rows = n_dec;
+    a.out->unfinished = 0ull;
+    if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
+  }
+}
+
 constexpr int kRing = 256;  // per-CTA finiteness aggregation ring (> max warp skew in updates)
 
 // Loads of one worker's update slice; V float4 per lane, element u at lo + lane + 32u.
@@ -868,6 +1022,12 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   // SM sub-partition's issue slot (the scheduler favours higher warp ids).
   if (blockIdx.x == 0) {
     if (threadIdx.x >= 32) return;
+    if (a.mode == 1) {
+      __shared__ int s_staged[kMaxP], s_sidx[kMaxP];
+      if constexpr (CTL == 2 || CTL == 4 || CTL == 8) control_warp_replay<CTL>(a, &s.gate, s_staged, s_sidx);
+      else control_warp_replay<0>(a, &s.gate, s_staged, s_sidx);
+      return;
+    }
     if constexpr (CTL == 32) control_warp_lanes(a);
     else if constexpr (CTL > 0) control_warp_regs<CTL>(a);
     else control_warp(a, s);
@@ -903,6 +1063,35 @@ int grow(ps_server* h, T** p, size_t* cap, size_t need) {
   *p = nullptr;
   PS_CK(h, cudaMalloc((void**)p, need * sizeof(T)));
   *cap = need;
+  return PS_OK;
+}
+
+// One CTA per SM; the weight slice of every data warp lives in registers when
+// it fits V float4 per lane (V in {1,2,4,8,16}), else in HBM (V = 0); the
+// control warp's layout follows P (see k_sim).
+int select_loop_kernel(ps_server* h, int P, int data_ctas, int* grid_out, const void** kern_out) {
+  int grid = data_ctas > 0 ? data_ctas + 1 : h->sm_count;
+  if (grid > h->sm_count) grid = h->sm_count;
+  if (grid < 2) grid = 2;
+  const long long dwarps = (long long)(grid - 1) * (kSimThreads / 32);
+  const long long per = (h->nv + dwarps - 1) / dwarps;
+  const long long need_v = (per + 31) / 32;
+  const int vi = need_v <= 1 ? 0 : need_v <= 2 ? 1 : need_v <= 4 ? 2 : need_v <= 8 ? 3 : need_v <= 16 ? 4 : 5;
+  const int pi = P <= 2 ? 0 : P <= 4 ? 1 : P <= 8 ? 2 : P <= kLaneP ? 3 : 4;
+  static const void* const table[6][5] = {
+      {(const void*)k_sim<1, 2>, (const void*)k_sim<1, 4>, (const void*)k_sim<1, 8>, (const void*)k_sim<1, 32>, (const void*)k_sim<1, 0>},
+      {(const void*)k_sim<2, 2>, (const void*)k_sim<2, 4>, (const void*)k_sim<2, 8>, (const void*)k_sim<2, 32>, (const void*)k_sim<2, 0>},
+      {(const void*)k_sim<4, 2>, (const void*)k_sim<4, 4>, (const void*)k_sim<4, 8>, (const void*)k_sim<4, 32>, (const void*)k_sim<4, 0>},
+      {(const void*)k_sim<8, 2>, (const void*)k_sim<8, 4>, (const void*)k_sim<8, 8>, (const void*)k_sim<8, 32>, (const void*)k_sim<8, 0>},
+      {(const void*)k_sim<16, 2>, (const void*)k_sim<16, 4>, (const void*)k_sim<16, 8>, (const void*)k_sim<16, 32>, (const void*)k_sim<16, 0>},
+      {(const void*)k_sim<0, 2>, (const void*)k_sim<0, 4>, (const void*)k_sim<0, 8>, (const void*)k_sim<0, 32>, (const void*)k_sim<0, 0>}};
+  const void* kern = table[vi][pi];
+  int per_sm = 0;
+  PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimThreads, 0));
+  if (grid > per_sm * h->sm_count) grid = per_sm * h->sm_count;
+  if (grid < 2) return ps_fail(h, PS_E_CUDA, "k_sim cannot be resident");
+  *grid_out = grid;
+  *kern_out = kern;
   return PS_OK;
 }
 
@@ -983,28 +1172,9 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   PS_CK(h, cudaMemsetAsync(b.out, 0, sizeof(SimOut), h->stream));
   PS_CK(h, cudaMemsetAsync(b.losses, 0, loss_need * sizeof(double), h->stream));
 
-  // one CTA per SM; the weight slice of every data warp lives in registers
-  // when it fits V float4 per lane (V in {1,2,4,8,16}), else in HBM (V = 0)
-  int grid = sc->data_ctas > 0 ? sc->data_ctas + 1 : h->sm_count;
-  if (grid > h->sm_count) grid = h->sm_count;
-  if (grid < 2) grid = 2;
-  const long long dwarps = (long long)(grid - 1) * (kSimThreads / 32);
-  const long long per = (h->nv + dwarps - 1) / dwarps;
-  const long long need_v = (per + 31) / 32;
-  const int vi = need_v <= 1 ? 0 : need_v <= 2 ? 1 : need_v <= 4 ? 2 : need_v <= 8 ? 3 : need_v <= 16 ? 4 : 5;
-  const int pi = P <= 2 ? 0 : P <= 4 ? 1 : P <= 8 ? 2 : P <= kLaneP ? 3 : 4;
-  static const void* const table[6][5] = {
-      {(const void*)k_sim<1, 2>, (const void*)k_sim<1, 4>, (const void*)k_sim<1, 8>, (const void*)k_sim<1, 32>, (const void*)k_sim<1, 0>},
-      {(const void*)k_sim<2, 2>, (const void*)k_sim<2, 4>, (const void*)k_sim<2, 8>, (const void*)k_sim<2, 32>, (const void*)k_sim<2, 0>},
-      {(const void*)k_sim<4, 2>, (const void*)k_sim<4, 4>, (const void*)k_sim<4, 8>, (const void*)k_sim<4, 32>, (const void*)k_sim<4, 0>},
-      {(const void*)k_sim<8, 2>, (const void*)k_sim<8, 4>, (const void*)k_sim<8, 8>, (const void*)k_sim<8, 32>, (const void*)k_sim<8, 0>},
-      {(const void*)k_sim<16, 2>, (const void*)k_sim<16, 4>, (const void*)k_sim<16, 8>, (const void*)k_sim<16, 32>, (const void*)k_sim<16, 0>},
-      {(const void*)k_sim<0, 2>, (const void*)k_sim<0, 4>, (const void*)k_sim<0, 8>, (const void*)k_sim<0, 32>, (const void*)k_sim<0, 0>}};
-  const void* kern = table[vi][pi];
-  int per_sm = 0;
-  PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimThreads, 0));
-  if (grid > per_sm * h->sm_count) grid = per_sm * h->sm_count;
-  if (grid < 2) return ps_fail(h, PS_E_CUDA, "k_sim cannot be resident");
+  int grid = 0;
+  const void* kern = nullptr;
+  if ((rc = select_loop_kernel(h, P, sc->data_ctas, &grid, &kern))) return rc;
 
   SimArgs a{};
   a.P = P;
@@ -1079,6 +1249,125 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
     res->status = PS_E_DEADLOCK;
     return ps_fail(h, PS_E_DEADLOCK, "simulation deadlocked");
   }
+  return PS_OK;
+}
+
+int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const float* synthetic,
+                  int32_t n_synthetic, int32_t reset_gate, int32_t data_ctas, ps_sim_result* res) {
+  DevGuard guard(h->dev);
+  std::memset(res, 0, sizeof(*res));
+  const int P = h->cfg.worker_count;
+  if (n < 0 || (n > 0 && !calls)) return ps_fail(h, PS_E_VALUE, "bad call list");
+  if (!synthetic || n_synthetic < 1) return ps_fail(h, PS_E_VALUE, "replay needs resident updates");
+  ps_sim_buffers& b = h->sim;
+  int rc;
+  size_t cap;
+  const size_t ops = 2 * (size_t)n + 8;  // a GRAD and an APPLY per apply call at most
+  if (b.ops_cap < ops || !b.ops) {
+    cudaFree(b.ops);
+    b.ops = nullptr;
+    PS_CK(h, cudaMalloc(&b.ops, ops * sizeof(Op)));
+    PS_CK(h, cudaMemsetAsync(b.ops, 0, ops * sizeof(Op), h->stream));
+    b.ops_cap = ops;
+    b.tag = 0;
+  }
+  b.tag = (b.tag + 1) & 0xffffu;
+  if (b.tag == 0) {
+    PS_CK(h, cudaMemsetAsync(b.ops, 0, b.ops_cap * sizeof(Op), h->stream));
+    b.tag = 1;
+  }
+  const size_t slots = (size_t)n + 1;
+  if (b.slots_cap < slots || !b.gcount) {
+    cudaFree(b.gcount);
+    b.gcount = nullptr;
+    PS_CK(h, cudaMalloc(&b.gcount, slots * sizeof(unsigned)));
+    b.slots_cap = slots;
+  }
+  if (!b.out) PS_CK(h, cudaMalloc(&b.out, sizeof(SimOut)));
+  if (b.P != P || !b.rep) {
+    cudaFree(b.rep); cudaFree(b.gbuf);
+    b.rep = nullptr; b.gbuf = nullptr;
+    PS_CK(h, cudaMalloc(&b.rep, (size_t)P * 2 * h->dpad * sizeof(float)));
+    PS_CK(h, cudaMalloc(&b.gbuf, (size_t)P * h->dpad * sizeof(float)));
+    b.P = P;
+  }
+  cap = b.calls_cap;
+  if ((rc = grow(h, (ReplayCall**)&b.calls, &cap, (size_t)n + 1))) return rc;
+  b.calls_cap = cap;
+  cap = b.dec_cap;
+  if ((rc = grow(h, &b.decisions, &cap, (size_t)n + 1))) return rc;
+  b.dec_cap = cap;
+  if (n) PS_CK(h, cudaMemcpyAsync(b.calls, calls, (size_t)n * sizeof(ReplayCall), cudaMemcpyHostToDevice,
+                                  h->stream));
+  PS_CK(h, cudaMemsetAsync(b.gcount, 0, slots * sizeof(unsigned), h->stream));
+  PS_CK(h, cudaMemsetAsync(b.out, 0, sizeof(SimOut), h->stream));
+  int grid = 0;
+  const void* kern = nullptr;
+  if ((rc = select_loop_kernel(h, P, data_ctas, &grid, &kern))) return rc;
+  SimArgs a{};
+  a.mode = 1;
+  a.P = P;
+  a.grad_kind = PS_GRAD_SYNTHETIC;
+  a.n_synth = n_synthetic;
+  a.reset_gate = reset_gate;
+  a.nv = h->nv;
+  a.dpad = h->dpad;
+  a.trace_cap = (long long)b.dec_cap;
+  a.ops_cap = (long long)ops;
+  a.lr = (float)h->cfg.learning_rate;
+  a.W = h->w[h->cur];
+  a.rep = b.rep;
+  a.gbuf = b.gbuf;
+  a.synth = synthetic;
+  a.ops = (Op*)b.ops;
+  a.gword = b.gcount;
+  a.tag = b.tag;
+  a.n_ctas = (unsigned)(grid - 1);
+  a.calls = (const ReplayCall*)b.calls;
+  a.n_calls = n;
+  a.decisions = b.decisions;
+  a.ctrl = h->ctrl;
+  a.out = (SimOut*)b.out;
+  a.n_data_warps = (unsigned)((grid - 1) * (kSimThreads / 32));
+  a.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  a.base_version = h->hctrl->gate.version;
+  void* args[] = {&a};
+  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  PS_CK(h, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSimThreads), args, 0, h->stream));
+  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
+  k_sim_finish<<<1, 1, 0, h->stream>>>(h->ctrl, (SimOut*)b.out);
+  PS_CK(h, cudaGetLastError());
+  SimOut o{};
+  PS_CK(h, cudaMemcpyAsync(&o, b.out, sizeof(SimOut), cudaMemcpyDeviceToHost, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  h->last_ms = ms;
+  PS_CK(h, cudaMemcpy(h->hctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+  h->cur = h->hctrl->cur;
+  res->events = o.events;
+  res->pushes = o.pushes;
+  res->applied = o.applied;
+  res->rejected = o.rejected;
+  res->trace_rows = o.trace_rows;
+  res->status = o.status;
+  res->diverged_worker = o.diverged_worker;
+  res->device_ms = ms;
+  res->control_ms = o.t_control_done > o.t_start ? (o.t_control_done - o.t_start) * 1e-6 : 0.0;
+  res->data_ms = o.t_data_done > o.t_start ? (o.t_data_done - o.t_start) * 1e-6 : 0.0;
+  b.last_decisions = o.trace_rows;
+  if (o.status == PS_E_TIMEOUT) return ps_fail(h, PS_E_TIMEOUT, "device watchdog fired in ps_replay_run");
+  if (o.status == PS_E_DIVERGED)
+    return ps_fail(h, PS_E_DIVERGED, "weights went non-finite on worker " + std::to_string(o.diverged_worker));
+  if (o.status == PS_E_PROTOCOL) return ps_fail(h, PS_E_PROTOCOL, "protocol violation in the replayed calls");
+  return PS_OK;
+}
+
+int ps_replay_decisions(ps_server* h, int64_t* out, int64_t cap, int64_t* n) {
+  DevGuard guard(h->dev);
+  *n = h->sim.last_decisions;
+  const int64_t m = h->sim.last_decisions < cap ? h->sim.last_decisions : cap;
+  if (m > 0) PS_CK(h, cudaMemcpy(out, h->sim.decisions, m * sizeof(int64_t), cudaMemcpyDeviceToHost));
   return PS_OK;
 }
 

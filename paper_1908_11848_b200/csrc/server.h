@@ -18,6 +18,10 @@ struct ps_sim_buffers {
   ps_trace_row* trace = nullptr;
   double* losses = nullptr;
   void* out = nullptr;                 // SimOut
+  void* calls = nullptr;               // replay: ps_replay_call[calls_cap]
+  long long* decisions = nullptr;      // replay: one word per decide
+  size_t calls_cap = 0, dec_cap = 0;
+  int64_t last_decisions = 0;
   int64_t last_trace_rows = 0, last_loss_samples = 0, last_loss_every = 0, last_base_version = 0;
 };
 

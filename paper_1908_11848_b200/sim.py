@@ -125,6 +125,64 @@ def run_device_simulation(config, grad="bowl", device: int = 0, **kw):
     return DeviceSimulation(config, grad=grad, device=device).run(**kw)
 
 
+CALL_PULL, CALL_APPLY, CALL_DECIDE = 0, 1, 2
+_CALL_DTYPE = np.dtype([("now", np.float64), ("kind", np.int32), ("worker", np.int32)])
+
+
+@dataclass
+class ReplayReport:
+    decisions: list      # [(outcome, released tuple)] per decide
+    applied: int
+    rejected: int
+    pushes: int
+    device_ms: float
+
+    @property
+    def updates_per_s(self) -> float:
+        return self.applied / (self.device_ms * 1e-3) if self.device_ms > 0 else 0.0
+
+
+class DeviceReplay:
+    """The server serving a recorded request stream on the device: the
+    reference's boundary calls (see calls_from_trace) replayed in one
+    persistent kernel, decisions by the device gate (ps_replay_run)."""
+
+    def __init__(self, engine, calls, synthetic, count):
+        self.engine = engine
+        arr = np.zeros(len(calls), dtype=_CALL_DTYPE)
+        for i, c in enumerate(calls):
+            if c[0] == "pull":
+                arr[i] = (0.0, CALL_PULL, c[1])
+            elif c[0] == "apply":
+                arr[i] = (0.0, CALL_APPLY, c[1])
+            else:
+                arr[i] = (float(c[2]), CALL_DECIDE, c[1])
+        self.calls = arr
+        self.synthetic = synthetic
+        self.count = int(count)
+
+    def run(self, reset_gate=True, data_ctas=0, decisions=True):
+        res = _lib.PSSimResult()
+        lib = self.engine.lib
+        rc = lib.ps_replay_run(self.engine.handle, self.calls.ctypes.data, len(self.calls),
+                               self.synthetic.data_ptr(), self.count, 1 if reset_gate else 0,
+                               int(data_ctas), ctypes.byref(res))
+        raise_for(rc, self.engine.error())
+        out = []
+        if decisions:
+            n = res.trace_rows
+            buf = (ctypes.c_int64 * max(n, 1))()
+            got = ctypes.c_int64(0)
+            self.engine.check(lib.ps_replay_decisions(self.engine.handle, buf, n, ctypes.byref(got)))
+            for i in range(n):
+                v = buf[i]
+                rel = tuple(q for q in range(56) if (v >> (8 + q)) & 1)
+                out.append(("grant" if (v & 0xff) == 0 else "defer", rel))
+        self.engine.refresh()
+        return ReplayReport(decisions=out, applied=res.applied, rejected=res.rejected,
+                            pushes=res.pushes, device_ms=res.device_ms)
+
+
 def calls_from_trace(entries):
     """The server-call sequence a host driver makes for this trace, in the
     reference's order (simnet.py:127-201): ("pull", w) at PULL_ARRIVE, and for
