@@ -8,13 +8,13 @@
 //
 // One step = one same-instant push group of all G workers (the homogeneous
 // schedule of simnet.py:167-201: apply every update in seq order, then decide
-// each), ONE kernel per step on every rank, with no host in the loop and no
-// collective (all of its CTAs are co-resident by construction):
+// each). A whole run of steps is ONE persistent cooperative kernel on every
+// rank (k_shard_run), with no host in the loop and no collective; per step:
 //
-//   push              CTA 0 of rank r's kernel: once every owner's slice of
-//                     worker r's previous pull has landed, release-store
-//                     ready = t into every owner's flag array.
-//   k_shard_apply     owner r waits for all G ready flags, then streams its
+//   push              CTA 0 of rank r: once every owner's slice of worker r's
+//                     previous pull has landed, release-store ready = t into
+//                     every owner's flag array.
+//   data CTAs         owner r waits for all G ready flags, then streams its
 //                     shard once: w' = w - lr*g_p for p in ticket order, each
 //                     g_p slice read straight from worker p's HBM over NVLink
 //                     (P2P loads, payload crosses once), w' written to the back
@@ -63,8 +63,7 @@ struct ShardPtrs {
 
 struct ShardCtl {
   ps_gate_state gate;
-  uint32_t arrive[3];
-  uint32_t bad;
+  uint32_t bad;       // this step's non-finite bits (per ticket) and result bit 31
   int32_t status;
   int32_t _pad;
   unsigned long long trace_n;
@@ -74,7 +73,17 @@ struct ShardCtl {
   // which every later event of the homogeneous chain inherits.
   int32_t order[2][kMaxRanks];  // [step parity]: this group's order, the next one's
   int32_t cur;  // which shard buffer holds the current weights
+  int32_t _pad2;
+  unsigned long long arrive_total;  // data-CTA arrivals over all steps (election)
+  unsigned long long gate_done;     // last step whose decisions and next order are written
+  unsigned long long committed;     // last step committed by the last data CTA
 };
+
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 struct IpcBlob {
   cudaIpcMemHandle_t w, upd, rep, flags;
@@ -101,24 +110,6 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
   return true;
 }
 
-// Last-CTA election; returns true in exactly one CTA (counter k is reset).
-// CTAs that stored to peer memory fence at system scope before arriving so
-// the winner's system-scope release covers their remote stores; CTAs that
-// only read need a GPU-scope fence.
-__device__ bool last_cta(ShardCtl* ctl, int k, bool wrote_remote, int participants) {
-  __shared__ int s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (wrote_remote) __threadfence_system();
-    else __threadfence();
-    const unsigned prev = atomicAdd(&ctl->arrive[k], 1u);
-    s_last = (prev == (unsigned)participants - 1);
-    if (s_last) ctl->arrive[k] = 0;
-  }
-  __syncthreads();
-  return s_last;
-}
-
 // End of a run: this rank's replica holds every owner's slice of step t.
 __global__ void k_shard_wait_pulled(ShardPtrs P, int G, int me, unsigned long long t, ShardCtl* ctl) {
   if (threadIdx.x == 0) wait_flags(P.flags[me] + G, G, t, nullptr, ctl);
@@ -126,13 +117,13 @@ __global__ void k_shard_wait_pulled(ShardPtrs P, int G, int me, unsigned long lo
 
 template <int G_MAX>
 __global__ void __launch_bounds__(kThreads)
-k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local, ShardPtrs P, int G,
-              int me, unsigned long long t, float lr, ShardCtl* ctl, double now, ps_trace_row* trace,
-              long long trace_cap) {
-  const int cur_order = (int)(t & 1);
-  // ---- the gate CTA: the replicated decisions for this group ------------
+k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, ShardPtrs P, int G,
+            int me, unsigned long long t0, int steps, float lr, ShardCtl* ctl, const double* now,
+            ps_trace_row* trace, long long trace_cap) {
+  const int ndata = gridDim.x - 1;
+  // ---- the gate CTA: the replicated decisions, one group per step --------
   // They depend only on (worker, now) and the gate tables, never on the data,
-  // so one extra CTA runs them from shared memory while the others stream.
+  // so this CTA runs them from shared memory while the data CTAs stream.
   if (blockIdx.x == gridDim.x - 1) {
     if (threadIdx.x >= 32) return;
     __shared__ ps_gate_state sg;
@@ -142,41 +133,55 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
       for (int i = threadIdx.x; i < (int)(sizeof(ps_gate_state) / 8); i += 32) d[i] = s[i];
     }
     __syncwarp();
-    int next[kMaxRanks];
-    int n_next = 0;
     int status = PS_OK;
-    for (int i = 0; i < G; ++i) {
-      const int p = ctl->order[cur_order][i];
-      const GateResult r = gate_on_push(&sg, p, now);
+    for (int i = 0; i < steps && status == PS_OK; ++i) {
+      const unsigned long long t = t0 + i;
+      const int co = (int)(t & 1);
       if (threadIdx.x == 0) {
-        if (r.status != PS_OK) status = r.status;
-        if (r.status == PS_OK && r.outcome == 0) {
-          next[n_next++] = p;
-          for (int q = 0; q < G; ++q)
-            if ((r.released >> q) & 1ull) next[n_next++] = q;
-        }
-        const unsigned long long n = ctl->trace_n++;
-        if ((long long)n < trace_cap) {
-          ps_trace_row row;
-          row.time = now;
-          row.worker = p;
-          row.kind = PS_EV_PUSH_ARRIVE;
-          row.count = sg.clocks[p];
-          row.decision = r.outcome;
-          row._pad = 0;
-          row.released = r.released;
-          trace[n] = row;
+        // order[co ^ 1] is still read by stragglers of step t-1 until it commits
+        const unsigned long long s0 = globaltimer_ns();
+        while (ld_acquire_u64(&ctl->committed) + 1 < t) {
+          if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); break; }
+          __nanosleep(32);
         }
       }
       __syncwarp();
+      int next[kMaxRanks];
+      int n_next = 0;
+      for (int k = 0; k < G; ++k) {
+        const int p = ctl->order[co][k];
+        const GateResult r = gate_on_push(&sg, p, now[i]);
+        if (threadIdx.x == 0) {
+          if (r.status != PS_OK) status = r.status;
+          if (r.status == PS_OK && r.outcome == 0) {
+            next[n_next++] = p;
+            for (int q = 0; q < G; ++q)
+              if ((r.released >> q) & 1ull) next[n_next++] = q;
+          }
+          const unsigned long long n = ctl->trace_n++;
+          if ((long long)n < trace_cap) {
+            ps_trace_row row;
+            row.time = now[i];
+            row.worker = p;
+            row.kind = PS_EV_PUSH_ARRIVE;
+            row.count = sg.clocks[p];
+            row.decision = r.outcome;
+            row._pad = 0;
+            row.released = r.released;
+            trace[n] = row;
+          }
+        }
+        __syncwarp();
+      }
+      if (threadIdx.x == 0) {
+        // every worker must be back for the next group (homogeneous schedule)
+        if (status == PS_OK && n_next != G) status = PS_E_PROTOCOL;
+        if (status != PS_OK) atomicCAS(&ctl->status, PS_OK, status);
+        for (int k = 0; k < n_next && k < G; ++k) ctl->order[co ^ 1][k] = next[k];
+        st_release_u64(&ctl->gate_done, t);
+      }
+      status = __shfl_sync(kFull, status, 0);
     }
-    if (threadIdx.x == 0) {
-      // every worker must be back for the next group (homogeneous schedule)
-      if (status == PS_OK && n_next != G) status = PS_E_PROTOCOL;
-      if (status != PS_OK) atomicCAS(&ctl->status, PS_OK, status);
-      for (int i = 0; i < n_next && i < G; ++i) ctl->order[cur_order ^ 1][i] = next[i];
-    }
-    __syncwarp();
     // tables back (version / rejected belong to the committing CTA)
     for (int q = threadIdx.x; q < G; q += 32) {
       ctl->gate.clocks[q] = sg.clocks[q];
@@ -191,134 +196,155 @@ k_shard_apply(float* __restrict__ w0, float* __restrict__ w1, long long n_local,
     }
     return;
   }
-  // ---- data CTAs ----------------------------------------------------------
+  // ---- data CTAs: one push group per step ---------------------------------
   __shared__ unsigned s_bits;
-  if (threadIdx.x == 0) {
-    s_bits = 0;
-    // worker `me` pushes its update for step t once every owner's slice of
-    // its previous pull has landed (CTA 0 publishes for the whole rank)
-    bool ok = true;
-    if (blockIdx.x == 0) {
-      ok = t <= 1 || wait_flags(P.flags[me] + G, G, t - 1, nullptr, ctl);
-      if (ok) {
-        __threadfence_system();
-        for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, t);
-      }
-    }
-    if (!ok || !wait_flags(P.flags[me], G, t, nullptr, ctl)) s_bits = 0xffffffffu;
-  }
-  __syncthreads();
-  if (s_bits == 0xffffffffu) return;  // watchdog fired
-  const long long nv = (n_local + 3) >> 2;
-  const long long lo = P.lo[me];
-  const int cur = ctl->cur;
-  const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
-  float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
-  const float4* src[G_MAX];
-#pragma unroll
-  for (int i = 0; i < G_MAX; ++i)
-    src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? ctl->order[cur_order][i] : 0] + lo);
-  unsigned dbad = 0;
-  unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
-  // Optimistic single pass: apply all G updates in ticket order into the back
-  // buffer and every worker's replica while scanning the update slices; the
-  // verdict exchange below commits it (or redoes it without the rejected
-  // updates, the rare path). U consecutive float4 per thread per trip with all
-  // G slices loaded first: U*G independent 128-bit loads in flight.
-  constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
-  const int ndata = gridDim.x - 1;
-  const long long stride = (long long)ndata * kThreads * U;
-  for (long long base = (long long)blockIdx.x * kThreads * U + threadIdx.x; base < nv; base += stride) {
-    float4 g[U][G_MAX];
-    float4 x[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long j = base + (long long)u * kThreads;
-      if (j < nv) {
-#pragma unroll
-        for (int i = 0; i < G_MAX; ++i)
-          if (i < G) g[u][i] = ld_stream(src[i] + j);
-        x[u] = wsrc[j];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long j = base + (long long)u * kThreads;
-      if (j < nv) {
-#pragma unroll
-        for (int i = 0; i < G_MAX; ++i)
-          if (i < G) {
-            gbad |= nonfinite4(g[u][i]) ? (1u << i) : 0u;
-            x[u] = apply4(x[u], lr, g[u][i]);
-          }
-        dbad |= nonfinite4(x[u]) ? 1u : 0u;
-        wdst[j] = x[u];
-        // every worker's pull of this slice (handle_pull, server.py:84-91):
-        // stored straight into each replica, G-1 of them over NVLink
-#pragma unroll
-        for (int q = 0; q < G_MAX; ++q)
-          if (q < G) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x[u];
-      }
-    }
-  }
-  gbad = __reduce_or_sync(kFull, gbad);
-  dbad = __reduce_or_sync(kFull, dbad);
-  if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
-  __syncthreads();
-  if (threadIdx.x == 0 && s_bits) atomicOr(&ctl->bad, s_bits);
-  if (!last_cta(ctl, 1, true, ndata)) return;
-  // ---- last data CTA: verdict exchange, commit ----------------------------
+  __shared__ int s_last;
   __shared__ unsigned long long s_rej;
   __shared__ int s_div;
-  if (threadIdx.x == 0) {
-    const unsigned b = atomicExch(&ctl->bad, 0u);
-    unsigned long long mine = 0;  // rejected pushers as worker-id bits
-    for (int i = 0; i < G; ++i)
-      if ((b >> i) & 1u) mine |= 1ull << ctl->order[cur_order][i];
-    // every owner saw a different slice of each update: the reference rejects
-    // an update if ANY element is non-finite (server.py:65-67)
-    __threadfence_system();
-    for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | mine);
-    unsigned long long rej = 0;
-    const unsigned long long t0 = globaltimer_ns();
-    for (int s = 0; s < G; ++s) {
-      unsigned long long v;
-      while (((v = ld_acquire_sys_u64(P.flags[me] + 2 * G + s)) >> 32) < t) {
-        if (globaltimer_ns() - t0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); v = 0; break; }
-        __nanosleep(20);
+  const long long nv = (n_local + 3) >> 2;
+  const long long lo = P.lo[me];
+  for (int step = 0; step < steps; ++step) {
+    const unsigned long long t = t0 + step;
+    const int co = (int)(t & 1);
+    if (threadIdx.x == 0) {
+      s_bits = 0;
+      bool ok = true;
+      // worker `me` pushes its update for step t once every owner's slice of
+      // its previous pull has landed (CTA 0 publishes for the whole rank)
+      if (blockIdx.x == 0) {
+        ok = t <= 1 || wait_flags(P.flags[me] + G, G, t - 1, nullptr, ctl);
+        if (ok) {
+          __threadfence_system();
+          for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, t);
+        }
       }
-      rej |= v & 0xffffffffull;
+      ok = ok && wait_flags(P.flags[me], G, t, nullptr, ctl);
+      // this group's ticket order is final once the gate finished step t-1
+      const unsigned long long s0 = globaltimer_ns();
+      while (ok && ld_acquire_u64(&ctl->gate_done) + 1 < t) {
+        if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); ok = false; }
+        __nanosleep(32);
+      }
+      if (!ok) s_bits = 0xffffffffu;
     }
-    s_rej = rej;
-    s_div = (b >> 31) & 1u;
-  }
-  __syncthreads();
-  const unsigned long long rej = s_rej;
-  if (rej) {
-    // rare path: recompute this slice without the rejected updates
-    unsigned redo_bad = 0;
-    for (long long j = threadIdx.x; j < nv; j += kThreads) {
-      float4 x = wsrc[j];
-      for (int i = 0; i < G; ++i)
-        if (!((rej >> ctl->order[cur_order][i]) & 1ull)) x = apply4(x, lr, src[i][j]);
-      redo_bad |= nonfinite4(x) ? 1u : 0u;
-      wdst[j] = x;
-      for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
-    }
-    if (__syncthreads_or(redo_bad)) s_div = 1;
-    else if (threadIdx.x == 0) s_div = 0;
     __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (s_div) {
-      atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);  // weights stay at w[cur]
-    } else {
-      ctl->cur = cur ^ 1;
-      ctl->gate.version += G - __popcll(rej);
-      ctl->gate.rejected += __popcll(rej);
+    if (s_bits == 0xffffffffu) return;  // watchdog fired
+    const int cur = ld_relaxed_s32(&ctl->cur);
+    const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
+    float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
+    const float4* src[G_MAX];
+#pragma unroll
+    for (int i = 0; i < G_MAX; ++i)
+      src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? ctl->order[co][i] : 0] + lo);
+    unsigned dbad = 0;
+    unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
+    // Optimistic single pass: apply all G updates in ticket order into the
+    // back buffer and every worker's replica while scanning the update
+    // slices; the verdict exchange below commits it (or redoes it without
+    // the rejected updates, the rare path). U consecutive float4 per thread
+    // per trip with all G slices loaded first: U*G independent 128-bit loads
+    // in flight, G-1 of every G over NVLink.
+    constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
+    const long long stride = (long long)ndata * kThreads * U;
+    for (long long base = (long long)blockIdx.x * kThreads * U + threadIdx.x; base < nv; base += stride) {
+      float4 g[U][G_MAX];
+      float4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long j = base + (long long)u * kThreads;
+        if (j < nv) {
+#pragma unroll
+          for (int i = 0; i < G_MAX; ++i)
+            if (i < G) g[u][i] = ld_stream(src[i] + j);
+          x[u] = wsrc[j];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long j = base + (long long)u * kThreads;
+        if (j < nv) {
+#pragma unroll
+          for (int i = 0; i < G_MAX; ++i)
+            if (i < G) {
+              gbad |= nonfinite4(g[u][i]) ? (1u << i) : 0u;
+              x[u] = apply4(x[u], lr, g[u][i]);
+            }
+          dbad |= nonfinite4(x[u]) ? 1u : 0u;
+          wdst[j] = x[u];
+          // every worker's pull of this slice (handle_pull, server.py:84-91):
+          // stored straight into each replica, G-1 of them over NVLink
+#pragma unroll
+          for (int q = 0; q < G_MAX; ++q)
+            if (q < G) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x[u];
+        }
+      }
     }
-    __threadfence_system();
-    for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, t);
+    gbad = __reduce_or_sync(kFull, gbad);
+    dbad = __reduce_or_sync(kFull, dbad);
+    if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_bits) atomicOr(&ctl->bad, s_bits);
+      // stores to peers are covered by the winner's system-scope release
+      __threadfence_system();
+      const unsigned long long prev = atomicAdd(&ctl->arrive_total, 1ull);
+      s_last = prev == t * (unsigned long long)ndata - 1;
+    }
+    __syncthreads();
+    if (!s_last) continue;
+    // ---- last data CTA of the step: verdict exchange, commit -------------
+    if (threadIdx.x == 0) {
+      const unsigned b = atomicExch(&ctl->bad, 0u);
+      unsigned long long mine = 0;  // rejected pushers as worker-id bits
+      for (int i = 0; i < G; ++i)
+        if ((b >> i) & 1u) mine |= 1ull << ctl->order[co][i];
+      // every owner saw a different slice of each update: the reference
+      // rejects an update if ANY element is non-finite (server.py:65-67)
+      for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | mine);
+      unsigned long long rej = 0;
+      const unsigned long long s0 = globaltimer_ns();
+      for (int s = 0; s < G; ++s) {
+        unsigned long long v;
+        while (((v = ld_acquire_sys_u64(P.flags[me] + 2 * G + s)) >> 32) < t) {
+          if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); v = 0; break; }
+          __nanosleep(20);
+        }
+        rej |= v & 0xffffffffull;
+      }
+      s_rej = rej;
+      s_div = (b >> 31) & 1u;
+    }
+    __syncthreads();
+    const unsigned long long rej = s_rej;
+    if (rej) {
+      // rare path: recompute this slice without the rejected updates
+      unsigned redo_bad = 0;
+      for (long long j = threadIdx.x; j < nv; j += kThreads) {
+        float4 x = wsrc[j];
+        for (int i = 0; i < G; ++i)
+          if (!((rej >> ctl->order[co][i]) & 1ull)) x = apply4(x, lr, src[i][j]);
+        redo_bad |= nonfinite4(x) ? 1u : 0u;
+        wdst[j] = x;
+        for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
+      }
+      if (__syncthreads_or(redo_bad)) s_div = 1;
+      else if (threadIdx.x == 0) s_div = 0;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (s_div) {
+        atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);  // weights stay at w[cur]
+      } else {
+        ctl->cur = cur ^ 1;
+        ctl->gate.version += G - __popcll(rej);
+        ctl->gate.rejected += __popcll(rej);
+      }
+      st_release_u64(&ctl->committed, t);
+      __threadfence_system();
+      for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, t);
+    }
+    __syncthreads();
+    if (s_div) return;
   }
 }
 
@@ -338,6 +364,8 @@ struct ps_shard_server {
   long long d = 0, S = 0, lo = 0, hi = 0, n_local = 0, dpad = 0;
   float* w = nullptr;                 // local shard (padded to a multiple of 4), buffer 0
   float* w_alt = nullptr;             // buffer 1 (ShardCtl::cur says which is current)
+  double* now_dev = nullptr;          // per-step push instants of the current run
+  int now_cap = 0;
   float* upd = nullptr;               // worker update buffer [dpad]
   float* rep = nullptr;               // worker replica [dpad]
   unsigned long long* flags = nullptr;
@@ -475,7 +503,7 @@ void ps_shard_destroy(ps_shard_server* h) {
   Dev guard(h->dev);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->opened) cudaIpcCloseMemHandle(p);
-  cudaFree(h->w); cudaFree(h->w_alt); cudaFree(h->upd); cudaFree(h->rep); cudaFree(h->flags); cudaFree(h->ctl);
+  cudaFree(h->w); cudaFree(h->w_alt); cudaFree(h->now_dev); cudaFree(h->upd); cudaFree(h->rep); cudaFree(h->flags); cudaFree(h->ctl);
   cudaFree(h->trace);
   if (h->hctl) cudaFreeHost(h->hctl);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -558,21 +586,32 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   }
   const int G = h->world, me = h->rank;
   const float lr = (float)h->cfg.learning_rate;
-  // CTAs per SM of the streaming kernel (tuning knob, default 4), clamped so
-  // every CTA is co-resident (CTA 0 publishes this rank's push that the other
-  // CTAs -- and the peers -- wait for), plus one gate CTA
+  // One persistent cooperative launch runs all the steps: CTAs per SM of the
+  // streaming loop (tuning knob, default 2, clamped to co-residency -- CTAs
+  // wait on each other and on peers), plus one gate CTA.
   static const int per_sm_env = [] {
     const char* v = getenv("PS_SHARD_CTAS_PER_SM");
-    const int n = v ? atoi(v) : 4;
-    return n > 0 && n <= 16 ? n : 4;
+    const int n = v ? atoi(v) : 2;
+    return n > 0 && n <= 16 ? n : 2;
   }();
-  const void* kern = G <= 2 ? (const void*)k_shard_apply<2> : G <= 4 ? (const void*)k_shard_apply<4>
-                   : G <= 8 ? (const void*)k_shard_apply<8> : (const void*)k_shard_apply<16>;
+  const void* kern = G <= 2 ? (const void*)k_shard_run<2> : G <= 4 ? (const void*)k_shard_run<4>
+                   : G <= 8 ? (const void*)k_shard_run<8> : (const void*)k_shard_run<16>;
   int resident = 0;
   SCK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kThreads, 0));
-  int data_ctas = h->sm_count * (per_sm_env < resident ? per_sm_env : resident) - 1;
-  if (data_ctas < 1) return sfail(h, PS_E_CUDA, "k_shard_apply cannot be resident");
-  const dim3 grid(data_ctas + 1), block(kThreads);
+  const int total = h->sm_count * (per_sm_env < resident ? per_sm_env : resident);
+  const int data_ctas = total - 1;
+  if (data_ctas < 1) return sfail(h, PS_E_CUDA, "k_shard_run cannot be resident");
+  if (h->now_cap < steps) {
+    cudaFree(h->now_dev);
+    h->now_dev = nullptr;
+    SCK(h, cudaMalloc(&h->now_dev, steps * sizeof(double)));
+    h->now_cap = steps;
+  }
+  SCK(h, cudaMemcpyAsync(h->now_dev, now, steps * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  // election counter and step marks continue from ticket t0 - 1
+  const unsigned long long marks[3] = {(unsigned long long)(t0 - 1) * (unsigned long long)data_ctas,
+                                       (unsigned long long)(t0 - 1), (unsigned long long)(t0 - 1)};
+  SCK(h, cudaMemcpyAsync(&h->ctl->arrive_total, marks, sizeof(marks), cudaMemcpyHostToDevice, h->stream));
   float* w0p = h->w;
   float* w1p = h->w_alt;
   long long nl = h->n_local;
@@ -580,37 +619,32 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   ShardCtl* ctl = h->ctl;
   ps_trace_row* trace = h->trace;
   long long tcap = h->trace_cap;
-  int Gv = G, mev = me;
+  int Gv = G, mev = me, nsteps = steps;
+  unsigned long long t0v = (unsigned long long)t0;
   float lrv = lr;
+  const double* nowp = h->now_dev;
+  void* args[] = {&w0p, &w1p, &nl, &ptrs, &Gv, &mev, &t0v, &nsteps, &lrv, &ctl, &nowp, &trace, &tcap};
   SCK(h, cudaEventRecord(h->ev0, h->stream));
-  for (int i = 0; i < steps; ++i) {
-    unsigned long long t = (unsigned long long)(t0 + i);
-    double nowv = now[i];
-    void* args[] = {&w0p, &w1p, &nl, &ptrs, &Gv, &mev, &t, &lrv, &ctl, &nowv, &trace, &tcap};
-    if (h->profile) cudaEventRecord(h->pev[0], h->stream);
-    SCK(h, cudaLaunchKernel(kern, grid, block, args, 0, h->stream));
-    if (h->profile) {
-      cudaEventRecord(h->pev[1], h->stream);
-      k_shard_wait_pulled<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, t, h->ctl);
-      cudaEventRecord(h->pev[2], h->stream);
-      cudaEventSynchronize(h->pev[2]);
-      for (int k = 0; k < 2; ++k) {
-        float e = 0.f;
-        cudaEventElapsedTime(&e, h->pev[k], h->pev[k + 1]);
-        h->phase_ms[k] += e;
-      }
-    }
-  }
+  SCK(h, cudaLaunchCooperativeKernel(kern, dim3(total), dim3(kThreads), args, 0, h->stream));
+  if (h->profile) SCK(h, cudaEventRecord(h->pev[0], h->stream));
   // the last step's pull: every owner's slice has landed in this replica
   k_shard_wait_pulled<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, (unsigned long long)(t0 + steps - 1), h->ctl);
   SCK(h, cudaGetLastError());
   SCK(h, cudaEventRecord(h->ev1, h->stream));
+  if (h->profile) SCK(h, cudaEventRecord(h->pev[1], h->stream));
   if (dst) SCK(h, cudaMemcpyAsync(dst, h->rep, h->d * sizeof(float), cudaMemcpyDeviceToDevice, h->stream));
   SCK(h, cudaMemcpyAsync(h->hctl, h->ctl, sizeof(ShardCtl), cudaMemcpyDeviceToHost, h->stream));
   SCK(h, cudaStreamSynchronize(h->stream));
   float e = 0.f;
   cudaEventElapsedTime(&e, h->ev0, h->ev1);
   if (ms) *ms = e;
+  if (h->profile) {
+    float k = 0.f, wt = 0.f;
+    cudaEventElapsedTime(&k, h->ev0, h->pev[0]);
+    cudaEventElapsedTime(&wt, h->pev[0], h->pev[1]);
+    h->phase_ms[0] += k;
+    h->phase_ms[1] += wt;
+  }
   const int st = h->hctl->status;
   if (st == PS_E_TIMEOUT) return sfail(h, PS_E_TIMEOUT, "device watchdog fired waiting for a peer");
   if (st == PS_E_DIVERGED) return sfail(h, PS_E_DIVERGED, "non-finite weights in the sharded server");
