@@ -143,6 +143,12 @@ typedef struct ps_sim_config {
   int64_t max_events;          /* 0: unbounded */
   int32_t data_ctas;           /* 0: one per SM minus the control CTA */
   int32_t reset_gate;          /* 1: zero the gate tables first (a fresh run) */
+  int32_t mode;                /* 0: virtual time (simnet.py); 2: free-running on the wall clock
+                                  (runner.py: each push is apply -> decide on its own, decided at
+                                  the time it actually arrives; P <= 8) */
+  int32_t _pad;
+  double time_scale;           /* mode 2: wall-clock seconds per schedule second */
+  double deadline_s;           /* mode 2: watchdog (deadline_guard, runner.py:294-298); 0 = none */
 } ps_sim_config;
 
 typedef struct ps_sim_result {
@@ -171,6 +177,10 @@ typedef struct ps_trace_row {
 } ps_trace_row;
 
 int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* out);
+/* Abort a free-running ps_sim_run from another host thread (ThreadedRun.abort,
+ * runner.py:110-111): the run stops, returns PS_E_TIMEOUT and reports its
+ * unfinished workers in ps_sim_result.unfinished. */
+int ps_abort(ps_server* h);
 
 /* Replay: the server serving a recorded request stream -- the reference's
  * boundary call sequence (handle_pull / apply_gradient / decide_push, in the

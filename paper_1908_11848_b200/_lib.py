@@ -54,7 +54,8 @@ class PSSimConfig(ctypes.Structure):
                 ("center", ctypes.c_void_p), ("center_dtype", ctypes.c_int32),
                 ("record_trace", ctypes.c_int32), ("synthetic", ctypes.c_void_p),
                 ("max_events", ctypes.c_int64), ("data_ctas", ctypes.c_int32),
-                ("reset_gate", ctypes.c_int32)]
+                ("reset_gate", ctypes.c_int32), ("mode", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("time_scale", ctypes.c_double), ("deadline_s", ctypes.c_double)]
 
 
 class PSSimResult(ctypes.Structure):
@@ -96,6 +97,7 @@ SIGNATURES = {
     "ps_apply_vectors": (ctypes.c_int, [_I32, _P, _P, _I32, _I64, _D, _P, _PI32]),
     "ps_sim_run": (ctypes.c_int, [_P, ctypes.POINTER(PSSimConfig), ctypes.POINTER(PSSimResult)]),
     "ps_sim_trace": (ctypes.c_int, [_P, ctypes.POINTER(PSTraceRow), _I64, _PI64]),
+    "ps_abort": (ctypes.c_int, [_P]),
     "ps_replay_run": (ctypes.c_int, [_P, _P, _I64, _P, _I32, _I32, _I32, ctypes.POINTER(PSSimResult)]),
     "ps_replay_decisions": (ctypes.c_int, [_P, _PI64, _I64, _PI64]),
     "ps_sim_losses": (ctypes.c_int, [_P, _PI64, _PD, _I64, _PI64]),

@@ -446,6 +446,7 @@ void ps_destroy(ps_server* h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->habort) cudaFreeHost(h->habort);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -579,6 +580,11 @@ int ps_last_kernel_ms(ps_server* h, double* ms) {
 
 int ps_set_profiling(ps_server* h, int32_t on) {
   h->profile = on ? 1 : 0;
+  return PS_OK;
+}
+
+int ps_abort(ps_server* h) {
+  if (h->habort) *reinterpret_cast<volatile int*>(h->habort) = 1;
   return PS_OK;
 }
 

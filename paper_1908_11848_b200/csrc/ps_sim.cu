@@ -71,6 +71,9 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ int ld_volatile_s32(const int* p) {
+  return p ? *reinterpret_cast<const volatile int*>(p) : 0;
+}
 
 struct ReplayCall {  // ps_replay_call
   double now;
@@ -106,7 +109,11 @@ struct SimArgs {
   unsigned n_data_warps;
   unsigned long long timeout_ns;
   long long base_version;
-  int mode;                   // 0: simulated run, 1: replay of a recorded call stream
+  int mode;                   // 0: simulated run, 1: replay of a recorded call stream,
+                              // 2: free-running (events fire on the wall clock)
+  double time_scale;          // mode 2: wall-clock seconds per schedule second
+  unsigned long long deadline_ns;  // mode 2: watchdog (deadline_guard, runner.py:294-298)
+  const int* abort_flag;      // mode 2: host-set abort (ThreadedRun.abort, runner.py:110-111)
   const struct ReplayCall* calls;
   long long n_calls;
   long long* decisions;       // replay: (released << 8) | outcome per decide
@@ -385,6 +392,12 @@ __device__ void control_warp_regs(const SimArgs& a) {
   for (int q = 0; q < PM; ++q)
     if (q < P) schedule(comm, PS_EV_PULL_ARRIVE, q);
   if (w0) a.out->t_start = globaltimer_ns();
+  const bool realtime = a.mode == 2;
+  const double ns_per_s = 1e9 * a.time_scale;  // config seconds -> wall-clock ns
+  // lanes run the loop redundantly, so every clock/flag read is lane 0's
+  const unsigned long long t_real0 = __shfl_sync(0xffffffffu, globaltimer_ns(), 0);
+  const unsigned long long deadline = t_real0 + a.deadline_ns;
+  bool aborted = false;
   PROF_DECL();
   for (;;) {
     PROF_MARK(t_a);
@@ -403,7 +416,21 @@ __device__ void control_warp_regs(const SimArgs& a) {
     PROF_MARK(t_b);
     PROF_ADD(c_pop, t_a);
     if (a.max_events > 0 && processed >= a.max_events) { status = PS_E_BUDGET; break; }
-    const double at = bt;
+    double at = bt;
+    if (realtime) {
+      // free-running (runner.py:168-291): the event fires when the wall clock
+      // reaches it and carries the time it actually fired at
+      // (the abort flag lives in host memory: poll it while idle and every
+      // 64 events, not on every event)
+      const unsigned long long due = t_real0 + (unsigned long long)(bt * ns_per_s);
+      unsigned long long nw;
+      bool stop = (processed & 63) == 0 && ld_volatile_s32(a.abort_flag);
+      while (!stop && (nw = globaltimer_ns()) < due) stop = nw > deadline || ld_volatile_s32(a.abort_flag);
+      nw = __shfl_sync(0xffffffffu, globaltimer_ns(), 0);
+      stop = __shfl_sync(0xffffffffu, stop, 0);
+      if (stop || nw > deadline) { aborted = true; break; }
+      at = (double)(nw - t_real0) / ns_per_s;
+    }
     const int kind = rget<PM>(ev_kind, w);
     rset<PM>(ev_kind, w, -1);
     processed += 1;
@@ -432,11 +459,13 @@ __device__ void control_warp_regs(const SimArgs& a) {
       schedule(at + comm, PS_EV_PULL_ARRIVE, w);
     } else {
       // PUSH_ARRIVE: every push queued at the same instant joins the group
-      // (simnet.py:167-182); the popped one first, the rest by seq.
+      // (simnet.py:167-182); the popped one first, the rest by seq. Free-
+      // running, each push is its own apply -> decide under the server lock
+      // (runner.py:226-249).
       unsigned rest = 0;
 #pragma unroll
       for (int q = 0; q < PM; ++q)
-        if (q < P && ev_kind[q] == PS_EV_PUSH_ARRIVE && ev_time[q] == at) {
+        if (!realtime && q < P && ev_kind[q] == PS_EV_PUSH_ARRIVE && ev_time[q] == at) {
           rest |= 1u << q;
           ev_kind[q] = -1;
         }
@@ -504,7 +533,9 @@ __device__ void control_warp_regs(const SimArgs& a) {
     a.out->events = processed;
     a.out->pushes = pushes;
     a.out->trace_rows = n_trace;
-    a.out->unfinished = status == PS_OK ? unfinished : 0ull;
+    // an aborted free-running run reports its stuck workers (runner.py:120-164)
+    a.out->unfinished = (status == PS_OK || aborted) ? unfinished : 0ull;
+    if (aborted) status = PS_E_TIMEOUT;
     if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
   }
 }
@@ -1104,6 +1135,14 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   std::memset(res, 0, sizeof(*res));
   const int P = h->cfg.worker_count;
   if (sc->budget < 0) return ps_fail(h, PS_E_VALUE, "budget must be >= 0");
+  if (sc->mode != 0 && sc->mode != 2) return ps_fail(h, PS_E_VALUE, "mode must be 0 or 2");
+  if (sc->mode == 2 && (P > 8 || !(sc->time_scale > 0)))
+    return ps_fail(h, PS_E_VALUE, "free-running runs need P <= 8 and time_scale > 0");
+  if (sc->mode == 2 && !h->habort) {
+    PS_CK(h, cudaHostAlloc((void**)&h->habort, sizeof(int), cudaHostAllocMapped));
+    PS_CK(h, cudaHostGetDevicePointer((void**)&h->habort_dev, h->habort, 0));
+  }
+  if (h->habort) *(volatile int*)h->habort = 0;
   if (sc->grad_kind == PS_GRAD_SYNTHETIC && (!sc->synthetic || sc->n_synthetic < 1))
     return ps_fail(h, PS_E_VALUE, "synthetic updates need a device buffer");
   if (sc->grad_kind == PS_GRAD_BOWL && !sc->center) return ps_fail(h, PS_E_VALUE, "bowl needs a center");
@@ -1210,6 +1249,12 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.base_version = h->hctrl->gate.version;
   b.last_base_version = a.base_version;
+  a.mode = sc->mode;
+  a.time_scale = sc->mode == 2 ? sc->time_scale : 1.0;
+  a.deadline_ns = sc->mode == 2 && sc->deadline_s > 0 ? (unsigned long long)(sc->deadline_s * 1e9)
+                                                      : 0xffffffffffffull;
+  a.abort_flag = sc->mode == 2 ? h->habort_dev : nullptr;
+  if (sc->mode == 2) a.timeout_ns = a.deadline_ns + 20ull * 1000 * 1000 * 1000;
   void* args[] = {&a};
   PS_CK(h, cudaEventRecord(h->ev0, h->stream));
   PS_CK(h, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSimThreads), args, 0, h->stream));
@@ -1239,7 +1284,11 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   b.last_trace_rows = res->trace_rows;
   b.last_loss_samples = res->loss_samples < a.loss_cap ? res->loss_samples : a.loss_cap;
   b.last_loss_every = sc->loss_every;
-  if (o.status == PS_E_TIMEOUT) return ps_fail(h, PS_E_TIMEOUT, "device watchdog fired in ps_sim_run");
+  if (o.status == PS_E_TIMEOUT) {
+    if (sc->mode == 2)
+      return ps_fail(h, PS_E_TIMEOUT, "free-running run aborted (deadline or abort) with workers unfinished");
+    return ps_fail(h, PS_E_TIMEOUT, "device watchdog fired in ps_sim_run");
+  }
   if (o.status == PS_E_DIVERGED)
     return ps_fail(h, PS_E_DIVERGED, "weights went non-finite on worker " + std::to_string(o.diverged_worker));
   if (o.status == PS_E_BUDGET)

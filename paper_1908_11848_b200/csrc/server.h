@@ -34,6 +34,8 @@ struct ps_server {
   dssp::Ctrl* ctrl = nullptr;          // device control block
   dssp::Ctrl* hctrl_dev = nullptr;     // device alias of the mapped host mirror hctrl
   int profile = 0;                     // 1: bracket each launch with CUDA events
+  int* habort = nullptr;               // mapped host flag: abort a free-running run
+  int* habort_dev = nullptr;
   cudaStream_t producer = nullptr;     // caller's stream that writes updates / reads pulls
   cudaEvent_t ev_in = nullptr;         // orders the server stream after `producer`
   dssp::Ctrl* hctrl = nullptr;         // pinned host mirror

@@ -38,6 +38,8 @@ class DeviceRunReport:
     final_weights: np.ndarray | None = None
     control_ms: float = 0.0
     data_ms: float = 0.0
+    completed: bool = True
+    stuck: list = field(default_factory=list)
 
     @property
     def updates_per_s(self) -> float:
@@ -72,7 +74,18 @@ class DeviceSimulation:
         self._synth_count = int(count)
 
     def run(self, record_trace=True, loss_every=None, max_events=0, data_ctas=0,
-            read_weights=True, reset_gate=False):
+            read_weights=True, reset_gate=False, realtime_scale=None, deadline_s=None):
+        """One run of the device loop.
+
+        ``realtime_scale`` switches to the free-running mode: every event
+        waits for its own wall-clock instant (simulated seconds x scale on
+        the GPU's global timer) and pushes are decided at the time they
+        actually reach the control warp, so decisions follow real arrival
+        order rather than the simulator's aggregated instants
+        (server.py:93-128 driven by real workers). ``deadline_s`` bounds the
+        run; on expiry (or :meth:`abort`) the report comes back with
+        ``completed=False`` and the workers still outstanding in ``stuck``.
+        """
         sc = _lib.PSSimConfig()
         sc.budget = self.budget
         sc.grad_kind = _lib.GRAD_BOWL if self.grad == "bowl" else _lib.GRAD_SYNTHETIC
@@ -90,13 +103,21 @@ class DeviceSimulation:
         sc.max_events = int(max_events or 0)
         sc.data_ctas = int(data_ctas)
         sc.reset_gate = 1 if reset_gate else 0
+        if realtime_scale is not None:
+            sc.mode = 2
+            sc.time_scale = float(realtime_scale)
+            sc.deadline_s = float(deadline_s or 0.0)
         res = _lib.PSSimResult()
         lib = self.engine.lib
         rc = lib.ps_sim_run(self.engine.handle, ctypes.byref(sc), ctypes.byref(res))
+        stuck = [q for q in range(self.config.worker_count) if (res.unfinished >> q) & 1]
         if rc == _lib.E_DEADLOCK:
-            raise DeadlockError([q for q in range(self.config.worker_count)
-                                 if (res.unfinished >> q) & 1])
-        raise_for(rc, self.engine.error())
+            raise DeadlockError(stuck)
+        completed = True
+        if rc == _lib.E_TIMEOUT and sc.mode == 2:
+            completed = False
+        else:
+            raise_for(rc, self.engine.error())
         entries = []
         if record_trace:
             n = res.trace_rows
@@ -118,7 +139,12 @@ class DeviceSimulation:
                                applied=res.applied, rejected=res.rejected,
                                device_ms=res.device_ms, version=int(self.engine.state.version),
                                loss_curve=curve, final_weights=weights,
-                               control_ms=res.control_ms, data_ms=res.data_ms)
+                               control_ms=res.control_ms, data_ms=res.data_ms,
+                               completed=completed, stuck=stuck if not completed else [])
+
+    def abort(self):
+        """Stop a free-running run in flight (callable from another thread)."""
+        self.engine.check(self.engine.lib.ps_abort(self.engine.handle))
 
 
 def run_device_simulation(config, grad="bowl", device: int = 0, **kw):
