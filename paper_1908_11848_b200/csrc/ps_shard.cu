@@ -76,7 +76,8 @@ struct ShardCtl {
   int32_t _pad2;
   unsigned long long arrive_total;  // data-CTA arrivals over all steps (election)
   unsigned long long gate_done;     // last step whose decisions and next order are written
-  unsigned long long committed;     // last step committed by the last data CTA
+  unsigned long long committed;     // unused (kept for the host marks layout)
+  unsigned long long redo_total;    // data-CTA arrivals at rejection redos (election)
 };
 
 __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
@@ -110,11 +111,6 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
   return true;
 }
 
-// End of a run: this rank's replica holds every owner's slice of step t.
-__global__ void k_shard_wait_pulled(ShardPtrs P, int G, int me, unsigned long long t, ShardCtl* ctl) {
-  if (threadIdx.x == 0) wait_flags(P.flags[me] + G, G, t, nullptr, ctl);
-}
-
 template <int G_MAX>
 __global__ void __launch_bounds__(kThreads)
 k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, ShardPtrs P, int G,
@@ -138,13 +134,17 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       const unsigned long long t = t0 + i;
       const int co = (int)(t & 1);
       if (threadIdx.x == 0) {
-        // order[co ^ 1] is still read by stragglers of step t-1 until it commits
+        // order[co ^ 1] is read by every data CTA at the start of step t-1
+        // (into shared memory); all of them have once they arrived there
         const unsigned long long s0 = globaltimer_ns();
-        while (ld_acquire_u64(&ctl->committed) + 1 < t) {
+        while (ld_acquire_u64(&ctl->arrive_total) < (t - 1) * (unsigned long long)ndata) {
+          // the data side stopped (divergence / a peer's watchdog): so do we
+          if (ld_relaxed_s32(&ctl->status) != PS_OK) { status = PS_E_TIMEOUT; break; }
           if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); break; }
           __nanosleep(32);
         }
       }
+      if (__shfl_sync(kFull, status, 0) != PS_OK) break;
       __syncwarp();
       int next[kMaxRanks];
       int n_next = 0;
@@ -197,56 +197,149 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     return;
   }
   // ---- data CTAs: one push group per step ---------------------------------
+  // Per step ONE cross-GPU hop: after streaming step t, owner s publishes
+  // V(t) = (t << 32 | diverged << 31 | rejected-worker bits seen in its slice)
+  // into every rank's flag array. V(t) from every owner is, at once, "every
+  // pull of step t has landed" (s wrote its slice into every replica before
+  // the release) and the global verdict (the union of the bits): the next
+  // step starts on it and commits step t first -- flip the buffers, or in the
+  // rare rejection case redo step t's slice without the rejected updates and
+  // exchange F(t) before any worker pushes again.
   __shared__ unsigned s_bits;
-  __shared__ int s_last;
+  __shared__ int s_last, s_stop, s_div;
   __shared__ unsigned long long s_rej;
-  __shared__ int s_div;
+  __shared__ int s_order[2][kMaxRanks];
   const long long nv = (n_local + 3) >> 2;
   const long long lo = P.lo[me];
-  for (int step = 0; step < steps; ++step) {
+  constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
+  const long long stride = (long long)ndata * kThreads * U;
+  const long long first = (long long)blockIdx.x * kThreads * U + threadIdx.x;
+  int cur = ld_relaxed_s32(&ctl->cur);  // the committed buffer at launch, identical in every CTA
+  long long redo_n = 0;                 // redo rounds so far (election targets)
+  const int steps_total = steps;
+  // Wait for V(t) of every owner and commit step t (see above). Returns false
+  // when the run must stop (watchdog or divergence).
+  auto resolve = [&](unsigned long long t) -> bool {
+    if (threadIdx.x == 0) {
+      unsigned long long rej = 0;
+      int div = 0, stop = 0;
+      const unsigned long long s0 = globaltimer_ns();
+      for (int s = 0; s < G && !stop; ++s) {
+        unsigned long long v;
+        while (((v = ld_acquire_sys_u64(P.flags[me] + G + s)) >> 32) < t) {
+          if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
+          __nanosleep(20);
+        }
+        rej |= v & 0x7fffffffull;
+        div |= (int)((v >> 31) & 1ull);
+      }
+      s_rej = rej; s_div = div; s_stop = stop;
+    }
+    __syncthreads();
+    if (s_stop) return false;
+    const unsigned long long rej = s_rej;
+    const int co = (int)(t & 1);
+    if (rej) {
+      // rare path: this CTA's part of the slice again, without the rejected
+      // updates (server.py:65-67), into the back buffer and every replica;
+      // the optimistic pass's divergence bit is void (it included them)
+      const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
+      float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
+      unsigned redo_bad = 0;
+      for (long long base = first; base < nv; base += stride)
+        for (int u = 0; u < U; ++u) {
+          const long long j = base + (long long)u * kThreads;
+          if (j >= nv) break;
+          float4 x = wsrc[j];
+          for (int i = 0; i < G; ++i) {
+            const int p = s_order[co][i];
+            if (!((rej >> p) & 1ull)) x = apply4(x, lr, reinterpret_cast<const float4*>(P.upd[p] + lo)[j]);
+          }
+          redo_bad |= nonfinite4(x) ? 1u : 0u;
+          wdst[j] = x;
+          for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
+        }
+      redo_bad = __syncthreads_or(redo_bad);
+      redo_n += 1;
+      if (threadIdx.x == 0) {
+        if (redo_bad) atomicOr(&ctl->bad, 1u);
+        __threadfence_system();
+        const unsigned long long prev = atomicAdd(&ctl->redo_total, 1ull);
+        if (prev == (unsigned long long)(redo_n * ndata) - 1) {  // last CTA: F(t) to every rank
+          const unsigned long long dv = atomicExch(&ctl->bad, 0u) & 1u;
+          __threadfence_system();
+          for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | dv);
+        }
+        int div = 0, stop = 0;
+        const unsigned long long s0 = globaltimer_ns();
+        for (int s = 0; s < G && !stop; ++s) {
+          unsigned long long v;
+          while (((v = ld_acquire_sys_u64(P.flags[me] + 2 * G + s)) >> 32) < t) {
+            if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
+            __nanosleep(20);
+          }
+          div |= (int)(v & 1ull);
+        }
+        s_div = div; s_stop = stop;
+      }
+      __syncthreads();
+      if (s_stop) return false;
+    }
+    if (s_div) {
+      // a non-finite result (server.py:38-41): the weights stay at w[cur]
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);
+      return false;
+    }
+    cur ^= 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctl->cur = cur;
+      ctl->gate.version += G - __popcll(rej);
+      ctl->gate.rejected += __popcll(rej);
+    }
+    return true;
+  };
+  for (int step = 0; step < steps_total; ++step) {
     const unsigned long long t = t0 + step;
     const int co = (int)(t & 1);
+    if (step > 0 && !resolve(t - 1)) return;
     if (threadIdx.x == 0) {
       s_bits = 0;
       bool ok = true;
-      // worker `me` pushes its update for step t once every owner's slice of
-      // its previous pull has landed (CTA 0 publishes for the whole rank)
-      if (blockIdx.x == 0) {
-        ok = t <= 1 || wait_flags(P.flags[me] + G, G, t - 1, nullptr, ctl);
-        if (ok) {
+      if (step == 0) {
+        // the run's first push: worker `me`'s update is in place (stream
+        // order on this rank); every owner starts once all workers pushed
+        if (blockIdx.x == 0) {
           __threadfence_system();
           for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, t);
         }
+        ok = wait_flags(P.flags[me], G, t, nullptr, ctl);
       }
-      ok = ok && wait_flags(P.flags[me], G, t, nullptr, ctl);
       // this group's ticket order is final once the gate finished step t-1
       const unsigned long long s0 = globaltimer_ns();
       while (ok && ld_acquire_u64(&ctl->gate_done) + 1 < t) {
         if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); ok = false; }
         __nanosleep(32);
       }
-      if (!ok) s_bits = 0xffffffffu;
+      if (ok)
+        for (int i = 0; i < G; ++i) s_order[co][i] = ctl->order[co][i];
+      s_stop = !ok;
     }
     __syncthreads();
-    if (s_bits == 0xffffffffu) return;  // watchdog fired
-    const int cur = ld_relaxed_s32(&ctl->cur);
+    if (s_stop) return;  // watchdog fired
     const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
     float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
     const float4* src[G_MAX];
 #pragma unroll
     for (int i = 0; i < G_MAX; ++i)
-      src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? ctl->order[co][i] : 0] + lo);
+      src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? s_order[co][i] : 0] + lo);
     unsigned dbad = 0;
     unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
     // Optimistic single pass: apply all G updates in ticket order into the
     // back buffer and every worker's replica while scanning the update
-    // slices; the verdict exchange below commits it (or redoes it without
-    // the rejected updates, the rare path). U consecutive float4 per thread
-    // per trip with all G slices loaded first: U*G independent 128-bit loads
-    // in flight, G-1 of every G over NVLink.
-    constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
-    const long long stride = (long long)ndata * kThreads * U;
-    for (long long base = (long long)blockIdx.x * kThreads * U + threadIdx.x; base < nv; base += stride) {
+    // slices. U consecutive float4 per thread per trip with all G slices
+    // loaded first: U*G independent 128-bit loads in flight, G-1 of every G
+    // over NVLink.
+    for (long long base = first; base < nv; base += stride) {
       float4 g[U][G_MAX];
       float4 x[U];
 #pragma unroll
@@ -288,64 +381,20 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       // stores to peers are covered by the winner's system-scope release
       __threadfence_system();
       const unsigned long long prev = atomicAdd(&ctl->arrive_total, 1ull);
-      s_last = prev == t * (unsigned long long)ndata - 1;
-    }
-    __syncthreads();
-    if (!s_last) continue;
-    // ---- last data CTA of the step: verdict exchange, commit -------------
-    if (threadIdx.x == 0) {
-      const unsigned b = atomicExch(&ctl->bad, 0u);
-      unsigned long long mine = 0;  // rejected pushers as worker-id bits
-      for (int i = 0; i < G; ++i)
-        if ((b >> i) & 1u) mine |= 1ull << ctl->order[co][i];
-      // every owner saw a different slice of each update: the reference
-      // rejects an update if ANY element is non-finite (server.py:65-67)
-      for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | mine);
-      unsigned long long rej = 0;
-      const unsigned long long s0 = globaltimer_ns();
-      for (int s = 0; s < G; ++s) {
-        unsigned long long v;
-        while (((v = ld_acquire_sys_u64(P.flags[me] + 2 * G + s)) >> 32) < t) {
-          if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); v = 0; break; }
-          __nanosleep(20);
-        }
-        rej |= v & 0xffffffffull;
-      }
-      s_rej = rej;
-      s_div = (b >> 31) & 1u;
-    }
-    __syncthreads();
-    const unsigned long long rej = s_rej;
-    if (rej) {
-      // rare path: recompute this slice without the rejected updates
-      unsigned redo_bad = 0;
-      for (long long j = threadIdx.x; j < nv; j += kThreads) {
-        float4 x = wsrc[j];
+      if (prev == t * (unsigned long long)ndata - 1) {
+        // last data CTA of the step: V(t) to every rank
+        const unsigned b = atomicExch(&ctl->bad, 0u);
+        unsigned long long v = (t << 32) | ((unsigned long long)(b >> 31) << 31);
         for (int i = 0; i < G; ++i)
-          if (!((rej >> ctl->order[co][i]) & 1ull)) x = apply4(x, lr, src[i][j]);
-        redo_bad |= nonfinite4(x) ? 1u : 0u;
-        wdst[j] = x;
-        for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
+          if ((b >> i) & 1u) v |= 1ull << s_order[co][i];
+        __threadfence_system();
+        for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, v);
       }
-      if (__syncthreads_or(redo_bad)) s_div = 1;
-      else if (threadIdx.x == 0) s_div = 0;
-      __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      if (s_div) {
-        atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);  // weights stay at w[cur]
-      } else {
-        ctl->cur = cur ^ 1;
-        ctl->gate.version += G - __popcll(rej);
-        ctl->gate.rejected += __popcll(rej);
-      }
-      st_release_u64(&ctl->committed, t);
-      __threadfence_system();
-      for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, t);
-    }
-    __syncthreads();
-    if (s_div) return;
   }
+  // the last step's verdict: this rank's replica is complete and committed
+  // when the kernel exits
+  resolve(t0 + steps_total - 1);
 }
 
 template <typename T>
@@ -609,8 +658,8 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   }
   SCK(h, cudaMemcpyAsync(h->now_dev, now, steps * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   // election counter and step marks continue from ticket t0 - 1
-  const unsigned long long marks[3] = {(unsigned long long)(t0 - 1) * (unsigned long long)data_ctas,
-                                       (unsigned long long)(t0 - 1), (unsigned long long)(t0 - 1)};
+  const unsigned long long marks[4] = {(unsigned long long)(t0 - 1) * (unsigned long long)data_ctas,
+                                       (unsigned long long)(t0 - 1), (unsigned long long)(t0 - 1), 0ull};
   SCK(h, cudaMemcpyAsync(&h->ctl->arrive_total, marks, sizeof(marks), cudaMemcpyHostToDevice, h->stream));
   float* w0p = h->w;
   float* w1p = h->w_alt;
@@ -627,9 +676,6 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   SCK(h, cudaEventRecord(h->ev0, h->stream));
   SCK(h, cudaLaunchCooperativeKernel(kern, dim3(total), dim3(kThreads), args, 0, h->stream));
   if (h->profile) SCK(h, cudaEventRecord(h->pev[0], h->stream));
-  // the last step's pull: every owner's slice has landed in this replica
-  k_shard_wait_pulled<<<1, 32, 0, h->stream>>>(h->ptrs, G, me, (unsigned long long)(t0 + steps - 1), h->ctl);
-  SCK(h, cudaGetLastError());
   SCK(h, cudaEventRecord(h->ev1, h->stream));
   if (h->profile) SCK(h, cudaEventRecord(h->pev[1], h->stream));
   if (dst) SCK(h, cudaMemcpyAsync(dst, h->rep, h->d * sizeof(float), cudaMemcpyDeviceToDevice, h->stream));

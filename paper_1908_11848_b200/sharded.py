@@ -269,11 +269,11 @@ def bench_main(args, metric):
                        "l2": "per-GPU working set > L2 (94 MB update + 94 MB replica + shard)"},
             "per_paradigm": {k: v for k, v in results.items() if not k.startswith("_")},
             "e2e": results["_e2e"],
-            "gpu_launches": 3 * steps,
+            "gpu_launches": 1,  # one persistent k_shard_run covers all K timed steps
             "roofline": {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s",
                          "frac": achieved / 770.0, "traffic": None,
                          "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                         "kernel": "k_shard_apply + k_shard_pull (whole step)",
+                         "kernel": "k_shard_run (persistent; whole step: push, apply, pull, verdict, gate)",
                          "bytes_model": "2*(G-1)*S*4 B received over NVLink per GPU per step"},
             "cpu_baseline": None,
             "clocks": sampler.summary() if sampler else None,

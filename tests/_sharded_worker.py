@@ -93,6 +93,33 @@ def main(out_dir):
     torch.cuda.synchronize()
     dist.barrier()
     srv.close()
+    # divergence: finite updates whose result overflows in ONE element of
+    # shard 0 -> DivergenceError on every rank, weights unchanged
+    # (server.py:38-41), and the run ends without a watchdog
+    cfg = ps.validate_config(ps.make_config(paradigm="asp", worker_count=world, dimension=d,
+                                            learning_rate=0.5, seed=3))
+    w0 = oracle.initial_weights_f64(3, d)
+    w0[7] = 3.0e38
+    srv = ShardedServer(cfg, d, rank, world, local, w0_host=w0)
+    g = oracle.synthetic_update(1, rank, 0, d)
+    if rank == 1:
+        g[7] = -3.4e38
+    srv.update[:d].copy_(torch.from_numpy(g))
+    torch.cuda.synchronize()
+    dist.barrier()
+    diverged = False
+    try:
+        srv.run([1.0])
+    except ps.DivergenceError:
+        diverged = True
+    w = w0.astype(np.float32)
+    verdict["checks"].append({
+        "run": "diverge", "d": d, "trace": diverged,
+        "shard": bool(np.array_equal(srv.read_shard().view(np.uint32), w[srv.lo:srv.hi].view(np.uint32))),
+        "replica": True, "version": int(srv.state().version), "steps": 0})
+    torch.cuda.synchronize()
+    dist.barrier()
+    srv.close()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
         json.dump(verdict, fh)
     dist.barrier()
