@@ -86,6 +86,16 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
   return v;
 }
 
+// Profiling build only (-DPS_SHARD_PROFILE, tools/libdssp_ps_prof.so): sums
+// of per-step phase durations on this rank, printed at the end of a run.
+#ifdef PS_SHARD_PROFILE
+__device__ unsigned long long g_prof[8];
+__device__ unsigned long long g_t_resolved;
+#define SPROF(stmt) stmt
+#else
+#define SPROF(stmt)
+#endif
+
 struct IpcBlob {
   cudaIpcMemHandle_t w, upd, rep, flags;
   long long lo, hi;
@@ -148,6 +158,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       __syncwarp();
       int next[kMaxRanks];
       int n_next = 0;
+      SPROF(const unsigned long long tg0 = globaltimer_ns());
       for (int k = 0; k < G; ++k) {
         const int p = ctl->order[co][k];
         const GateResult r = gate_on_push(&sg, p, now[i]);
@@ -179,6 +190,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         if (status != PS_OK) atomicCAS(&ctl->status, PS_OK, status);
         for (int k = 0; k < n_next && k < G; ++k) ctl->order[co ^ 1][k] = next[k];
         st_release_u64(&ctl->gate_done, t);
+        SPROF(g_prof[4] += globaltimer_ns() - tg0);
       }
       status = __shfl_sync(kFull, status, 0);
     }
@@ -221,6 +233,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
   // when the run must stop (watchdog or divergence).
   auto resolve = [&](unsigned long long t) -> bool {
     if (threadIdx.x == 0) {
+      SPROF(const unsigned long long tr0 = globaltimer_ns());
       unsigned long long rej = 0;
       int div = 0, stop = 0;
       const unsigned long long s0 = globaltimer_ns();
@@ -234,6 +247,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         div |= (int)((v >> 31) & 1ull);
       }
       s_rej = rej; s_div = div; s_stop = stop;
+      SPROF(if (blockIdx.x == 0) { const unsigned long long tn = globaltimer_ns(); g_prof[0] += tn - tr0; g_t_resolved = tn; })
     }
     __syncthreads();
     if (s_stop) return false;
@@ -263,12 +277,11 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       redo_n += 1;
       if (threadIdx.x == 0) {
         if (redo_bad) atomicOr(&ctl->bad, 1u);
-        __threadfence_system();
-        const unsigned long long prev = atomicAdd(&ctl->redo_total, 1ull);
+        const unsigned long long prev = atom_add_acq_rel_gpu_u64(&ctl->redo_total, 1ull);
         if (prev == (unsigned long long)(redo_n * ndata) - 1) {  // last CTA: F(t) to every rank
           const unsigned long long dv = atomicExch(&ctl->bad, 0u) & 1u;
           __threadfence_system();
-          for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | dv);
+          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | dv);
         }
         int div = 0, stop = 0;
         const unsigned long long s0 = globaltimer_ns();
@@ -310,16 +323,18 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         // order on this rank); every owner starts once all workers pushed
         if (blockIdx.x == 0) {
           __threadfence_system();
-          for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + me, t);
+          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + me, t);
         }
         ok = wait_flags(P.flags[me], G, t, nullptr, ctl);
       }
       // this group's ticket order is final once the gate finished step t-1
       const unsigned long long s0 = globaltimer_ns();
+      SPROF(const unsigned long long tw0 = globaltimer_ns());
       while (ok && ld_acquire_u64(&ctl->gate_done) + 1 < t) {
         if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); ok = false; }
         __nanosleep(32);
       }
+      SPROF(if (blockIdx.x == 0) g_prof[5] += globaltimer_ns() - tw0);
       if (ok)
         for (int i = 0; i < G; ++i) s_order[co][i] = ctl->order[co][i];
       s_stop = !ok;
@@ -378,23 +393,38 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     __syncthreads();
     if (threadIdx.x == 0) {
       if (s_bits) atomicOr(&ctl->bad, s_bits);
-      // stores to peers are covered by the winner's system-scope release
-      __threadfence_system();
-      const unsigned long long prev = atomicAdd(&ctl->arrive_total, 1ull);
+      // this CTA's stores (local and to peers) are released at GPU scope; the
+      // winner acquires them all and its fence.sc.sys orders them before V(t)
+      // at system scope (causality order is transitive across scopes) -- one
+      // system fence per step instead of one per CTA
+      const unsigned long long prev = atom_add_acq_rel_gpu_u64(&ctl->arrive_total, 1ull);
+      SPROF(if (blockIdx.x == 0) g_prof[1] += globaltimer_ns() - g_t_resolved);
       if (prev == t * (unsigned long long)ndata - 1) {
+        SPROF(const unsigned long long te = globaltimer_ns(); g_prof[2] += te - g_t_resolved);
         // last data CTA of the step: V(t) to every rank
         const unsigned b = atomicExch(&ctl->bad, 0u);
         unsigned long long v = (t << 32) | ((unsigned long long)(b >> 31) << 31);
         for (int i = 0; i < G; ++i)
           if ((b >> i) & 1u) v |= 1ull << s_order[co][i];
         __threadfence_system();
-        for (int s = 0; s < G; ++s) st_release_sys_u64(P.flags[s] + G + me, v);
+        for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + G + me, v);
+        SPROF(g_prof[3] += globaltimer_ns() - te; g_prof[6] += 1);
       }
     }
   }
   // the last step's verdict: this rank's replica is complete and committed
   // when the kernel exits
   resolve(t0 + steps_total - 1);
+#ifdef PS_SHARD_PROFILE
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double n = g_prof[6] ? (double)g_prof[6] : 1.0;
+    printf("[shard-prof rank %d] per step us: resolve_wait %.2f cta0_stream %.2f last_arrival %.2f "
+           "publish_V %.2f gate %.2f gate_wait %.2f (steps %llu, data CTAs %d)\n", me,
+           g_prof[0] * 1e-3 / n, g_prof[1] * 1e-3 / n, g_prof[2] * 1e-3 / n, g_prof[3] * 1e-3 / n,
+           g_prof[4] * 1e-3 / n, g_prof[5] * 1e-3 / n, g_prof[6], ndata);
+    for (int i = 0; i < 8; ++i) g_prof[i] = 0;
+  }
+#endif
 }
 
 template <typename T>
