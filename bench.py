@@ -170,10 +170,63 @@ def reference_sample(calls, synth, d, paradigm, s_lower, r_max, lr, max_updates)
     return updates, time.perf_counter() - t0
 
 
+def reference_c3_step(srv, grads, times_i, world):
+    """One C3 push group through the reference algorithm (simnet.py:167-201):
+    every worker's apply in seq order, then each decision, then every pull."""
+    for p in range(world):
+        srv.apply_gradient(grads[p % len(grads)])
+    for p in range(world):
+        srv.decide_push(p, times_i)
+    for p in range(world):
+        srv.handle_pull(p)
+
+
+def run_reference_arm_sharded(args, world):
+    """N > 1: the reference CPU server on OUR arm's N>1 workload (C3: d =
+    23,528,522, `world` homogeneous workers, DSSP(3,12)); one step = one push
+    group, exactly what one step of the sharded engine does."""
+    import oracle
+    from paper_1908_11848_b200.sharded import C3_DIM, homogeneous_push_times
+    d = C3_DIM
+    rng = np.random.default_rng(1000)
+    grads = []
+    for _ in range(2):  # two distinct N(0,1) updates, alternated by worker (memory bound on the host)
+        g = rng.standard_normal(d)
+        g.flags.writeable = False
+        grads.append(g)
+    srv = oracle.RefPortServer("dssp", world, 3, 12, 0.05, oracle.initial_weights_f64(0, d))
+    times = homogeneous_push_times(1.0, 0.05, args.warmup + args.steps)
+    for i in range(args.warmup):
+        reference_c3_step(srv, grads, times[i], world)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        reference_c3_step(srv, grads, times[args.warmup + i], world)
+    total = time.perf_counter() - t0
+    value = args.steps * world / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C3 (BASELINE configs[2]): d={d}, {world} homogeneous workers, "
+                               "DSSP(3,12); step = one push group (every worker's apply, decide, pull)",
+                   "d": d, "workers": world},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} push groups of {world} updates (oracle.RefPortServer, "
+                                   "fp64 numpy, single-threaded like the reference)"},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if world > 1:
+        return run_reference_arm_sharded(args, world)
     import paper_1908_11848_b200 as ps
     # the call sequence of the C2 schedule is fixed by the reference
     # simulator semantics; replay it with the same synthetic updates

@@ -4,8 +4,9 @@ shards, push/pull over NVLink P2P, replicated device gate.
 torch.distributed is plumbing only: it exchanges the CUDA-IPC blobs once at
 start-up (all_gather_object), broadcasts the initial weights once over NCCL
 (the north star's only collective) and takes the max of the per-rank device
-times for the benchmark. Every step after that is three kernels per rank
-that talk to their peers through mapped device memory (csrc/ps_shard.cu).
+times for the benchmark. A run of steps after that is ONE persistent kernel
+per rank that talks to its peers through mapped device memory
+(csrc/ps_shard.cu).
 """
 
 from __future__ import annotations
@@ -180,6 +181,48 @@ def c3_config(paradigm, s_lower, r_max, world):
         learning_rate=0.05, seed=0, dimension=C3_DIM, batch_size=1, dataset_size=world))
 
 
+SWEEP_MB = (1, 4, 16, 64, 256, 1024)
+
+
+def bandwidth_sweep(world, rank, local, warm, steps):
+    """BASELINE configs[4] at N GPUs: the sharded push+pull step on 1 MB - 1 GB
+    parameter vectors (ASP, every worker pushes every step), NVLink GB/s
+    received per GPU against the 770 GB/s peer-copy peak. Returns rank 0's
+    rows (max-over-ranks device times)."""
+    import torch
+    import torch.distributed as dist
+
+    rows = []
+    for mb in SWEEP_MB:
+        d = mb * (1 << 18)
+        cfg = validate_config(make_config(
+            paradigm="asp", worker_count=world, timing_preset="homogeneous", compute_base=1.0,
+            comm_delay=0.05, learning_rate=0.05, seed=0, dimension=d, batch_size=1,
+            dataset_size=world))
+        w0 = torch.zeros(d, dtype=torch.float32, device=f"cuda:{local}")
+        srv = ShardedServer(cfg, d, rank, world, local, w0_device=w0)
+        gen = torch.Generator(device=f"cuda:{local}")
+        gen.manual_seed(7 + rank)
+        srv.update[:d].normal_(generator=gen)
+        times = homogeneous_push_times(1.0, 0.05, warm + steps)
+        srv.run(times[:warm])
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(srv.run(times[warm:warm + steps])) / steps
+        lo, hi = shard_range(d, world, rank)
+        nv_bytes = 2 * (world - 1) * (hi - lo) * 4
+        gbs = nv_bytes / (ms * 1e-3) / 1e9
+        rows.append({"mbytes": mb, "d": d, "step_ms": round(ms, 4),
+                     "updates_per_s": round(world / (ms * 1e-3), 1),
+                     "nvlink_gbs": round(gbs, 1), "nvlink_frac": round(gbs / 770.0, 3)})
+        torch.cuda.synchronize()
+        dist.barrier()
+        srv.close()
+        del w0
+        torch.cuda.empty_cache()
+    return rows
+
+
 def bench_main(args, metric):
     import torch
     import torch.distributed as dist
@@ -249,6 +292,7 @@ def bench_main(args, metric):
         torch.cuda.synchronize()
         dist.barrier()  # no peer may still be reading this rank's memory
         srv.close()
+    sweep = bandwidth_sweep(world, rank, local, warm, steps) if not getattr(args, "no_sweep", False) else []
     if sampler is not None:
         sampler.__exit__(None, None, None)
     if rank == 0:
@@ -276,6 +320,7 @@ def bench_main(args, metric):
                          "kernel": "k_shard_run (persistent; whole step: push, apply, pull, verdict, gate)",
                          "bytes_model": "2*(G-1)*S*4 B received over NVLink per GPU per step"},
             "cpu_baseline": None,
+            "sweep": sweep,
             "clocks": sampler.summary() if sampler else None,
         }
         print(json.dumps(line))
