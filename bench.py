@@ -355,6 +355,33 @@ def c4_throttled(torch, ps, reps=3):
     return out
 
 
+def c4_realtime(torch, ps, scale=1e-3):
+    """configs[3] free-running: the same 1x/2x/4x cluster on the wall clock
+    (1 virtual second = `scale` s of GPU global time), every push decided at
+    the instant it reaches the device gate. Reports the wall-clock makespan,
+    the fast worker's wait and the staleness the gate allowed."""
+    from paper_1908_11848_b200.metrics import per_worker, staleness_histogram
+    d = C4_DIM
+    synth = torch.from_numpy(synthetic_host(3, 2, d)).cuda()
+    out = {}
+    for name, s, r in PARADIGMS:
+        cfg = c4_config(name, s, r)
+        sim = ps.DeviceSimulation(cfg, dimension=d, grad="synthetic")
+        sim.set_synthetic(synth, 2)
+        rep = sim.run(read_weights=False, reset_gate=True, realtime_scale=scale, deadline_s=30.0)
+        pw = per_worker(rep.entries)
+        hist = staleness_histogram(rep.entries)
+        out[name] = {"completed": rep.completed, "updates": rep.applied,
+                     "wall_ms": rep.device_ms,
+                     "virtual_duration_s": max(e.time for e in rep.entries),
+                     "fast_worker_wait_s": pw[0].wait_s,
+                     "max_staleness": max(hist) if hist else 0,
+                     "time_scale": scale}
+        sim.engine.close()
+    del synth
+    return out
+
+
 def torch_workers(torch, ps, iters=48, batch=128):
     """Real ResNet-20 workers (PyTorch fwd/bwd) on one GPU,
     round-robin, pushing .grad views and pulling into parameter views through
@@ -532,6 +559,7 @@ def bench_single(args):
                                           max_updates=args.cpu_updates)
     sweep = apply_sweep(torch, ps, hbm_peak) if not args.no_sweep else None
     c4 = c4_throttled(torch, ps) if not args.no_sweep else None
+    c4_rt = c4_realtime(torch, ps) if not args.no_sweep else None
     tw = torch_workers(torch, ps) if not args.no_sweep else None
     clocks = sampler.summary()
     line = {
@@ -573,6 +601,7 @@ def bench_single(args):
                          "host_cpus": os.cpu_count()},
         "sweep": sweep,
         "c4_throttled": c4,
+        "c4_free_running": c4_rt,
         "torch_workers": tw,
         "clocks": clocks,
     }

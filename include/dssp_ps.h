@@ -209,8 +209,10 @@ int ps_set_profiling(ps_server* h, int32_t on);
 
 /* Device-pointer updates and pull destinations are usually produced/consumed
  * on the caller's own CUDA stream (a cudaStream_t passed as an opaque
- * pointer; NULL = none). Every later push/pull is stream-ordered after the
- * work already enqueued there (an event edge, no host synchronization). */
+ * pointer; NULL = none; the legacy default stream is cudaStreamLegacy,
+ * (void*)1, since its handle 0 would read as "none"). Every later push/pull
+ * is stream-ordered after the work already enqueued there (an event edge, no
+ * host synchronization). */
 int ps_set_producer_stream(ps_server* h, void* cuda_stream);
 
 /* ------------------------------------------------------------------------

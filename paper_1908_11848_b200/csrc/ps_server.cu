@@ -348,6 +348,8 @@ int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_
 
 }  // namespace
 
+int ps_order_after_producer(ps_server* h) { return after_producer(h); }
+
 extern "C" {
 
 int ps_device_count(int32_t* n) {

@@ -1257,6 +1257,7 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   if (sc->mode == 2) a.timeout_ns = a.deadline_ns + 20ull * 1000 * 1000 * 1000;
   void* args[] = {&a};
   PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  if ((rc = ps_order_after_producer(h))) return rc;  // resident updates may come from the caller's stream
   PS_CK(h, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSimThreads), args, 0, h->stream));
   PS_CK(h, cudaEventRecord(h->ev1, h->stream));
   k_sim_finish<<<1, 1, 0, h->stream>>>(h->ctrl, (SimOut*)b.out);
@@ -1382,6 +1383,7 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   a.base_version = h->hctrl->gate.version;
   void* args[] = {&a};
   PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  if ((rc = ps_order_after_producer(h))) return rc;  // resident updates may come from the caller's stream
   PS_CK(h, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSimThreads), args, 0, h->stream));
   PS_CK(h, cudaEventRecord(h->ev1, h->stream));
   k_sim_finish<<<1, 1, 0, h->stream>>>(h->ctrl, (SimOut*)b.out);

@@ -51,6 +51,8 @@ struct ps_server {
 };
 
 int ps_fail(ps_server* h, int code, const std::string& msg);
+// Order h->stream after the caller's producer stream (ps_set_producer_stream).
+int ps_order_after_producer(ps_server* h);
 int ps_cuda_fail(ps_server* h, cudaError_t e, const char* what);
 
 #define PS_CK(h, call)                                          \

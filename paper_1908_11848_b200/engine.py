@@ -126,7 +126,9 @@ class Engine:
             ptr = None
         else:
             import torch
-            ptr = torch.cuda.current_stream(tensor.device).cuda_stream
+            # handle 0 is the legacy default stream: name it cudaStreamLegacy
+            # (0x1), because NULL means "no producer" at the C-ABI
+            ptr = torch.cuda.current_stream(tensor.device).cuda_stream or 1
         if ptr != getattr(self, "_producer", None):
             self.lib.ps_set_producer_stream(self._h, ptr)
             self._producer = ptr

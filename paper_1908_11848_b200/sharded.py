@@ -133,6 +133,10 @@ class ShardedServer:
         """Enqueue len(now_times) push groups (+ this rank's pulls); returns
         the device time in ms. dst: CUDA fp32 tensor with >= round_up(d,4)
         elements, or None for the internal replica."""
+        import torch
+        # the update buffer is written on the caller's stream (copy_, normal_,
+        # a backward); the run's own stream must not start before that work
+        torch.cuda.current_stream(self.device).synchronize()
         now = np.ascontiguousarray(now_times, dtype=np.float64)
         ms = ctypes.c_double(0)
         rc = self.lib.ps_shard_run(self._h, self.ticket, len(now), now.ctypes.data,

@@ -109,6 +109,7 @@ class DeviceSimulation:
             sc.deadline_s = float(deadline_s or 0.0)
         res = _lib.PSSimResult()
         lib = self.engine.lib
+        self.engine._order_after(self._synthetic)
         rc = lib.ps_sim_run(self.engine.handle, ctypes.byref(sc), ctypes.byref(res))
         stuck = [q for q in range(self.config.worker_count) if (res.unfinished >> q) & 1]
         if rc == _lib.E_DEADLOCK:
@@ -190,6 +191,7 @@ class DeviceReplay:
     def run(self, reset_gate=True, data_ctas=0, decisions=True):
         res = _lib.PSSimResult()
         lib = self.engine.lib
+        self.engine._order_after(self.synthetic)
         rc = lib.ps_replay_run(self.engine.handle, self.calls.ctypes.data, len(self.calls),
                                self.synthetic.data_ptr(), self.count, 1 if reset_gate else 0,
                                int(data_ctas), ctypes.byref(res))
