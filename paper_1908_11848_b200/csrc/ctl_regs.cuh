@@ -19,6 +19,10 @@
 
 namespace dssp {
 
+#ifdef PS_SIM_PROFILE
+__device__ long long g_ctl_calls, g_ctl_cycles;
+#endif
+
 template <int PM, typename T>
 __device__ __forceinline__ T rget(const T (&a)[PM], int i) {
   T r = a[0];
@@ -142,9 +146,16 @@ struct RegGate {
           int pred = 0;
           if (r_max > 0) {
             const int sl = slowest();
-            if (rget<PM>(populated, p) >= 2 && rget<PM>(populated, sl) >= 2)
+            if (rget<PM>(populated, p) >= 2 && rget<PM>(populated, sl) >= 2) {
+#ifdef PS_SIM_PROFILE
+              const long long tc = clock64();
+#endif
               pred = controller_grid(rget<PM>(latest, p), rget<PM>(previous, p), rget<PM>(latest, sl),
                                      rget<PM>(previous, sl), r_max);
+#ifdef PS_SIM_PROFILE
+              if ((threadIdx.x & 31) == 0) { g_ctl_calls += 1; g_ctl_cycles += clock64() - tc; }
+#endif
+            }
           }
           int headroom = s_lower + r_max - gap;
           if (headroom < 0) headroom = 0;

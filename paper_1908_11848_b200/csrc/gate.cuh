@@ -63,13 +63,14 @@ __device__ __forceinline__ int controller_grid(double lp, double pp, double ls, 
     }
     if (m < best) { best = m; best_r = r; }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const double ob = __shfl_xor_sync(kFull, best, off);
-    const int orr = __shfl_xor_sync(kFull, best_r, off);
-    if (ob < best || (ob == best && orr < best_r)) { best = ob; best_r = orr; }
-  }
-  return best_r;
+  // argmin over the lanes, first index wins on ties: the bit pattern of a
+  // non-negative double orders like its value, so three integer redux
+  // steps (high word, low word, r) replace a 5-round shuffle tree
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(best);
+  const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+  const unsigned mhi = __reduce_min_sync(kFull, hi);
+  const unsigned mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xffffffffu);
+  return (int)__reduce_min_sync(kFull, (hi == mhi && lo == mlo) ? (unsigned)best_r : 0x7fffffffu);
 }
 
 __device__ __forceinline__ void record(ps_gate_state* s, int q, double t) {

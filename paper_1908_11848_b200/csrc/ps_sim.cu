@@ -87,6 +87,7 @@ struct SimOut {
   unsigned long long unfinished;
   int status, diverged_worker;
   unsigned long long t_start, t_control_done, t_data_done;  // %globaltimer ns
+  unsigned long long validated;  // replay: (calls validated by the gate << 1) | done
 };
 
 struct SimArgs {
@@ -698,15 +699,15 @@ __device__ void control_warp_lanes(const SimArgs& a) {
 // ---------------------------------------------------------------------------
 // Replay mode: the server serving a recorded request stream.
 //
-// The control warp reads the reference's boundary call sequence (pull /
-// apply / decide, in the order simnet.py:127-201 issues them) from HBM and
-// executes it: pulls and applies become data ops exactly as in the simulated
-// run, every decide runs the gate on the device. It is what a parameter
-// server does with the requests its workers send, without simulating the
-// workers -- the same work the reference arm times on the CPU
-// (ParameterServer.apply_gradient / decide_push / handle_pull).
-// Each update's finiteness scan (GRAD op) is emitted one 32-call chunk
-// ahead of its apply, so the apply rarely waits for it.
+// The kernel reads the reference's boundary call sequence (pull / apply /
+// decide, in the order simnet.py:127-201 issues them) from HBM and executes
+// it: every decide runs the gate on the device (gate warp), every pull and
+// apply runs on the data warps' parameter slices in call order. It is what a
+// parameter server does with the requests its workers send, without
+// simulating the workers -- the same work the reference arm times on the CPU
+// (ParameterServer.apply_gradient / decide_push / handle_pull). Decisions
+// never feed the data (they only validate the protocol), so the two sides
+// run concurrently, coupled by the gate's validated-calls watermark.
 // ---------------------------------------------------------------------------
 
 template <int PM>
@@ -714,7 +715,7 @@ struct ReplayGate {  // scalar register tables (ctl_regs.cuh), P <= PM
   RegGate<PM> g;
   __device__ __forceinline__ void load(const ps_gate_state& s, bool reset, ps_gate_state*) { g.load(s, reset); }
   __device__ __forceinline__ void store(ps_gate_state& d) { g.store(d); }
-  __device__ __forceinline__ bool deferred(int q) const { return (g.deferred >> q) & 1ull; }
+  __device__ __forceinline__ unsigned long long deferred_mask() const { return g.deferred; }
   __device__ __forceinline__ GateResult on_push(int p, double now) { return g.on_push(p, now); }
 };
 
@@ -743,7 +744,9 @@ struct ReplayGate<0> {  // shared-memory tables (gate.cuh), any P <= 64
       d.rejected = r;
     }
   }
-  __device__ __forceinline__ bool deferred(int q) const { return (s->deferred >> q) & 1ull; }
+  __device__ __forceinline__ unsigned long long deferred_mask() const {
+    return *reinterpret_cast<const volatile unsigned long long*>(&s->deferred);
+  }
   __device__ __forceinline__ GateResult on_push(int p, double now) {
     const GateResult r = gate_on_push(s, p, now);
     __syncwarp();
@@ -751,86 +754,98 @@ struct ReplayGate<0> {  // shared-memory tables (gate.cuh), any P <= 64
   }
 };
 
+// The gate warp of a replay: decides every DECIDE in order and validates the
+// protocol (unknown worker, pull or push while deferred). It publishes a
+// watermark -- (calls validated << 1) | done -- once per 32 calls; the data
+// warps number and execute the pulls / applies themselves (data_warp_replay)
+// and never run past it, so a protocol error stops the data exactly where
+// the reference would have raised.
 template <int PM>
-__device__ void control_warp_replay(const SimArgs& a, ps_gate_state* sgate, int* s_staged, int* s_sidx) {
+__device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
   const int lane = threadIdx.x & 31;
-  const int P = a.P, nsyn = a.n_synth;
-  const unsigned tag = a.tag;
-  Op* const ops = a.ops;
+  const int P = a.P;
   ReplayGate<PM> g;
   g.load(a.ctrl->gate, a.reset_gate != 0, sgate);
-  for (int q = lane; q < P; q += 32) { s_staged[q] = 0; s_sidx[q] = 0; }
-  __syncwarp();
-  long long n_ops = 0, next_slot = 0, n_dec = 0, pushes = 0;
+  long long n_dec = 0, pushes = 0, valid = 0;
   int status = PS_OK;
-  auto emit = [&](int type, int w, int buf, long long slot) {
-    if (lane == 0) st_relaxed_u64(ops + n_ops, op_pack(tag, type, w, buf, slot));
-    n_ops += 1;
-  };
   const long long n = a.n_calls;
-  // lane l holds call (base + l) of the current chunk and its (slot, buf)
-  auto load_chunk = [&](long long base, ReplayCall& c) {
+  if (lane == 0) a.out->t_start = globaltimer_ns();
+#ifdef PS_SIM_PROFILE
+  long long c_gate = 0;
+  const long long c_start = clock64();
+#endif
+  auto load = [&](long long base, ReplayCall& c) {
     const long long i = base + lane;
     if (i < n) c = a.calls[i];
     else { c.now = 0.0; c.kind = -1; c.worker = 0; }
   };
-  auto emit_grads = [&](const ReplayCall& c, long long& slot_l, int& buf_l) {
-    for (int l = 0; l < 32; ++l) {
-      const int kind = __shfl_sync(kFull, c.kind, l);
-      if (kind != kCallApply) continue;
-      const int p = __shfl_sync(kFull, c.worker, l);
-      const int si = s_sidx[p];
-      const int buf = si % nsyn;
-      const long long slot = next_slot++;
-      __syncwarp();
-      if (lane == 0) s_sidx[p] = si + 1;
-      __syncwarp();
-      if (lane == l) { slot_l = slot; buf_l = buf; }
-      emit(OP_GRAD, p, buf, slot);
-    }
-  };
-  ReplayCall cur, nxt;
-  long long cur_slot = 0, nxt_slot = 0;
-  int cur_buf = 0, nxt_buf = 0;
-  if (lane == 0) a.out->t_start = globaltimer_ns();
-  load_chunk(0, cur);
-  emit_grads(cur, cur_slot, cur_buf);
+  ReplayCall c, nx;
+  load(0, c);
   for (long long base = 0; base < n && status == PS_OK; base += 32) {
-    load_chunk(base + 32, nxt);
-    emit_grads(nxt, nxt_slot, nxt_buf);  // one chunk of lookahead for the scans
+    load(base + 32, nx);  // in flight while this chunk is decided
     const int m = n - base < 32 ? (int)(n - base) : 32;
-    for (int i = 0; i < m; ++i) {
-      const int kind = __shfl_sync(kFull, cur.kind, i);
-      const int w = __shfl_sync(kFull, cur.worker, i);
-      if (w < 0 || w >= P) { status = PS_E_PROTOCOL; break; }
-      if (kind == kCallPull) {
-        if (g.deferred(w)) { status = PS_E_PROTOCOL; break; }  // pulled while deferred
-        const int st = s_staged[w] ^ 1;
-        __syncwarp();
-        if (lane == 0) s_staged[w] = st;
-        __syncwarp();
-        emit(OP_PULL, w, st, 0);
-      } else if (kind == kCallApply) {
-        emit(OP_APPLY, w, __shfl_sync(kFull, cur_buf, i), __shfl_sync(kFull, cur_slot, i));
-      } else {
-        const double now = __shfl_sync(kFull, cur.now, i);
-        const GateResult r = g.on_push(w, now);
-        pushes += 1;
-        if (r.status != PS_OK) { status = r.status; break; }
-        if (lane == 0 && n_dec < a.trace_cap)
-          a.decisions[n_dec] = (long long)((r.released << 8) | (unsigned)r.outcome);
-        n_dec += 1;
-      }
+    const unsigned live = m >= 32 ? kFull : ((1u << m) - 1u);
+    const bool inr = lane < m;
+    // an unknown worker ends the valid prefix of the chunk
+    const unsigned badw = __ballot_sync(kFull, inr && (c.worker < 0 || c.worker >= P));
+    const int limit = badw ? __ffs(badw) - 1 : m;
+    const unsigned below_limit = limit >= 32 ? kFull : ((1u << limit) - 1u);
+    unsigned md = __ballot_sync(kFull, c.kind == kCallDecide) & live & below_limit;
+    const unsigned mp = __ballot_sync(kFull, c.kind == kCallPull) & live & below_limit;
+    int prev = 0;
+    int fail = -1;
+    // pulls in [from, to) must not come from a deferred worker (one vote per
+    // run of pulls: the deferred set only changes at decides)
+    auto check_pulls = [&](int from, int to) {
+      const unsigned rng = mp & (to >= 32 ? kFull : ((1u << to) - 1u)) & ~((1u << from) - 1u);
+      if (!rng) return;
+      const unsigned long long dm = g.deferred_mask();
+      const unsigned hit = __ballot_sync(kFull, ((rng >> lane) & 1u) && ((dm >> (c.worker & 63)) & 1ull));
+      if (hit) fail = __ffs(hit) - 1;
+    };
+    while (md && fail < 0) {
+      const int i = __ffs(md) - 1;
+      md &= md - 1;
+      check_pulls(prev, i);
+      if (fail >= 0) break;
+      const int w = __shfl_sync(kFull, c.worker, i);
+      const double now = __shfl_sync(kFull, c.now, i);
+#ifdef PS_SIM_PROFILE
+      const long long tg = clock64();
+#endif
+      const GateResult r = g.on_push(w, now);
+#ifdef PS_SIM_PROFILE
+      c_gate += clock64() - tg;
+#endif
+      pushes += 1;
+      if (r.status != PS_OK) { status = r.status; fail = i; break; }
+      if (lane == 0 && n_dec < a.trace_cap)
+        a.decisions[n_dec] = (long long)((r.released << 8) | (unsigned)r.outcome);
+      n_dec += 1;
+      prev = i + 1;
     }
-    cur = nxt;
-    cur_slot = nxt_slot;
-    cur_buf = nxt_buf;
+    if (fail < 0) check_pulls(prev, limit);
+    if (fail < 0 && limit < m) fail = limit;
+    if (fail >= 0) {
+      if (status == PS_OK) status = PS_E_PROTOCOL;
+      valid = base + fail;
+      break;
+    }
+    valid = base + m;
+    // relaxed: the watermark publishes no data, only how far the data may go
+    if (lane == 0 && valid < n) st_relaxed_u64(&a.out->validated, (unsigned long long)valid << 1);
+    c = nx;
   }
-  emit(OP_END, 0, 0, 0);
+  if (lane == 0) st_relaxed_u64(&a.out->validated, ((unsigned long long)valid << 1) | 1ull);
+#ifdef PS_SIM_PROFILE
+  if (lane == 0)
+    printf("[replay-gate] calls %lld decides %lld: total %lld cycles, on_push %lld, controller %lld calls %lld cycles\n",
+           n, pushes, clock64() - c_start, c_gate, g_ctl_calls, g_ctl_cycles);
+#endif
   g.store(a.ctrl->gate);
   if (lane == 0) {
     a.out->t_control_done = globaltimer_ns();
-    a.out->events = n;
+    a.out->events = valid;
     a.out->pushes = pushes;
     a.out->trace_rows = n_dec;
     a.out->unfinished = 0ull;
@@ -1039,6 +1054,255 @@ __device__ void data_warp(const SimArgs& a, unsigned dw, unsigned* s_ring, int w
   }
 }
 
+// Replay data warp. The op stream of a replay is a function of the call list
+// alone: an apply's update index is the number of earlier applies by the
+// same worker, a pull's replica buffer the parity of that worker's earlier
+// pulls. Every data warp derives these per 32-call chunk with ballots /
+// match_any (prefix counts, no serial producer) and keeps two chunks of
+// lookahead: while it executes chunk c it numbers and scans chunk c+2.
+//
+// Finiteness verdicts are per chunk (server.py:65-67 rejects an update if ANY
+// element is non-finite, and every warp sees only its slice): each warp ORs
+// the calls whose slice holds a non-finite value into a 32-bit mask, the CTA
+// aggregates its warps in a shared 64-bit word {warps done << 32 | bits},
+// and the last warp adds the CTA to the chunk's global word {CTAs done << 32
+// | bits} -- an OR then an ADD on the same address, so a reader that sees the
+// full count sees every CTA's bits without a fence. Executing a chunk takes
+// ONE poll of that word.
+template <int V>
+__device__ void data_warp_replay(const SimArgs& a, unsigned dw, unsigned* s_ring32, int warps_here) {
+  constexpr int K = V == 1 ? 8 : V == 2 ? 4 : V == 4 ? 2 : 1;     // scan: update slices in flight
+  constexpr int KG = V == 1 ? 16 : V == 2 ? 8 : V == 4 ? 4 : V == 8 ? 2 : 1;  // execute: calls per group
+  constexpr int VV = V > 0 ? V : 1;
+  constexpr int kRingChunks = kRing / 2;
+  unsigned long long* s_ring = reinterpret_cast<unsigned long long*>(s_ring32);
+  unsigned long long* gchunk = reinterpret_cast<unsigned long long*>(a.gword);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int P = a.P, nsyn = a.n_synth;
+  const long long n = a.n_calls;
+  const long long per = (a.nv + a.n_data_warps - 1) / a.n_data_warps;
+  const long long lo = (long long)dw * per < a.nv ? (long long)dw * per : a.nv;
+  const long long hi = lo + per < a.nv ? lo + per : a.nv;
+  float4* W = reinterpret_cast<float4*>(a.W);
+  float4 wr[VV];
+  if constexpr (V > 0) {
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const long long j = lo + lane + 32ll * u;
+      wr[u] = j < hi ? W[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  const unsigned long long t0 = globaltimer_ns();
+  // per-worker counters, lane q holds workers q and q + 32
+  int sidx_lo = 0, sidx_hi = 0, stg_lo = 0, stg_hi = 0;
+  long long applied = 0, rejected = 0;
+  int diverged = -1;
+  // per chunk: lane l's call as (worker << 8 | buffer), and the warp-uniform
+  // masks of its applies and pulls
+  struct Chunk { int wb; unsigned ma, mp; };
+  auto number = [&](long long base, Chunk& c) {
+    const long long i = base + lane;
+    int kind = -1, worker = 0, buf = 0;
+    if (i < n) {
+      const int2 kw = *reinterpret_cast<const int2*>(&a.calls[i].kind);
+      kind = kw.x;
+      worker = kw.y;
+    }
+    const bool okw = worker >= 0 && worker < P;
+    const bool isa = okw && kind == kCallApply, isp = okw && kind == kCallPull;
+    c.ma = __ballot_sync(kFull, isa);
+    c.mp = __ballot_sync(kFull, isp);
+    const unsigned peers = __match_any_sync(kFull, isa ? worker : isp ? 64 + worker : 128 + lane);
+    const int rank = __popc(peers & lt);
+    const int wq = worker & 31;
+    const int s_lo = __shfl_sync(kFull, sidx_lo, wq), s_hi = __shfl_sync(kFull, sidx_hi, wq);
+    const int g_lo = __shfl_sync(kFull, stg_lo, wq), g_hi = __shfl_sync(kFull, stg_hi, wq);
+    if (isa) buf = ((worker < 32 ? s_lo : s_hi) + rank) % nsyn;
+    if (isp) buf = (worker < 32 ? g_lo : g_hi) ^ ((rank + 1) & 1);
+    c.wb = (okw ? worker : 0) << 8 | buf;
+    for (int q = 0; q < P; ++q) {
+      const int na = __popc(__ballot_sync(kFull, isa && worker == q));
+      const int np = __popc(__ballot_sync(kFull, isp && worker == q));
+      if (lane == (q & 31)) {
+        if (q < 32) { sidx_lo += na; stg_lo ^= np & 1; }
+        else { sidx_hi += na; stg_hi ^= np & 1; }
+      }
+    }
+  };
+  auto slice_of = [&](const Chunk& c, int l) {
+    const int wb = __shfl_sync(kFull, c.wb, l);
+    return reinterpret_cast<const float4*>(a.synth + ((long long)(wb >> 8) * nsyn + (wb & 255)) * a.dpad);
+  };
+  // x * 0 is 0 for finite x and NaN otherwise: one FFMA per component
+  auto acc_nonfinite = [](float acc, const float4& v) {
+    return __fmaf_rn(v.w, 0.f, __fmaf_rn(v.z, 0.f, __fmaf_rn(v.y, 0.f, __fmaf_rn(v.x, 0.f, acc))));
+  };
+  auto scan = [&](const Chunk& c, long long chunk) {
+    unsigned m = c.ma;
+    unsigned badbits = 0;
+    while (m) {
+      int ls[K];
+      float4 r[K][VV];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ls[k] = -1;
+        if (m) {
+          ls[k] = __ffs(m) - 1;
+          m &= m - 1;
+          if constexpr (V > 0) load_slice<V>(r[k], slice_of(c, ls[k]), lo, hi, lane);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (ls[k] < 0) break;
+        float acc = 0.f;
+        if constexpr (V > 0) {
+#pragma unroll
+          for (int u = 0; u < V; ++u) acc = acc_nonfinite(acc, r[k][u]);
+        } else {
+          const float4* src = slice_of(c, ls[k]);
+          for (long long j = lo + lane; j < hi; j += 32) acc = acc_nonfinite(acc, ld_stream(src + j));
+        }
+        if (__any_sync(kFull, acc != acc)) badbits |= 1u << ls[k];
+      }
+    }
+    if (lane == 0 && chunk * 32 < n) {
+      unsigned long long* w = &s_ring[chunk & (kRingChunks - 1)];
+      if (badbits) atomicOr(w, (unsigned long long)badbits);
+      const unsigned long long old = atomicAdd(w, 1ull << 32);
+      if ((unsigned)(old >> 32) == (unsigned)warps_here - 1) {  // last warp of this CTA
+        const unsigned long long bits = atomicExch(w, 0ull) & 0xffffffffull;
+        if (bits) atomicOr(&gchunk[chunk], bits);
+        atomicAdd(&gchunk[chunk], 1ull << 32);
+      }
+    }
+  };
+  Chunk c0, c1, c2;
+  number(0, c0);
+  scan(c0, 0);
+  number(32, c1);
+  scan(c1, 1);
+  bool stop = false;
+  for (long long base = 0, chunk = 0; base < n && !stop; base += 32, ++chunk) {
+    // polls for this chunk, issued before the lookahead work hides them
+    unsigned long long wm = 0, cv = 0;
+    if (lane == 0) {
+      wm = ld_relaxed_u64(&a.out->validated);
+      cv = ld_relaxed_u64(&gchunk[chunk]);
+    }
+    number(base + 64, c2);
+    scan(c2, chunk + 2);
+    const long long need = n - base < 32 ? n : base + 32;
+    if (lane == 0) {
+      // the gate warp's watermark: calls validated so far (| 1 once done).
+      // Relaxed is enough: no data is published under it.
+      unsigned backoff = 32;
+      while ((wm >> 1) < (unsigned long long)need && !(wm & 1ull)) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) { wm = ~0ull; break; }
+        __nanosleep(backoff);
+        backoff = backoff < 256 ? backoff * 2 : 256;
+        wm = ld_relaxed_u64(&a.out->validated);
+      }
+      // every data CTA has scanned this chunk
+      while (wm != ~0ull && (unsigned)(cv >> 32) < a.n_ctas) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) { wm = ~0ull; break; }
+        __nanosleep(20);
+        cv = ld_relaxed_u64(&gchunk[chunk]);
+      }
+    }
+    wm = __shfl_sync(kFull, wm, 0);
+    const unsigned bits = (unsigned)__shfl_sync(kFull, cv, 0);
+    if (wm == ~0ull) {
+      if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
+      return;
+    }
+    long long upto = (long long)(wm >> 1);
+    if (upto < need) stop = true;  // the gate stopped inside this chunk
+    else upto = need;
+    const int m = upto > base ? (int)(upto - base) : 0;
+    const unsigned live = m >= 32 ? kFull : ((1u << m) - 1u);
+    // pulls and applies in call order (decides are the gate warp's), KG calls
+    // at a time with every update slice of the group loaded up front
+    bool dbad = false;
+    unsigned calls = (c0.ma | c0.mp) & live;
+    while (calls) {
+      int idx[KG];
+      float4 g[KG][VV];
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        idx[k] = -1;
+        if (calls) {
+          const int i = __ffs(calls) - 1;
+          calls &= calls - 1;
+          idx[k] = i;
+          if constexpr (V > 0)
+            if (((c0.ma & ~bits) >> i) & 1u) load_slice<V>(g[k], slice_of(c0, i), lo, hi, lane);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const int i = idx[k];
+        if (i < 0) break;
+        const int wb = __shfl_sync(kFull, c0.wb, i);
+        const int w = wb >> 8, buf = wb & 255;
+        if ((c0.mp >> i) & 1u) {
+          float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)w * 2 + buf) * a.dpad);
+          if constexpr (V > 0) {
+#pragma unroll
+            for (int u = 0; u < V; ++u) {
+              const long long j = lo + lane + 32ll * u;
+              if (j < hi) dst[j] = wr[u];
+            }
+          } else {
+            for (long long j = lo + lane; j < hi; j += 32) dst[j] = W[j];
+          }
+        } else if ((bits >> i) & 1u) {
+          rejected += 1;
+        } else {
+          float acc = 0.f;
+          if constexpr (V > 0) {
+#pragma unroll
+            for (int u = 0; u < V; ++u) {
+              wr[u] = apply4(wr[u], a.lr, g[k][u]);
+              acc = acc_nonfinite(acc, wr[u]);
+            }
+          } else {
+            const float4* gp = reinterpret_cast<const float4*>(a.synth + ((long long)w * nsyn + buf) * a.dpad);
+            for (long long j = lo + lane; j < hi; j += 32) {
+              const float4 r = apply4(W[j], a.lr, gp[j]);
+              acc = acc_nonfinite(acc, r);
+              W[j] = r;
+            }
+          }
+          if (acc != acc && !dbad) { dbad = true; diverged = w; }
+          applied += 1;
+        }
+      }
+    }
+    // a non-finite result (server.py:38-41): the run stops with the worker named
+    if (__any_sync(kFull, dbad)) {
+      const int src = __ffs(__ballot_sync(kFull, dbad)) - 1;
+      const int wdiv = __shfl_sync(kFull, diverged, src);
+      if (lane == 0 && atomicCAS(&a.out->status, PS_OK, PS_E_DIVERGED) == PS_OK) a.out->diverged_worker = wdiv;
+    }
+    c0 = c1;
+    c1 = c2;
+  }
+  if constexpr (V > 0) {
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const long long j = lo + lane + 32ll * u;
+      if (j < hi) W[j] = wr[u];
+    }
+  }
+  if (lane == 0) atomicMax(&a.out->t_data_done, globaltimer_ns());
+  if (dw == 0 && lane == 0) {
+    a.out->applied = applied;
+    a.out->rejected = rejected;
+  }
+}
+
 // V: float4 per lane of register-resident weights (0 = in HBM);
 // CTL: control tables in registers -- 2/4/8: scalar, replicated in every lane
 // (fastest for few workers, ctl_regs.cuh); 32: one worker per lane
@@ -1046,7 +1310,7 @@ __device__ void data_warp(const SimArgs& a, unsigned dw, unsigned* s_ring, int w
 template <int V, int CTL>
 __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   __shared__ CtlState s;
-  __shared__ unsigned s_ring[kRing];
+  __shared__ __align__(8) unsigned s_ring[kRing];
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) s_ring[i] = 0;
   __syncthreads();
   // CTA 0 is the control warp alone: no data warp competes with it for its
@@ -1054,9 +1318,8 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   if (blockIdx.x == 0) {
     if (threadIdx.x >= 32) return;
     if (a.mode == 1) {
-      __shared__ int s_staged[kMaxP], s_sidx[kMaxP];
-      if constexpr (CTL == 2 || CTL == 4 || CTL == 8) control_warp_replay<CTL>(a, &s.gate, s_staged, s_sidx);
-      else control_warp_replay<0>(a, &s.gate, s_staged, s_sidx);
+      if constexpr (CTL == 2 || CTL == 4 || CTL == 8) gate_warp_replay<CTL>(a, &s.gate);
+      else gate_warp_replay<0>(a, &s.gate);
       return;
     }
     if constexpr (CTL == 32) control_warp_lanes(a);
@@ -1065,7 +1328,8 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
     return;
   }
   const unsigned dw = ((blockIdx.x - 1) * kSimThreads + threadIdx.x) >> 5;
-  data_warp<V>(a, dw, s_ring, kSimThreads / 32);
+  if (a.mode == 1) data_warp_replay<V>(a, dw, s_ring, kSimThreads / 32);
+  else data_warp<V>(a, dw, s_ring, kSimThreads / 32);
 }
 
 // After the run: fold the data side's counters into the control block.
@@ -1326,7 +1590,8 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
     PS_CK(h, cudaMemsetAsync(b.ops, 0, b.ops_cap * sizeof(Op), h->stream));
     b.tag = 1;
   }
-  const size_t slots = (size_t)n + 1;
+  // replay verdicts: one {CTAs done, non-finite bits} pair per 32-call chunk
+  const size_t slots = 2 * ((size_t)n / 32 + 4);
   if (b.slots_cap < slots || !b.gcount) {
     cudaFree(b.gcount);
     b.gcount = nullptr;

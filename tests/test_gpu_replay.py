@@ -57,3 +57,76 @@ def test_replay_rejects_protocol_violation():
     calls = [("apply", 0), ("decide", 0, 1.0), ("pull", 0)]  # worker 0 is deferred, then pulls
     with pytest.raises(ps.ProtocolError):
         DeviceReplay(eng, calls, synth, 1).run()
+
+
+def _fp32_replay(calls, synth, d, lr, seed=0, reject=lambda p, k: False):
+    w = oracle.initial_weights_f64(seed, d).astype(np.float32)
+    seen = {}
+    applied = rejected = 0
+    K = synth.shape[1]
+    for c in calls:
+        if c[0] == "apply":
+            k = seen.get(c[1], 0)
+            seen[c[1]] = k + 1
+            if reject(c[1], k % K):
+                rejected += 1
+                continue
+            w = oracle.apply_f32(w, synth[c[1], k % K, :d], lr)
+            applied += 1
+    return w, applied, rejected
+
+
+def test_replay_stops_data_exactly_at_a_protocol_error():
+    """The data warps run ahead of the gate warp but never past its validated
+    watermark: a violation deep in the stream (call 70 of 100, applies after
+    it) leaves exactly the applies before it in the weights."""
+    d, K = 4099, 2
+    dpad = (d + 3) // 4 * 4
+    synth = np.zeros((2, K, dpad), dtype=np.float32)
+    for p in range(2):
+        for k in range(K):
+            synth[p, k, :d] = oracle.synthetic_update(5, p, k, d)
+    calls, t = [], 0.0
+    while len(calls) < 69:
+        for p in range(2):
+            t += 1.0
+            calls += [("apply", p), ("decide", p, t), ("pull", p)]
+    calls = calls[:69]
+    # ASP never defers: make the violation an unknown worker, then more applies
+    bad = calls + [("pull", 7)] + [("apply", 0), ("decide", 0, t + 1.0), ("pull", 0)] * 10
+    eng = Engine("asp", 2, 0, 0, 0.05, d, w0=oracle.initial_weights_f64(0, d))
+    with pytest.raises(ps.ProtocolError):
+        DeviceReplay(eng, bad, torch.from_numpy(synth).cuda(), K).run()
+    got, _ = eng.read()
+    want, applied, _ = _fp32_replay(calls, synth, d, 0.05)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    eng.refresh()
+    assert eng.state.version == applied
+    eng.close()
+
+
+def test_replay_rejects_nonfinite_updates_per_call():
+    """One non-finite element in one worker's resident update rejects exactly
+    the applies that use it (server.py:65-67), across chunk boundaries."""
+    run = next(r for r in oracle.load_golden("c2_schedule.json.gz")["runs"] if r["name"] == "c2_dssp")
+    norm = run["normalized"]
+    d, K, P = 4099, 2, norm["worker_count"]
+    dpad = (d + 3) // 4 * 4
+    synth = np.zeros((P, K, dpad), dtype=np.float32)
+    for p in range(P):
+        for k in range(K):
+            synth[p, k, :d] = oracle.synthetic_update(6, p, k, d)
+    synth[1, 0, 4000] = np.inf  # worker 1's even-numbered pushes
+    calls = [tuple(c[:2]) if c[0] != "decide" else ("decide", c[1], c[2])
+             for c in run["calls"] if c[0] in ("pull", "apply", "decide")]
+    eng = Engine(norm["paradigm"], P, norm["s_lower"], norm["r_max"], norm["learning_rate"], d,
+                 w0=oracle.initial_weights_f64(0, d))
+    rep = DeviceReplay(eng, calls, torch.from_numpy(synth).cuda(), K).run()
+    want, applied, rejected = _fp32_replay(calls, synth, d, norm["learning_rate"],
+                                           reject=lambda p, k: p == 1 and k == 0)
+    assert rep.rejected == rejected > 0 and rep.applied == applied
+    got, _ = eng.read()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    # decisions do not depend on the data
+    assert rep.decisions == [(c[3], tuple(c[4])) for c in run["calls"] if c[0] == "decide"]
+    eng.close()
