@@ -593,7 +593,11 @@ def bench_single(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "k_sim (replay mode)",
-                     "bytes_model": "12 B/param per push-apply + 8 B/param per pull"},
+                     "bytes_model": "12 B/param per push-apply + 8 B/param per pull",
+                     "note": "C2's 1 MB of weights stay in registers and its updates in L2 for "
+                             "the whole stream (traffic = DRAM bytes per launch from ncu), so "
+                             "frac can exceed 1: the kernel is bound by the latency of the "
+                             "serial gate and per-call issue, not by HBM"},
         "cpu_baseline": {"value": cpu_updates / cpu_s, "unit": "updates/s", "cores": 1,
                          "kind": "port",
                          "sample": f"first {cpu_updates} updates of the same C2 request stream, "
