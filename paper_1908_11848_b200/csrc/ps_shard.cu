@@ -673,8 +673,15 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
     const int n = v ? atoi(v) : 2;
     return n > 0 && n <= 16 ? n : 2;
   }();
-  const void* kern = G <= 2 ? (const void*)k_shard_run<2> : G <= 4 ? (const void*)k_shard_run<4>
-                   : G <= 8 ? (const void*)k_shard_run<8> : (const void*)k_shard_run<16>;
+  // PS_SHARD_GMAX (test knob): run a wider instantiation than G needs, so the
+  // G <= 8 / 16 code paths are exercised on a box with fewer GPUs
+  static const int gmax_env = [] {
+    const char* v = getenv("PS_SHARD_GMAX");
+    return v ? atoi(v) : 0;
+  }();
+  const int gsel = G > gmax_env ? G : gmax_env;
+  const void* kern = gsel <= 2 ? (const void*)k_shard_run<2> : gsel <= 4 ? (const void*)k_shard_run<4>
+                   : gsel <= 8 ? (const void*)k_shard_run<8> : (const void*)k_shard_run<16>;
   int resident = 0;
   SCK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kThreads, 0));
   const int total = h->sm_count * (per_sm_env < resident ? per_sm_env : resident);

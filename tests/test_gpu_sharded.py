@@ -21,15 +21,18 @@ def _gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_parity(tmp_path, world):
+@pytest.mark.parametrize("world,gmax", [(2, 0), (4, 0), (2, 8), (4, 16)])
+def test_sharded_parity(tmp_path, world, gmax):
+    """gmax > 0 runs the G <= 8 / G <= 16 kernel instantiations on this box's
+    GPUs (PS_SHARD_GMAX), the code the 8-GPU runs execute."""
     if _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
-           "--master-port", str(29400 + world), os.path.join(ROOT, "tests", "_sharded_worker.py"),
+           "--master-port", str(29400 + world + gmax), os.path.join(ROOT, "tests", "_sharded_worker.py"),
            str(tmp_path)]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, PS_SHARD_GMAX=str(gmax))
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     files = sorted(glob.glob(str(tmp_path / "rank*.json")))
     assert len(files) == world
