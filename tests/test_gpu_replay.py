@@ -105,18 +105,21 @@ def test_replay_stops_data_exactly_at_a_protocol_error():
     eng.close()
 
 
-def test_replay_rejects_nonfinite_updates_per_call():
+@pytest.mark.parametrize("d", [4099, 272_474, 500_000, 1_730_714])
+def test_replay_rejects_nonfinite_updates_per_call(d):
     """One non-finite element in one worker's resident update rejects exactly
-    the applies that use it (server.py:65-67), across chunk boundaries."""
+    the applies that use it (server.py:65-67), across chunk boundaries. The
+    sizes cover every data-warp variant: speculative execution with rollback
+    (1, 2 and 4 float4 of weights per lane) and the scan-ahead path (16)."""
     run = next(r for r in oracle.load_golden("c2_schedule.json.gz")["runs"] if r["name"] == "c2_dssp")
     norm = run["normalized"]
-    d, K, P = 4099, 2, norm["worker_count"]
+    K, P = 2, norm["worker_count"]
     dpad = (d + 3) // 4 * 4
     synth = np.zeros((P, K, dpad), dtype=np.float32)
     for p in range(P):
         for k in range(K):
             synth[p, k, :d] = oracle.synthetic_update(6, p, k, d)
-    synth[1, 0, 4000] = np.inf  # worker 1's even-numbered pushes
+    synth[1, 0, d - 99] = np.inf  # worker 1's even-numbered pushes
     calls = [tuple(c[:2]) if c[0] != "decide" else ("decide", c[1], c[2])
              for c in run["calls"] if c[0] in ("pull", "apply", "decide")]
     eng = Engine(norm["paradigm"], P, norm["s_lower"], norm["r_max"], norm["learning_rate"], d,
