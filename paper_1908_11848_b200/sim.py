@@ -156,13 +156,34 @@ CALL_PULL, CALL_APPLY, CALL_DECIDE = 0, 1, 2
 _CALL_DTYPE = np.dtype([("now", np.float64), ("kind", np.int32), ("worker", np.int32)])
 
 
+def decode_decisions(raw):
+    """Decision words ((released << 8) | outcome) -> [(outcome, released ids)]."""
+    out = []
+    for v in np.asarray(raw, dtype=np.int64).tolist():
+        rel = v >> 8
+        ids = []
+        q = 0
+        while rel:
+            if rel & 1:
+                ids.append(q)
+            rel >>= 1
+            q += 1
+        out.append(("grant" if (v & 0xff) == 0 else "defer", tuple(ids)))
+    return out
+
+
 @dataclass
 class ReplayReport:
-    decisions: list      # [(outcome, released tuple)] per decide
+    raw: np.ndarray      # one decision word per decide: (released << 8) | outcome
     applied: int
     rejected: int
     pushes: int
     device_ms: float
+
+    @property
+    def decisions(self) -> list:
+        """[(outcome, released tuple)] per decide (decoded on demand)."""
+        return decode_decisions(self.raw)
 
     @property
     def updates_per_s(self) -> float:
@@ -196,18 +217,17 @@ class DeviceReplay:
                                self.synthetic.data_ptr(), self.count, 1 if reset_gate else 0,
                                int(data_ctas), ctypes.byref(res))
         raise_for(rc, self.engine.error())
-        out = []
+        raw = np.zeros(0, dtype=np.int64)
         if decisions:
             n = res.trace_rows
-            buf = (ctypes.c_int64 * max(n, 1))()
+            raw = np.empty(max(n, 1), dtype=np.int64)
             got = ctypes.c_int64(0)
-            self.engine.check(lib.ps_replay_decisions(self.engine.handle, buf, n, ctypes.byref(got)))
-            for i in range(n):
-                v = buf[i]
-                rel = tuple(q for q in range(56) if (v >> (8 + q)) & 1)
-                out.append(("grant" if (v & 0xff) == 0 else "defer", rel))
+            self.engine.check(lib.ps_replay_decisions(
+                self.engine.handle, raw.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n,
+                ctypes.byref(got)))
+            raw = raw[:n]
         self.engine.refresh()
-        return ReplayReport(decisions=out, applied=res.applied, rejected=res.rejected,
+        return ReplayReport(raw=raw, applied=res.applied, rejected=res.rejected,
                             pushes=res.pushes, device_ms=res.device_ms)
 
 
