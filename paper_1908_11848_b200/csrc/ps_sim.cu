@@ -371,6 +371,8 @@ __device__ void control_warp_regs(const SimArgs& a) {
   unsigned finished = 0;
   int seq = 0, status = PS_OK;
   long long processed = 0, n_ops = 0, n_trace = 0, pushes = 0, next_slot = 0;
+  double pend_v = 0.0;  // a compute draw in flight to nct[pend_w]
+  int pend_w = -1;
   auto emit = [&](int type, int w, int buf, long long slot) {
     if (w0) st_relaxed_u64(ops + n_ops, op_pack(tag, type, w, buf, slot));
     n_ops += 1;
@@ -445,12 +447,17 @@ __device__ void control_warp_regs(const SimArgs& a) {
     } else if (kind == PS_EV_PULL_RETURN) {
       rset<PM>(active, w, rget<PM>(staged, w));  // adopt (simnet.py:156-165)
       trace_row(at, w, kind, -1, 0);
+      if (pend_w >= 0) { rset<PM>(nct, pend_w, pend_v); pend_w = -1; }
       if (rget<PM>(iters, w) < budget) schedule(at + rget<PM>(nct, w), PS_EV_COMPUTE_DONE, w);
       else finished |= 1u << w;
     } else if (kind == PS_EV_COMPUTE_DONE) {
       const int it = rget<PM>(iters, w) + 1;
       rset<PM>(iters, w, it);
-      if (it < budget) rset<PM>(nct, w, a.ctime[(long long)w * budget + it]);  // prefetch the next draw
+      // the next draw: loaded now, written into the table only when a later
+      // event needs it, so the load's latency hides behind those events
+      if (pend_w >= 0) rset<PM>(nct, pend_w, pend_v);
+      pend_w = -1;
+      if (it < budget) { pend_v = a.ctime[(long long)w * budget + it]; pend_w = w; }
       const long long slot = next_slot++;
       rset<PM>(gslot, w, (int)slot);
       emit(OP_GRAD, w, bowl ? rget<PM>(active, w) : rget<PM>(sidx, w) % nsyn, slot);
@@ -465,51 +472,50 @@ __device__ void control_warp_regs(const SimArgs& a) {
       // running, each push is its own apply -> decide under the server lock
       // (runner.py:226-249).
       unsigned rest = 0;
+      if (!realtime) {
 #pragma unroll
-      for (int q = 0; q < PM; ++q)
-        if (!realtime && q < P && ev_kind[q] == PS_EV_PUSH_ARRIVE && ev_time[q] == at) {
-          rest |= 1u << q;
-          ev_kind[q] = -1;
-        }
-      int order[PM];
+        for (int q = 0; q < PM; ++q)
+          if (q < P && ev_kind[q] == PS_EV_PUSH_ARRIVE && ev_time[q] == at) {
+            rest |= 1u << q;
+            ev_kind[q] = -1;
+          }
+      }
+      // the group's order as a packed list of 4-bit worker ids: the loops
+      // below run n times (usually once) instead of being unrolled PM times
+      // around an inlined gate
+      unsigned long long order = (unsigned long long)w;
       int n = 1;
-      order[0] = w;
-#pragma unroll
-      for (int i = 1; i < PM; ++i) {
+      while (rest) {
         int m = -1, ms = 0;
 #pragma unroll
         for (int q = 0; q < PM; ++q)
           if (((rest >> q) & 1u) && (m < 0 || ev_seq[q] < ms)) { m = q; ms = ev_seq[q]; }
-        order[i] = m;
-        if (m >= 0) { rest &= ~(1u << m); n = i + 1; }
+        rest &= ~(1u << m);
+        order |= (unsigned long long)m << (4 * n);
+        n += 1;
       }
-#pragma unroll
-      for (int i = 0; i < PM; ++i) {
-        if (i < n) {
-          const int m = order[i];
-          const int si = rget<PM>(sidx, m);
-          emit(OP_APPLY, m, bowl ? 0 : si % nsyn, rget<PM>(gslot, m));
-          rset<PM>(sidx, m, si + 1);
-        }
+#pragma unroll 1
+      for (int i = 0; i < n; ++i) {
+        const int m = (int)((order >> (4 * i)) & 15ull);
+        const int si = rget<PM>(sidx, m);
+        emit(OP_APPLY, m, bowl ? 0 : si % nsyn, rget<PM>(gslot, m));
+        rset<PM>(sidx, m, si + 1);
       }
-#pragma unroll
-      for (int i = 0; i < PM; ++i) {
-        if (i < n && status == PS_OK) {
-          const int m = order[i];
-          PROF_MARK(t_g);
-          const GateResult r = g.on_push(m, at);
-          PROF_ADD(c_gate, t_g);
-          pushes += 1;
-          if (r.status != PS_OK) {
-            status = r.status;
-          } else {
-            trace_row(at, m, PS_EV_PUSH_ARRIVE, r.outcome, r.released);
-            if (r.outcome == 0) {
-              schedule(at + comm, PS_EV_GRANT_DELIVER, m);
-#pragma unroll
-              for (int q = 0; q < PM; ++q)
-                if ((r.released >> q) & 1ull) schedule(at + comm, PS_EV_GRANT_DELIVER, q);
-            }
+#pragma unroll 1
+      for (int i = 0; i < n && status == PS_OK; ++i) {
+        const int m = (int)((order >> (4 * i)) & 15ull);
+        PROF_MARK(t_g);
+        const GateResult r = g.on_push(m, at);
+        PROF_ADD(c_gate, t_g);
+        pushes += 1;
+        if (r.status != PS_OK) {
+          status = r.status;
+        } else {
+          trace_row(at, m, PS_EV_PUSH_ARRIVE, r.outcome, r.released);
+          if (r.outcome == 0) {
+            schedule(at + comm, PS_EV_GRANT_DELIVER, m);
+            for (unsigned long long rel = r.released; rel; rel &= rel - 1)
+              schedule(at + comm, PS_EV_GRANT_DELIVER, __ffsll((long long)rel) - 1);
           }
         }
       }
