@@ -186,8 +186,11 @@ int ps_abort(ps_server* h);
  * boundary call sequence (handle_pull / apply_gradient / decide_push, in the
  * order the simulator issues them) executed in one persistent kernel: pulls
  * and applies as data ops, every decide through the device gate (decisions
- * retrievable with ps_replay_decisions as (released << 8) | outcome). Updates
- * are resident: apply k of worker p uses synthetic[p][k % n_synthetic]. */
+ * retrievable with ps_replay_decisions as (released << 8) | outcome, hence at
+ * most 55 workers). Updates are resident: apply k of worker p uses
+ * synthetic[p][k % n_synthetic]. A protocol violation stops the data at the
+ * offending call (PS_E_PROTOCOL); a non-finite update is rejected and
+ * counted (ps_sim_result.rejected). */
 enum { PS_CALL_PULL = 0, PS_CALL_APPLY = 1, PS_CALL_DECIDE = 2 };
 typedef struct ps_replay_call {
   double now;       /* PS_CALL_DECIDE: the push instant */

@@ -1848,6 +1848,8 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   const int P = h->cfg.worker_count;
   if (n < 0 || (n > 0 && !calls)) return ps_fail(h, PS_E_VALUE, "bad call list");
   if (!synthetic || n_synthetic < 1) return ps_fail(h, PS_E_VALUE, "replay needs resident updates");
+  // a decision word carries the released set in bits 8..63
+  if (P > 55) return ps_fail(h, PS_E_VALUE, "replay supports at most 55 workers");
   ps_sim_buffers& b = h->sim;
   int rc;
   size_t cap;

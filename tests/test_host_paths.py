@@ -2,8 +2,12 @@
 derived from a trace equals the reference's recorded boundary calls, and the
 PyTorch worker flattening keeps parameters and gradients as views."""
 
+import os
+
 import oracle
 from paper_1908_11848_b200.sim import calls_from_trace
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 from paper_1908_11848_b200.trace import TraceEntry
 
 
@@ -44,3 +48,27 @@ def test_flatten_makes_views():
         assert p.grad.data_ptr() == flat_g[off:off + k].data_ptr()
         assert float(p.data.reshape(-1)[0]) == float(off)
         off += k
+
+
+def test_decision_words_decode_like_the_reference_tokens():
+    """ps_replay_decisions words ((released << 8) | outcome) decode into the
+    reference's SyncDecision shape (policy.py:33-40): outcome, released ids
+    ascending."""
+    from paper_1908_11848_b200.sim import decode_decisions
+    words = [0, 1, (0b1011 << 8) | 0, (1 << 54) << 8]
+    assert decode_decisions(words) == [("grant", ()), ("defer", ()), ("grant", (0, 1, 3)),
+                                       ("grant", (54,))]
+
+
+def test_replay_call_array_layout_matches_the_c_abi():
+    """DeviceReplay packs calls as ps_replay_call {double now; int32 kind;
+    int32 worker} (include/dssp_ps.h)."""
+    import ctypes
+    from paper_1908_11848_b200 import sim
+    assert sim._CALL_DTYPE.itemsize == 16
+    assert [sim._CALL_DTYPE.fields[k][1] for k in ("now", "kind", "worker")] == [0, 8, 12]
+    assert (sim.CALL_PULL, sim.CALL_APPLY, sim.CALL_DECIDE) == (0, 1, 2)
+    header = open(os.path.join(ROOT, "include", "dssp_ps.h")).read()
+    for name in ("PS_CALL_PULL", "PS_CALL_APPLY", "PS_CALL_DECIDE"):
+        assert name in header
+    assert ctypes.sizeof(ctypes.c_double) + 2 * ctypes.sizeof(ctypes.c_int32) == 16
