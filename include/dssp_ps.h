@@ -240,6 +240,10 @@ int ps_shard_ipc_handles(ps_shard_server* h, void* out, int64_t cap); /* returns
 int ps_shard_connect(ps_shard_server* h, const void* blobs, int64_t len);
 /* The worker's update buffer (device, fp32, padded_len >= d): push source. */
 int ps_shard_update_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len);
+/* The worker's replica (device, fp32): starts as w0 and is rewritten by every
+ * owner at each pull (handle_pull, server.py:84-91); a GPU-resident worker can
+ * keep its model parameters in it. */
+int ps_shard_replica_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len);
 /* Run `steps` push groups (tickets t0..t0+steps-1, one push per rank each,
  * applied in rank order then decided in rank order at virtual time now[i]),
  * each followed by this rank's pull into dst (device fp32, >= round_up(d,4)

@@ -542,6 +542,7 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
   if ((e = cudaMalloc(&h->upd, h->dpad * sizeof(float)))) return bail("update buffer");
   if ((e = cudaMemset(h->upd, 0, h->dpad * sizeof(float)))) return bail("update memset");
   if ((e = cudaMalloc(&h->rep, h->dpad * sizeof(float)))) return bail("replica");
+  if ((e = cudaMemset(h->rep, 0, h->dpad * sizeof(float)))) return bail("replica memset");
   if ((e = cudaMalloc(&h->flags, 3 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags");
   if ((e = cudaMemset(h->flags, 0, 3 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags memset");
   if ((e = cudaMalloc(&h->ctl, sizeof(ShardCtl)))) return bail("ctl");
@@ -555,20 +556,28 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
   gs.threshold = cfg->paradigm == PS_BSP ? 0 : cfg->s_lower;
   for (int r = 0; r < kMaxRanks; ++r) h->hctl->order[1][r] = r;  // step 1: initial pulls arrive in worker order
   if ((e = cudaMemcpy(h->ctl, h->hctl, sizeof(ShardCtl), cudaMemcpyHostToDevice))) return bail("ctl upload");
-  // w0: full-length initial weights; bit 0 of w0_flags = on device, bit 1 = fp64
+  // w0: full-length initial weights; bit 0 of w0_flags = on device, bit 1 = fp64.
+  // The shard gets its range; the worker's replica starts as the whole vector
+  // (the worker's first pull, simnet.py:135-138, before it computes anything).
   if (w0) {
     const bool on_dev = w0_flags & 1, f64 = w0_flags & 2;
     const size_t esz = f64 ? 8 : 4;
-    const char* src = (const char*)w0 + (size_t)h->lo * esz;
+    const char* src = (const char*)w0;
     void* tmp = nullptr;
     if (!on_dev) {
-      if ((e = cudaMalloc(&tmp, h->n_local * esz + 16))) return bail("w0 staging");
-      if ((e = cudaMemcpy(tmp, src, h->n_local * esz, cudaMemcpyHostToDevice))) return bail("w0 upload");
+      if ((e = cudaMalloc(&tmp, h->d * esz + 16))) return bail("w0 staging");
+      if ((e = cudaMemcpy(tmp, src, h->d * esz, cudaMemcpyHostToDevice))) return bail("w0 upload");
       src = (const char*)tmp;
     }
-    if (h->n_local > 0) {
-      if (f64) k_shard_load<double><<<h->sm_count * 2, 256, 0, h->stream>>>((const double*)src, h->w, h->n_local);
-      else k_shard_load<float><<<h->sm_count * 2, 256, 0, h->stream>>>((const float*)src, h->w, h->n_local);
+    const char* mine = src + (size_t)h->lo * esz;
+    if (f64) {
+      if (h->n_local > 0)
+        k_shard_load<double><<<h->sm_count * 2, 256, 0, h->stream>>>((const double*)mine, h->w, h->n_local);
+      k_shard_load<double><<<h->sm_count * 2, 256, 0, h->stream>>>((const double*)src, h->rep, h->d);
+    } else {
+      if (h->n_local > 0)
+        k_shard_load<float><<<h->sm_count * 2, 256, 0, h->stream>>>((const float*)mine, h->w, h->n_local);
+      k_shard_load<float><<<h->sm_count * 2, 256, 0, h->stream>>>((const float*)src, h->rep, h->d);
     }
     if ((e = cudaStreamSynchronize(h->stream))) return bail("w0 convert");
     if (tmp) cudaFree(tmp);
@@ -642,6 +651,15 @@ int ps_shard_connect(ps_shard_server* h, const void* blobs, int64_t len) {
 // Device pointer of this rank's update buffer (the worker writes its update here).
 int ps_shard_update_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len) {
   *ptr = h->upd;
+  *padded_len = h->dpad;
+  return PS_OK;
+}
+
+// Device pointer of this rank's replica: the worker's copy of the weights,
+// written by every owner at each pull (a worker may keep its model
+// parameters right here and compute on them between runs).
+int ps_shard_replica_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len) {
+  *ptr = h->rep;
   *padded_len = h->dpad;
   return PS_OK;
 }

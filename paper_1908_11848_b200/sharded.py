@@ -118,6 +118,9 @@ class ShardedServer:
         padded = ctypes.c_int64(0)
         self.lib.ps_shard_update_buffer(self._h, ctypes.byref(p), ctypes.byref(padded))
         self.update = torch.as_tensor(_CudaArray(p.value, padded.value), device=f"cuda:{self.device}")
+        # the worker's replica: w0 at start, rewritten by every owner at each pull
+        self.lib.ps_shard_replica_buffer(self._h, ctypes.byref(p), ctypes.byref(padded))
+        self.replica = torch.as_tensor(_CudaArray(p.value, padded.value), device=f"cuda:{self.device}")
         self.lo, self.hi = shard_range(self.dimension, self.world, self.rank)
         self.ticket = 1
 

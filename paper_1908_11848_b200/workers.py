@@ -70,18 +70,27 @@ def resnet50_cifar(num_classes=10):
     return torchvision.models.resnet50(num_classes=num_classes)
 
 
-def flatten_(model: nn.Module, device="cuda"):
+def flatten_(model: nn.Module, device="cuda", into=None, copy_params=True):
     """Re-home every parameter and its gradient as views of two flat fp32
-    buffers (padded to a multiple of 4 floats). Returns (params, grads)."""
+    buffers (padded to a multiple of 4 floats). ``into=(params, grads)``
+    uses caller-owned buffers instead -- e.g. a sharded server's replica and
+    update buffer, so pulls land in the parameters and pushes read the
+    gradients with no copy at all. Returns (params, grads, n)."""
     params = [p for p in model.parameters()]
     n = sum(p.numel() for p in params)
     pad = (n + 3) // 4 * 4
-    flat_p = torch.zeros(pad, dtype=torch.float32, device=device)
-    flat_g = torch.zeros(pad, dtype=torch.float32, device=device)
+    if into is None:
+        flat_p = torch.zeros(pad, dtype=torch.float32, device=device)
+        flat_g = torch.zeros(pad, dtype=torch.float32, device=device)
+    else:
+        flat_p, flat_g = into
+        if flat_p.numel() < n or flat_g.numel() < n:
+            raise ValueError(f"buffers hold {flat_p.numel()} / {flat_g.numel()} floats, model has {n}")
     off = 0
     for p in params:
         k = p.numel()
-        flat_p[off:off + k].copy_(p.data.reshape(-1))
+        if copy_params:
+            flat_p[off:off + k].copy_(p.data.reshape(-1))
         p.data = flat_p[off:off + k].view_as(p)
         p.grad = flat_g[off:off + k].view_as(p)
         off += k

@@ -42,3 +42,22 @@ def test_sharded_parity(tmp_path, world, gmax):
         for c in v["checks"]:
             assert c["trace"] and c["shard"] and c["replica"], c
             assert c["version"] == c["steps"] * world
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_torch_workers_on_the_sharded_server(tmp_path, world):
+    """Real ResNet-20 workers whose parameters live in the server's replica
+    and whose gradients live in its update buffer: every step's weights equal
+    the fp32 replay of all workers' gradients in the gate's ticket order."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(29470 + world), os.path.join(ROOT, "tests", "_sharded_torch_worker.py"),
+           str(tmp_path)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    for f in sorted(glob.glob(str(tmp_path / "torch_rank*.json"))):
+        for c in json.load(open(f)):
+            assert c["ok"], c
+            assert c["version"] == 6 * world, c
