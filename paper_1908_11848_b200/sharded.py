@@ -230,6 +230,60 @@ def bandwidth_sweep(world, rank, local, warm, steps):
     return rows
 
 
+def torch_workers_bench(world, rank, local, warm, steps, batch=128):
+    """configs[2] with real workers: a torchvision ResNet-50 (10 classes,
+    23,528,522 parameters) per GPU on synthetic 32x32x3 batches, parameters
+    living in the server's replica and gradients in its update buffer; one
+    step = every worker's forward/backward + one sharded push/apply/pull.
+    Returns rank 0's iterations/s per paradigm (max-over-ranks time)."""
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+    from .workers import flatten_, resnet50_cifar, synthetic_cifar
+
+    out = {}
+    for name, s, r in PARADIGMS:
+        torch.manual_seed(0)
+        model = resnet50_cifar().cuda()
+        w0 = torch.cat([p.detach().reshape(-1) for p in model.parameters()])
+        d = w0.numel()
+        cfg = validate_config(make_config(
+            paradigm=name, worker_count=world, s_lower=s, r_max=r, timing_preset="homogeneous",
+            compute_base=1.0, comm_delay=0.05, learning_rate=0.01, seed=0, dimension=d,
+            batch_size=batch, dataset_size=world * batch))
+        srv = ShardedServer(cfg, d, rank, world, local, w0_device=w0)
+        flatten_(model, into=(srv.replica, srv.update), copy_params=False)
+        del w0
+        batches = synthetic_cifar(2, batch, seed=100 + rank)
+        times = homogeneous_push_times(1.0, 0.05, warm + steps)
+        ps_ms = 0.0
+
+        def step(i):
+            x, y = batches[i % 2]
+            srv.update.zero_()
+            F.cross_entropy(model(x), y).backward()
+            return srv.run(times[i:i + 1])
+
+        for i in range(warm):
+            step(i)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(warm, warm + steps):
+            ps_ms += step(i)
+        torch.cuda.synchronize()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        out[name] = {"iters_per_s": steps * world / wall, "server_share_of_wall": ps_ms * 1e-3 / wall,
+                     "model": "ResNet-50 (torchvision, 10 classes, 23,528,522 params)",
+                     "batch_per_worker": batch, "workers": world}
+        torch.cuda.synchronize()
+        dist.barrier()
+        srv.close()
+        del model
+        torch.cuda.empty_cache()
+    return out
+
+
 def bench_main(args, metric):
     import torch
     import torch.distributed as dist
@@ -304,6 +358,8 @@ def bench_main(args, metric):
         dist.barrier()  # no peer may still be reading this rank's memory
         srv.close()
     sweep = bandwidth_sweep(world, rank, local, warm, steps) if not getattr(args, "no_sweep", False) else []
+    tw = (torch_workers_bench(world, rank, local, max(warm, 5), min(steps, 10))
+          if not getattr(args, "no_sweep", False) else None)
     if sampler is not None:
         sampler.__exit__(None, None, None)
     if rank == 0:
@@ -332,6 +388,7 @@ def bench_main(args, metric):
                          "bytes_model": "2*(G-1)*S*4 B received over NVLink per GPU per step"},
             "cpu_baseline": None,
             "sweep": sweep,
+            "torch_workers": tw,
             "clocks": sampler.summary() if sampler else None,
         }
         print(json.dumps(line))
