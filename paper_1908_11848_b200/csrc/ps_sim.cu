@@ -1853,20 +1853,7 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   ps_sim_buffers& b = h->sim;
   int rc;
   size_t cap;
-  const size_t ops = 2 * (size_t)n + 8;  // a GRAD and an APPLY per apply call at most
-  if (b.ops_cap < ops || !b.ops) {
-    cudaFree(b.ops);
-    b.ops = nullptr;
-    PS_CK(h, cudaMalloc(&b.ops, ops * sizeof(Op)));
-    PS_CK(h, cudaMemsetAsync(b.ops, 0, ops * sizeof(Op), h->stream));
-    b.ops_cap = ops;
-    b.tag = 0;
-  }
-  b.tag = (b.tag + 1) & 0xffffu;
-  if (b.tag == 0) {
-    PS_CK(h, cudaMemsetAsync(b.ops, 0, b.ops_cap * sizeof(Op), h->stream));
-    b.tag = 1;
-  }
+  // (no op log: the data warps number the calls themselves)
   // replay verdicts: one {CTAs done, non-finite bits} pair per 32-call chunk
   const size_t slots = 2 * ((size_t)n / 32 + 4);
   if (b.slots_cap < slots || !b.gcount) {
@@ -1905,15 +1892,14 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   a.nv = h->nv;
   a.dpad = h->dpad;
   a.trace_cap = (long long)b.dec_cap;
-  a.ops_cap = (long long)ops;
+  a.ops_cap = 0;
   a.lr = (float)h->cfg.learning_rate;
   a.W = h->w[h->cur];
   a.rep = b.rep;
   a.gbuf = b.gbuf;
   a.synth = synthetic;
-  a.ops = (Op*)b.ops;
+  a.ops = nullptr;
   a.gword = b.gcount;
-  a.tag = b.tag;
   a.n_ctas = (unsigned)(grid - 1);
   a.calls = (const ReplayCall*)b.calls;
   a.n_calls = n;
