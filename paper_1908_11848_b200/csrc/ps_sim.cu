@@ -810,13 +810,17 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
       const unsigned hit = __ballot_sync(kFull, ((rng >> lane) & 1u) && ((dm >> (c.worker & 63)) & 1ull));
       if (hit) fail = __ffs(hit) - 1;
     };
-    while (md && fail < 0) {
-      const int i = __ffs(md) - 1;
+    // the next decide's (worker, now) is fetched while this one is decided
+    int i = md ? __ffs(md) - 1 : -1;
+    int w = __shfl_sync(kFull, c.worker, i & 31);
+    double now = __shfl_sync(kFull, c.now, i & 31);
+    while (i >= 0 && fail < 0) {
       md &= md - 1;
+      const int ni = md ? __ffs(md) - 1 : -1;
+      const int nw = __shfl_sync(kFull, c.worker, ni & 31);
+      const double nnow = __shfl_sync(kFull, c.now, ni & 31);
       check_pulls(prev, i);
       if (fail >= 0) break;
-      const int w = __shfl_sync(kFull, c.worker, i);
-      const double now = __shfl_sync(kFull, c.now, i);
 #ifdef PS_SIM_PROFILE
       const long long tg = clock64();
 #endif
@@ -830,6 +834,9 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
         a.decisions[n_dec] = (long long)((r.released << 8) | (unsigned)r.outcome);
       n_dec += 1;
       prev = i + 1;
+      i = ni;
+      w = nw;
+      now = nnow;
     }
     if (fail < 0) check_pulls(prev, limit);
     if (fail < 0 && limit < m) fail = limit;
