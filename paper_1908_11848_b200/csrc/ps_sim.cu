@@ -607,6 +607,12 @@ __device__ void control_warp_lanes(const SimArgs& a) {
   };
   for (int q = 0; q < P; ++q) schedule(comm, PS_EV_PULL_ARRIVE, q);
   if (lane == 0) a.out->t_start = globaltimer_ns();
+  // free-running (mode 2): see control_warp_regs
+  const bool realtime = a.mode == 2;
+  const double ns_per_s = 1e9 * a.time_scale;
+  const unsigned long long t_real0 = __shfl_sync(kFull, globaltimer_ns(), 0);
+  const unsigned long long deadline = t_real0 + a.deadline_ns;
+  bool aborted = false;
   for (;;) {
     // pop the (time, seq)-minimum event: time bits, then seq
     const bool cand = mine && ev_kind >= 0;
@@ -620,7 +626,17 @@ __device__ void control_warp_lanes(const SimArgs& a) {
     if (!who) break;
     const int w = __ffs(who) - 1;
     if (a.max_events > 0 && processed >= a.max_events) { status = PS_E_BUDGET; break; }
-    const double at = from_lane(ev_time, w);
+    double at = from_lane(ev_time, w);
+    if (realtime) {
+      const unsigned long long due = t_real0 + (unsigned long long)(at * ns_per_s);
+      unsigned long long nw;
+      bool stop = (processed & 63) == 0 && ld_volatile_s32(a.abort_flag);
+      while (!stop && (nw = globaltimer_ns()) < due) stop = nw > deadline || ld_volatile_s32(a.abort_flag);
+      nw = __shfl_sync(kFull, globaltimer_ns(), 0);
+      stop = __shfl_sync(kFull, stop, 0);
+      if (stop || nw > deadline) { aborted = true; break; }
+      at = (double)(nw - t_real0) / ns_per_s;
+    }
     const int kind = from_lane(ev_kind, w);
     if (lane == w) ev_kind = -1;
     processed += 1;
@@ -651,7 +667,7 @@ __device__ void control_warp_lanes(const SimArgs& a) {
     } else {
       // PUSH_ARRIVE: every push queued at the same instant joins the group
       // (simnet.py:167-182); the popped one first, the rest by seq.
-      const bool join = mine && ev_kind == PS_EV_PUSH_ARRIVE && dbits(ev_time) == dbits(at);
+      const bool join = !realtime && mine && ev_kind == PS_EV_PUSH_ARRIVE && dbits(ev_time) == dbits(at);
       unsigned rest = __ballot_sync(kFull, join);
       if (join) ev_kind = -1;
       int n = 1;
@@ -698,7 +714,8 @@ __device__ void control_warp_lanes(const SimArgs& a) {
     a.out->events = processed;
     a.out->pushes = pushes;
     a.out->trace_rows = n_trace;
-    a.out->unfinished = status == PS_OK ? (unsigned long long)(all & ~done) : 0ull;
+    a.out->unfinished = (status == PS_OK || aborted) ? (unsigned long long)(all & ~done) : 0ull;
+    if (aborted) status = PS_E_TIMEOUT;
     if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
   }
 }
@@ -1682,8 +1699,8 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   const int P = h->cfg.worker_count;
   if (sc->budget < 0) return ps_fail(h, PS_E_VALUE, "budget must be >= 0");
   if (sc->mode != 0 && sc->mode != 2) return ps_fail(h, PS_E_VALUE, "mode must be 0 or 2");
-  if (sc->mode == 2 && (P > 8 || !(sc->time_scale > 0)))
-    return ps_fail(h, PS_E_VALUE, "free-running runs need P <= 8 and time_scale > 0");
+  if (sc->mode == 2 && (P > kLaneP || !(sc->time_scale > 0)))
+    return ps_fail(h, PS_E_VALUE, "free-running runs need P <= 32 and time_scale > 0");
   if (sc->mode == 2 && !h->habort) {
     PS_CK(h, cudaHostAlloc((void**)&h->habort, sizeof(int), cudaHostAllocMapped));
     PS_CK(h, cudaHostGetDevicePointer((void**)&h->habort_dev, h->habort, 0));

@@ -122,3 +122,25 @@ def test_abort_from_another_thread():
     timer.join()
     assert not rep.completed and rep.stuck
     assert elapsed < 10.0
+
+
+@pytest.mark.parametrize("workers,paradigm", [(12, "dssp"), (24, "ssp"), (32, "dssp")])
+def test_free_running_lane_gate_for_larger_clusters(workers, paradigm):
+    """9-32 workers run on the lane-per-worker control warp (ctl_lanes.cuh);
+    the free-running mode there is held to the same oracle checks."""
+    cfg = ps.validate_config(ps.make_config(
+        paradigm=paradigm, worker_count=workers, s_lower=2, r_max=6 if paradigm == "dssp" else 0,
+        timing_preset="lognormal", compute_base=1.0, comm_delay=0.05, model_kind="quadratic_bowl",
+        dimension=257, dataset_size=workers * 8, batch_size=4, epochs=3, learning_rate=0.05, seed=3))
+    sim = ps.DeviceSimulation(cfg, dimension=257, grad="bowl")
+    ref = sim.run(loss_every=0)                  # simulated: the schedule's length
+    span = max(e.time for e in ref.entries)
+    sim2 = ps.DeviceSimulation(cfg, dimension=257, grad="bowl")
+    rep = sim2.run(loss_every=0, realtime_scale=0.05 / span, deadline_s=20.0)
+    assert rep.completed
+    pushes = [e for e in rep.entries if e.kind == "push_arrive"]
+    assert len(pushes) == workers * sim2.budget
+    assert [e.decision for e in pushes] == _gate_tokens(cfg, rep.entries)
+    w32, applied = _replay(cfg, rep.entries, 257)
+    assert applied == rep.applied
+    assert np.array_equal(rep.final_weights.view(np.uint32), w32.view(np.uint32))
