@@ -397,8 +397,34 @@ def c2_schedule():
     _dump("c2_schedule.json.gz", {"runs": out}, gz=True)
 
 
+def sim_large():
+    """Worker counts beyond the main corpus: P = 1 (serial SGD), and the
+    lane-per-worker (9..32) and shared-memory (33..64) control-warp layouts
+    of the device run loop, every paradigm, closed-loop quadratic bowl."""
+    runs = []
+    k = 0
+    for workers in (1, 12, 33, 64):
+        for paradigm, s, r in (("dssp", 2, 6), ("ssp", 2, 0), ("bsp", 0, 0), ("asp", 0, 0)):
+            preset = ("lognormal", "gtx-mix", "straggler", "jitter")[k % 4]
+            runs.append((f"large_{paradigm}_p{workers}_{preset}", dict(
+                paradigm=paradigm, worker_count=workers, s_lower=s, r_max=r,
+                timing_preset=preset, compute_base=1.0, comm_delay=(0.01, 0.05)[k % 2],
+                straggler_ratio=3.0, model_kind="quadratic_bowl", dimension=(33, 130)[k % 2],
+                dataset_size=8 * workers, batch_size=4, learning_rate=0.05, epochs=3, seed=40 + k),
+                True))
+            k += 1
+    out = []
+    for name, flat, keep in runs:
+        rec = _run_recorded(flat, keep)
+        rec["name"] = name
+        out.append(rec)
+    _dump("sim_large.json.gz", {"runs": out}, gz=True)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2"]
+    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2", "large"]
+    if "large" in which:
+        sim_large()
     if "c2" in which:
         c2_schedule()
     if "controller" in which:
