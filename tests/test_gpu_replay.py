@@ -16,8 +16,11 @@ from paper_1908_11848_b200.sim import DeviceReplay  # noqa: E402
 
 
 def _runs():
+    # sim_large: P = 1, 12, 33 (the decision word carries at most 55 workers)
+    large = [r for r in oracle.load_golden("sim_large.json.gz")["runs"]
+             if r["normalized"]["worker_count"] <= 55]
     return oracle.load_golden("sim_corpus.json.gz")["runs"] + \
-        oracle.load_golden("c2_schedule.json.gz")["runs"]
+        oracle.load_golden("c2_schedule.json.gz")["runs"] + large
 
 
 @pytest.mark.parametrize("d", [5, 4099, 272_474])
@@ -133,3 +136,15 @@ def test_replay_rejects_nonfinite_updates_per_call(d):
     # decisions do not depend on the data
     assert rep.decisions == [(c[3], tuple(c[4])) for c in run["calls"] if c[0] == "decide"]
     eng.close()
+
+
+def test_replay_empty_stream_and_worker_limit():
+    eng = Engine("dssp", 4, 3, 12, 0.05, 64)
+    synth = torch.zeros(4, 1, 64, device="cuda")
+    rep = DeviceReplay(eng, [], synth, 1).run()
+    assert rep.applied == 0 and rep.decisions == []
+    eng.close()
+    big = Engine("asp", 56, 0, 0, 0.05, 8)
+    with pytest.raises(ValueError):
+        DeviceReplay(big, [("pull", 0)], torch.zeros(56, 1, 8, device="cuda"), 1).run()
+    big.close()
