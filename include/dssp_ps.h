@@ -234,6 +234,11 @@ int ps_shard_range(int64_t d, int32_t world, int32_t rank, int64_t* lo, int64_t*
 /* w0: full-length initial weights; w0_flags bit 0 = device pointer, bit 1 = fp64. */
 int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const void* w0,
                     int64_t w0_flags, ps_shard_server** out);
+/* Collective shutdown: every rank calls ps_shard_disconnect (unmaps its
+ * peers' buffers), the ranks synchronize, then every rank calls
+ * ps_shard_destroy (frees its own). A process must not free memory a peer
+ * still has mapped. */
+int ps_shard_disconnect(ps_shard_server* h);
 void ps_shard_destroy(ps_shard_server* h);
 const char* ps_shard_last_error(const ps_shard_server* h);
 int ps_shard_ipc_handles(ps_shard_server* h, void* out, int64_t cap); /* returns blob size */

@@ -109,6 +109,7 @@ SIGNATURES = {
     "ps_shard_ipc_handles": (ctypes.c_int, [_P, _P, _I64]),
     "ps_shard_connect": (ctypes.c_int, [_P, _P, _I64]),
     "ps_shard_destroy": (None, [_P]),
+    "ps_shard_disconnect": (ctypes.c_int, [_P]),
     "ps_shard_last_error": (ctypes.c_char_p, [_P]),
     "ps_shard_update_buffer": (ctypes.c_int, [_P, ctypes.POINTER(_P), _PI64]),
     "ps_shard_replica_buffer": (ctypes.c_int, [_P, ctypes.POINTER(_P), _PI64]),

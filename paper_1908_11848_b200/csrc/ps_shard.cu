@@ -273,6 +273,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
           wdst[j] = x;
           for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
         }
+      __threadfence_system();  // every warp's replica stores before F(t) (see below)
       redo_bad = __syncthreads_or(redo_bad);
       redo_n += 1;
       if (threadIdx.x == 0) {
@@ -390,13 +391,14 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     gbad = __reduce_or_sync(kFull, gbad);
     dbad = __reduce_or_sync(kFull, dbad);
     if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
+    // every warp's stores to peers must have landed before any peer can see
+    // V(t). The fence is issued by every warp that stored: measured, a fence
+    // in one thread after the barrier (or one fence in the election winner)
+    // let a peer read the tail of a slice stale after V(t).
+    __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
       if (s_bits) atomicOr(&ctl->bad, s_bits);
-      // this CTA's stores (local and to peers) are released at GPU scope; the
-      // winner acquires them all and its fence.sc.sys orders them before V(t)
-      // at system scope (causality order is transitive across scopes) -- one
-      // system fence per step instead of one per CTA
       const unsigned long long prev = atom_add_acq_rel_gpu_u64(&ctl->arrive_total, 1ull);
       SPROF(if (blockIdx.x == 0) g_prof[1] += globaltimer_ns() - g_t_resolved);
       if (prev == t * (unsigned long long)ndata - 1) {
@@ -536,14 +538,19 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
   };
   if ((e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking))) return bail("stream");
   if ((e = cudaEventCreate(&h->ev0)) || (e = cudaEventCreate(&h->ev1))) return bail("events");
-  if ((e = cudaMalloc(&h->w, shard_bytes)) || (e = cudaMalloc(&h->w_alt, shard_bytes))) return bail("shard");
+  // Every buffer a peer maps through CUDA IPC gets its own 2 MB-granular
+  // allocation: small allocations are carved out of shared blocks, and an IPC
+  // mapping of a block outlives the buffer it was opened for (measured: a
+  // later server's replica mapped through a stale block of an earlier one).
+  auto ipc_bytes = [](size_t b) { return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1); };
+  if ((e = cudaMalloc(&h->w, ipc_bytes(shard_bytes))) || (e = cudaMalloc(&h->w_alt, shard_bytes))) return bail("shard");
   if ((e = cudaMemset(h->w, 0, shard_bytes)) || (e = cudaMemset(h->w_alt, 0, shard_bytes)))
     return bail("shard memset");
-  if ((e = cudaMalloc(&h->upd, h->dpad * sizeof(float)))) return bail("update buffer");
+  if ((e = cudaMalloc(&h->upd, ipc_bytes(h->dpad * sizeof(float))))) return bail("update buffer");
   if ((e = cudaMemset(h->upd, 0, h->dpad * sizeof(float)))) return bail("update memset");
-  if ((e = cudaMalloc(&h->rep, h->dpad * sizeof(float)))) return bail("replica");
+  if ((e = cudaMalloc(&h->rep, ipc_bytes(h->dpad * sizeof(float))))) return bail("replica");
   if ((e = cudaMemset(h->rep, 0, h->dpad * sizeof(float)))) return bail("replica memset");
-  if ((e = cudaMalloc(&h->flags, 3 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags");
+  if ((e = cudaMalloc(&h->flags, ipc_bytes(3 * kMaxRanks * sizeof(unsigned long long))))) return bail("flags");
   if ((e = cudaMemset(h->flags, 0, 3 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags memset");
   if ((e = cudaMalloc(&h->ctl, sizeof(ShardCtl)))) return bail("ctl");
   if ((e = cudaMallocHost(&h->hctl, sizeof(ShardCtl)))) return bail("hctl");
@@ -583,6 +590,22 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
     if (tmp) cudaFree(tmp);
   }
   *out = h;
+  return PS_OK;
+}
+
+// First half of a collective shutdown: unmap every peer buffer this rank
+// opened. A peer must not free memory another process still has mapped (CUDA
+// IPC: undefined behaviour -- measured, a later server's mapping then
+// aliased stale pages), so every rank disconnects, the ranks synchronize,
+// and only then does each free its own buffers (ps_shard_destroy).
+int ps_shard_disconnect(ps_shard_server* h) {
+  if (!h) return PS_OK;
+  Dev guard(h->dev);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->opened) cudaIpcCloseMemHandle(p);
+  h->opened.clear();
+  for (int r = 0; r < kMaxRanks; ++r)
+    if (r != h->rank) { h->ptrs.w[r] = nullptr; h->ptrs.upd[r] = nullptr; h->ptrs.rep[r] = nullptr; h->ptrs.flags[r] = nullptr; }
   return PS_OK;
 }
 

@@ -128,7 +128,13 @@ class ShardedServer:
         raise_for(rc, self.lib.ps_shard_last_error(self._h).decode())
 
     def close(self):
+        """Collective: unmap the peers' buffers, wait for every rank to have
+        done the same, then free this rank's own (ps_shard_disconnect)."""
         if self._h and self._h.value:
+            import torch.distributed as dist
+            self.lib.ps_shard_disconnect(self._h)
+            if dist.is_initialized():
+                dist.barrier()
             self.lib.ps_shard_destroy(self._h)
             self._h = ctypes.c_void_p()
 

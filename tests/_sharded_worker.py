@@ -22,13 +22,23 @@ def main(out_dir):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    # PS_SHARD_OVERSUBSCRIBE=1: more ranks than GPUs (ranks share GPUs round-
+    # robin, host plumbing over gloo) -- exercises G = 8 on a 4-GPU box
+    if os.environ.get("PS_SHARD_OVERSUBSCRIBE") == "1":
+        local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     verdict = {"rank": rank, "checks": []}
     runs = [r for r in oracle.load_golden("sim_corpus.json.gz")["runs"]
             if r["config"].get("timing_preset") == "homogeneous"
             and r["normalized"]["worker_count"] == world]
-    for d in (5, 100_003):
+    only = os.environ.get("PS_TEST_ONLY_RUN")  # diagnosis: one run, one size
+    if only:
+        runs = [r for r in runs if r["name"] == only]
+    for d in ((100_003,) if only else (5, 100_003)):
         for run in runs:
             cfg = ps.validate_config(ps.make_config(**run["config"]))
             rows = [line.split("\t") for line in run["trace"].splitlines()]
@@ -56,6 +66,13 @@ def main(out_dir):
             ok_rep = bool(np.array_equal(rep.view(np.uint32), w.view(np.uint32)))
             st = srv.state()
             diff = [(a, b) for a, b in zip(got, want) if a != b][:3]
+            if not ok_rep:
+                bad = np.nonzero(rep.view(np.uint32) != w.view(np.uint32))[0]
+                diff = {"replica_mismatches": int(bad.size), "first": int(bad[0]), "last": int(bad[-1]),
+                        "lo_hi": [srv.lo, srv.hi],
+                        "got": float(rep[bad[0]]), "want": float(w[bad[0]]),
+                        "w0": float(w0[bad[0]]),
+                        "stale_equals_w0": bool(np.all(rep[bad] == w0[bad].astype(np.float32)))}
             verdict["checks"].append({"run": run["name"], "d": d, "trace": ok_trace,
                                       "diff": diff, "n_got": len(got), "n_want": len(want),
                                       "shard": ok_shard, "replica": ok_rep,
@@ -83,8 +100,13 @@ def main(out_dir):
             if p != 1:
                 w = oracle.apply_f32(w, oracle.synthetic_update(1, p, 0, d), 0.05)
     st = srv.state()
+    rep = srv.read_replica()
+    bad = np.nonzero(rep.view(np.uint32) != w.view(np.uint32))[0]
     verdict["checks"].append({
         "run": "reject", "d": d, "trace": True,
+        "diff": {} if bad.size == 0 else {"replica_mismatches": int(bad.size), "first": int(bad[0]),
+                                          "last": int(bad[-1]), "lo_hi": [srv.lo, srv.hi],
+                                          "stale_equals_w0": bool(np.all(rep[bad] == w0[bad].astype(np.float32)))},
         "shard": bool(np.array_equal(srv.read_shard().view(np.uint32), w[srv.lo:srv.hi].view(np.uint32))),
         "replica": bool(np.array_equal(srv.read_replica().view(np.uint32), w.view(np.uint32))),
         "version": int(st.version) + int(st.rejected), "steps": 2,

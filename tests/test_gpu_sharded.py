@@ -33,6 +33,10 @@ def test_sharded_parity(tmp_path, world, gmax):
            str(tmp_path)]
     env = dict(os.environ, PS_SHARD_GMAX=str(gmax))
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    _check_verdicts(tmp_path, res, world)
+
+
+def _check_verdicts(tmp_path, res, world):
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     files = sorted(glob.glob(str(tmp_path / "rank*.json")))
     assert len(files) == world
@@ -40,7 +44,7 @@ def test_sharded_parity(tmp_path, world, gmax):
         v = json.load(open(f))
         assert v["checks"], v
         for c in v["checks"]:
-            assert c["trace"] and c["shard"] and c["replica"], c
+            assert c["trace"] and c["shard"] and c["replica"], json.dumps(c)
             assert c["version"] == c["steps"] * world
 
 
@@ -61,3 +65,17 @@ def test_torch_workers_on_the_sharded_server(tmp_path, world):
         for c in json.load(open(f)):
             assert c["ok"], c
             assert c["version"] == 6 * world, c
+
+
+def test_sharded_parity_eight_ranks_on_four_gpus(tmp_path):
+    """G = 8 (the driver's scaling run) on a 4-GPU box: two ranks per GPU,
+    host plumbing over gloo. Every rank runs k_shard_run<8> with seven peers:
+    reference traces, shards, replicas, rejection and divergence as above."""
+    if _gpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=8", "--master-addr", "127.0.0.1", "--master-port", "29488",
+           os.path.join(ROOT, "tests", "_sharded_worker.py"), str(tmp_path)]
+    env = dict(os.environ, PS_SHARD_OVERSUBSCRIBE="1", PS_SHARD_CTAS_PER_SM="1")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    _check_verdicts(tmp_path, res, 8)
