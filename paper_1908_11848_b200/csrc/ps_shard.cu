@@ -273,7 +273,6 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
           wdst[j] = x;
           for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
         }
-      __threadfence_system();  // every warp's replica stores before F(t) (see below)
       redo_bad = __syncthreads_or(redo_bad);
       redo_n += 1;
       if (threadIdx.x == 0) {
@@ -391,14 +390,14 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     gbad = __reduce_or_sync(kFull, gbad);
     dbad = __reduce_or_sync(kFull, dbad);
     if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
-    // every warp's stores to peers must have landed before any peer can see
-    // V(t). The fence is issued by every warp that stored: measured, a fence
-    // in one thread after the barrier (or one fence in the election winner)
-    // let a peer read the tail of a slice stale after V(t).
-    __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
       if (s_bits) atomicOr(&ctl->bad, s_bits);
+      // this CTA's stores (local and to peers; the barrier orders every warp's
+      // before this thread) are released at GPU scope; the winner acquires
+      // them all and its fence.sc.sys orders them before V(t) at system scope
+      // (causality order is transitive across scopes) -- one system fence
+      // per step instead of one per warp
       const unsigned long long prev = atom_add_acq_rel_gpu_u64(&ctl->arrive_total, 1ull);
       SPROF(if (blockIdx.x == 0) g_prof[1] += globaltimer_ns() - g_t_resolved);
       if (prev == t * (unsigned long long)ndata - 1) {
