@@ -190,16 +190,31 @@ __global__ void k_decide(Ctrl* ctrl, int worker, double now, Ctrl* mirror) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_copy_out(const float* __restrict__ src, T* __restrict__ dst,
                                                   long long n) {
+  // kApplyUnroll float4 per thread per trip, all loads issued before the
+  // stores: enough bytes in flight per SM to cover HBM latency
+  constexpr int U = kApplyUnroll;
   const long long nv = n >> 2;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += stride) {
-    const float4 v = reinterpret_cast<const float4*>(src)[j];
-    if constexpr (sizeof(T) == 4) {
-      reinterpret_cast<float4*>(dst)[j] = v;
-    } else {
-      double2* o = reinterpret_cast<double2*>(dst) + 2 * j;
-      o[0] = make_double2(v.x, v.y);
-      o[1] = make_double2(v.z, v.w);
+  const long long stride = (long long)gridDim.x * blockDim.x * U;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  for (long long base = (long long)blockIdx.x * blockDim.x * U + threadIdx.x; base < nv; base += stride) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = base + (long long)u * blockDim.x;
+      if (j < nv) v[u] = ld_stream(s4 + j);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = base + (long long)u * blockDim.x;
+      if (j < nv) {
+        if constexpr (sizeof(T) == 4) {
+          reinterpret_cast<float4*>(dst)[j] = v[u];
+        } else {
+          double2* o = reinterpret_cast<double2*>(dst) + 2 * j;
+          o[0] = make_double2(v[u].x, v[u].y);
+          o[1] = make_double2(v[u].z, v[u].w);
+        }
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
