@@ -543,14 +543,18 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
   // later server's replica mapped through a stale block of an earlier one).
   auto ipc_bytes = [](size_t b) { return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1); };
   if ((e = cudaMalloc(&h->w, ipc_bytes(shard_bytes))) || (e = cudaMalloc(&h->w_alt, shard_bytes))) return bail("shard");
-  if ((e = cudaMemset(h->w, 0, shard_bytes)) || (e = cudaMemset(h->w_alt, 0, shard_bytes)))
+  // every initialization is ordered on the server's own (non-blocking)
+  // stream: a plain cudaMemset runs on the legacy stream, which does not
+  // order against it -- measured, a late memset zeroed part of a shard after
+  // its w0 load
+  if ((e = cudaMemsetAsync(h->w, 0, shard_bytes, h->stream)) || (e = cudaMemsetAsync(h->w_alt, 0, shard_bytes, h->stream)))
     return bail("shard memset");
   if ((e = cudaMalloc(&h->upd, ipc_bytes(h->dpad * sizeof(float))))) return bail("update buffer");
-  if ((e = cudaMemset(h->upd, 0, h->dpad * sizeof(float)))) return bail("update memset");
+  if ((e = cudaMemsetAsync(h->upd, 0, h->dpad * sizeof(float), h->stream))) return bail("update memset");
   if ((e = cudaMalloc(&h->rep, ipc_bytes(h->dpad * sizeof(float))))) return bail("replica");
-  if ((e = cudaMemset(h->rep, 0, h->dpad * sizeof(float)))) return bail("replica memset");
+  if ((e = cudaMemsetAsync(h->rep, 0, h->dpad * sizeof(float), h->stream))) return bail("replica memset");
   if ((e = cudaMalloc(&h->flags, ipc_bytes(3 * kMaxRanks * sizeof(unsigned long long))))) return bail("flags");
-  if ((e = cudaMemset(h->flags, 0, 3 * kMaxRanks * sizeof(unsigned long long)))) return bail("flags memset");
+  if ((e = cudaMemsetAsync(h->flags, 0, 3 * kMaxRanks * sizeof(unsigned long long), h->stream))) return bail("flags memset");
   if ((e = cudaMalloc(&h->ctl, sizeof(ShardCtl)))) return bail("ctl");
   if ((e = cudaMallocHost(&h->hctl, sizeof(ShardCtl)))) return bail("hctl");
   std::memset(h->hctl, 0, sizeof(ShardCtl));
@@ -572,7 +576,9 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
     void* tmp = nullptr;
     if (!on_dev) {
       if ((e = cudaMalloc(&tmp, h->d * esz + 16))) return bail("w0 staging");
-      if ((e = cudaMemcpy(tmp, src, h->d * esz, cudaMemcpyHostToDevice))) return bail("w0 upload");
+      // on the server's stream: a pageable cudaMemcpy may return before its
+      // DMA lands, and the legacy stream does not order against h->stream
+      if ((e = cudaMemcpyAsync(tmp, src, h->d * esz, cudaMemcpyHostToDevice, h->stream))) return bail("w0 upload");
       src = (const char*)tmp;
     }
     const char* mine = src + (size_t)h->lo * esz;
@@ -588,6 +594,7 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
     if ((e = cudaStreamSynchronize(h->stream))) return bail("w0 convert");
     if (tmp) cudaFree(tmp);
   }
+  if ((e = cudaStreamSynchronize(h->stream))) return bail("initialization");
   *out = h;
   return PS_OK;
 }

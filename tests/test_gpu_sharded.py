@@ -79,3 +79,18 @@ def test_sharded_parity_eight_ranks_on_four_gpus(tmp_path):
     env = dict(os.environ, PS_SHARD_OVERSUBSCRIBE="1", PS_SHARD_CTAS_PER_SM="1")
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     _check_verdicts(tmp_path, res, 8)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_many_short_lived_servers(world):
+    """60 create / run / verify / close cycles of varying sizes: every
+    replica bit-exact (guards the initialization ordering of ps_shard_create
+    and the collective shutdown)."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(29520 + world), os.path.join(ROOT, "tools", "shard_stress.py"), "60"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert f"stress: 60 servers x {world} ranks, 0 replica mismatches" in res.stdout, res.stdout[-3000:]
