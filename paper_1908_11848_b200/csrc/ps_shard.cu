@@ -729,8 +729,13 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   const int gsel = G > gmax_env ? G : gmax_env;
   const void* kern = gsel <= 2 ? (const void*)k_shard_run<2> : gsel <= 4 ? (const void*)k_shard_run<4>
                    : gsel <= 8 ? (const void*)k_shard_run<8> : (const void*)k_shard_run<16>;
-  int resident = 0;
-  SCK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kThreads, 0));
+  static int occupancy[4] = {-1, -1, -1, -1};  // per instantiation, queried once
+  const int oi = gsel <= 2 ? 0 : gsel <= 4 ? 1 : gsel <= 8 ? 2 : 3;
+  int resident = occupancy[oi];
+  if (resident < 0) {
+    SCK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kThreads, 0));
+    occupancy[oi] = resident;
+  }
   const int total = h->sm_count * (per_sm_env < resident ? per_sm_env : resident);
   const int data_ctas = total - 1;
   if (data_ctas < 1) return sfail(h, PS_E_CUDA, "k_shard_run cannot be resident");

@@ -1680,8 +1680,15 @@ int select_loop_kernel(ps_server* h, int P, int data_ctas, int* grid_out, const 
       {(const void*)k_sim<16, 2>, (const void*)k_sim<16, 4>, (const void*)k_sim<16, 8>, (const void*)k_sim<16, 32>, (const void*)k_sim<16, 0>},
       {(const void*)k_sim<0, 2>, (const void*)k_sim<0, 4>, (const void*)k_sim<0, 8>, (const void*)k_sim<0, 32>, (const void*)k_sim<0, 0>}};
   const void* kern = table[vi][pi];
-  int per_sm = 0;
-  PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimThreads, 0));
+  // the occupancy of each instantiation, queried once per process (it is a
+  // driver round trip on every run otherwise)
+  static int occupancy[6][5] = {{-1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1},
+                                {-1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1}};
+  int per_sm = occupancy[vi][pi];
+  if (per_sm < 0) {
+    PS_CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSimThreads, 0));
+    occupancy[vi][pi] = per_sm;
+  }
   if (grid > per_sm * h->sm_count) grid = per_sm * h->sm_count;
   if (grid < 2) return ps_fail(h, PS_E_CUDA, "k_sim cannot be resident");
   *grid_out = grid;

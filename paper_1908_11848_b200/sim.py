@@ -134,7 +134,7 @@ class DeviceSimulation:
             got = ctypes.c_int64(0)
             self.engine.check(lib.ps_sim_losses(self.engine.handle, vs, ls, m, ctypes.byref(got)))
             curve = [(int(vs[i]), float(ls[i])) for i in range(m)]
-        self.engine.refresh()
+        self.engine.refresh(sync=False)  # the run already mirrored the control block
         weights = self.engine.read()[0] if read_weights else None
         return DeviceRunReport(entries=entries, events=res.events, pushes=res.pushes,
                                applied=res.applied, rejected=res.rejected,
@@ -226,7 +226,7 @@ class DeviceReplay:
                 self.engine.handle, raw.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n,
                 ctypes.byref(got)))
             raw = raw[:n]
-        self.engine.refresh()
+        self.engine.refresh(sync=False)  # the run already mirrored the control block
         return ReplayReport(raw=raw, applied=res.applied, rejected=res.rejected,
                             pushes=res.pushes, device_ms=res.device_ms)
 
