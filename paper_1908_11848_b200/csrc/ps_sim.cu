@@ -1364,7 +1364,7 @@ template <int V>
 __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s_ring32, int warps_here) {
   static_assert(V > 0 && V <= 4, "register-resident slices of at most 4 float4 per lane");
   constexpr int KG = V == 1 ? 16 : V == 2 ? 8 : 2;  // calls per group
-  constexpr int L = 2;  // chunks executed before their verdict is read
+  constexpr int L = V <= 2 ? 3 : 2;  // chunks executed before their verdict is read
   constexpr int kRingChunks = kRing / 2;
   unsigned long long* s_ring = reinterpret_cast<unsigned long long*>(s_ring32);
   unsigned long long* gchunk = reinterpret_cast<unsigned long long*>(a.gword);
@@ -1422,8 +1422,8 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   // execute the live calls of a chunk with the rejected set `rej`; returns the
   // calls whose update (gb) / result (rb) holds a non-finite value in this slice
   auto exec = [&](const Chunk& c, unsigned live, unsigned rej, unsigned& gb, unsigned& rb) {
-    gb = 0;
-    rb = 0;
+    // per-lane bits, one warp reduction per chunk (not two votes per apply)
+    unsigned lgb = 0, lrb = 0;
     unsigned calls = (c.ma | c.mp) & live;
     while (calls) {
       int idx[KG];
@@ -1464,11 +1464,13 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
             wr[u] = apply4(wr[u], a.lr, g[k][u]);
             ra = acc_nonfinite(ra, wr[u]);
           }
-          if (__any_sync(kFull, ga != ga)) gb |= bit;
-          if (__any_sync(kFull, ra != ra)) rb |= bit;
+          if (ga != ga) lgb |= bit;
+          if (ra != ra) lrb |= bit;
         }
       }
     }
+    gb = __reduce_or_sync(kFull, lgb);
+    rb = __reduce_or_sync(kFull, lrb);
   };
   auto publish = [&](long long chunk, unsigned bits) {
     if (lane == 0) {
@@ -1574,6 +1576,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   // drain: every pending chunk final, oldest first
   if (!timed_out) {
     const long long newest = chunk - 1;
+    if constexpr (L >= 3) resolve(std::integral_constant<int, (L >= 3 ? 3 : 0)>{}, newest);
     resolve(std::integral_constant<int, 2>{}, newest);
     resolve(std::integral_constant<int, 1>{}, newest);
     resolve(std::integral_constant<int, 0>{}, newest);
