@@ -1422,8 +1422,8 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   // execute the live calls of a chunk with the rejected set `rej`; returns the
   // calls whose update (gb) / result (rb) holds a non-finite value in this slice
   auto exec = [&](const Chunk& c, unsigned live, unsigned rej, unsigned& gb, unsigned& rb) {
-    // per-lane bits, one warp reduction per chunk (not two votes per apply)
-    unsigned lgb = 0, lrb = 0;
+    // per-lane bits, one warp reduction per chunk (not a vote per apply)
+    unsigned lrb = 0;
     unsigned calls = (c.ma | c.mp) & live;
     while (calls) {
       int idx[KG];
@@ -1457,20 +1457,35 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
           }
         }
         if (c.ma & ~rej & bit) {
-          float ga = 0.f, ra = 0.f;
+          // only the result is checked here: a non-finite update always
+          // gives a non-finite result (lr > 0), and the rare non-finite
+          // result is classified below
+          float ra = 0.f;
 #pragma unroll
           for (int u = 0; u < V; ++u) {
-            ga = acc_nonfinite(ga, g[k][u]);
             wr[u] = apply4(wr[u], a.lr, g[k][u]);
             ra = acc_nonfinite(ra, wr[u]);
           }
-          if (ga != ga) lgb |= bit;
           if (ra != ra) lrb |= bit;
         }
       }
     }
-    gb = __reduce_or_sync(kFull, lgb);
     rb = __reduce_or_sync(kFull, lrb);
+    gb = 0;
+    // rare: which of the non-finite results come from a non-finite update
+    // (a rejection, server.py:65-67) rather than from the weights
+    for (unsigned m = rb; m; m &= m - 1) {
+      const int i = __ffs(m) - 1;
+      const int wb = __shfl_sync(kFull, c.wb, i);
+      float4 r[V];
+      load_slice<V>(r, reinterpret_cast<const float4*>(
+                           a.synth + ((long long)(wb >> 8) * nsyn + (wb & 255)) * a.dpad),
+                    lo, hi, lane);
+      float ga = 0.f;
+#pragma unroll
+      for (int u = 0; u < V; ++u) ga = acc_nonfinite(ga, r[u]);
+      if (__any_sync(kFull, ga != ga)) gb |= 1u << i;
+    }
   };
   auto publish = [&](long long chunk, unsigned bits) {
     if (lane == 0) {
