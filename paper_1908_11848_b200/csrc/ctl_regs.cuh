@@ -104,9 +104,8 @@ struct RegGate {
     for (int i = 0; i < PM; ++i)
       if (i == q) { previous[i] = latest[i]; latest[i] = t; populated[i] += 1; }
   }
-  __device__ __forceinline__ unsigned long long release_ready() {
+  __device__ __forceinline__ unsigned long long release_ready(int low) {
     if (!deferred) return 0ull;
-    const int low = min_clock();
     unsigned long long ready = 0ull;
 #pragma unroll
     for (int q = 0; q < PM; ++q)
@@ -116,61 +115,56 @@ struct RegGate {
   }
 
   // policy.py:152-206, warp-uniform (every lane holds the same tables).
+  // Every paradigm records the push in the history (policy.py:158-195; the
+  // controller records before it reads it), so the record is done once, up
+  // front, and the minimum clock once for the gap test and the release scan.
   __device__ __forceinline__ GateResult on_push(int p, double now) {
     GateResult r{PS_OK, 0, 0ull};
     if (p < 0 || p >= P || ((deferred >> p) & 1ull)) { r.status = PS_E_PROTOCOL; return r; }
     const int count = rget<PM>(clocks, p) + 1;
     rset<PM>(clocks, p, count);
     decisions += 1;
-    if (paradigm == PS_ASP) {
-      record(p, now);
-      return r;  // grant, no release scan
-    }
+    record(p, now);
+    if (paradigm == PS_ASP) return r;  // grant, no release scan
+    const int low = min_clock();
     int outcome;
     if (paradigm == PS_DSSP) {
       const int cred = rget<PM>(credits, p);
+      const int gap = count - low;
       if (cred > 0) {
         rset<PM>(credits, p, cred - 1);
-        record(p, now);
         outcome = 0;
+      } else if (gap <= s_lower) {
+        outcome = 0;
+      } else if (!(count >= max_clock())) {
+        outcome = 1;
       } else {
-        const int gap = count - min_clock();
-        if (gap <= s_lower) {
-          record(p, now);
-          outcome = 0;
-        } else if (!(count >= max_clock())) {
-          record(p, now);
-          outcome = 1;
-        } else {
-          record(p, now);  // the controller records first
-          int pred = 0;
-          if (r_max > 0) {
-            const int sl = slowest();
-            if (rget<PM>(populated, p) >= 2 && rget<PM>(populated, sl) >= 2) {
+        int pred = 0;
+        if (r_max > 0) {
+          const int sl = slowest();
+          if (rget<PM>(populated, p) >= 2 && rget<PM>(populated, sl) >= 2) {
 #ifdef PS_SIM_PROFILE
-              const long long tc = clock64();
+            const long long tc = clock64();
 #endif
-              pred = controller_grid(rget<PM>(latest, p), rget<PM>(previous, p), rget<PM>(latest, sl),
-                                     rget<PM>(previous, sl), r_max);
+            pred = controller_grid(rget<PM>(latest, p), rget<PM>(previous, p), rget<PM>(latest, sl),
+                                   rget<PM>(previous, sl), r_max);
 #ifdef PS_SIM_PROFILE
-              if ((threadIdx.x & 31) == 0) { g_ctl_calls += 1; g_ctl_cycles += clock64() - tc; }
+            if ((threadIdx.x & 31) == 0) { g_ctl_calls += 1; g_ctl_cycles += clock64() - tc; }
 #endif
-            }
           }
-          int headroom = s_lower + r_max - gap;
-          if (headroom < 0) headroom = 0;
-          const int c = pred < headroom ? pred : headroom;
-          rset<PM>(credits, p, c);
-          outcome = c > 0 ? 0 : 1;
         }
+        int headroom = s_lower + r_max - gap;
+        if (headroom < 0) headroom = 0;
+        const int c = pred < headroom ? pred : headroom;
+        rset<PM>(credits, p, c);
+        outcome = c > 0 ? 0 : 1;
       }
     } else {
-      record(p, now);
-      outcome = (count - min_clock() <= threshold) ? 0 : 1;
+      outcome = (count - low <= threshold) ? 0 : 1;
     }
     r.outcome = outcome;
     if (outcome == 1) deferred |= 1ull << p;
-    else r.released = release_ready();
+    else r.released = release_ready(low);
     return r;
   }
 };
