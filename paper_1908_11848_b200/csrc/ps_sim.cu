@@ -827,6 +827,16 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
       const unsigned hit = __ballot_sync(kFull, ((rng >> lane) & 1u) && ((dm >> (c.worker & 63)) & 1ull));
       if (hit) fail = __ffs(hit) - 1;
     };
+    // the chunk's decision words stay in registers (lane j holds the j-th)
+    // and leave in one coalesced store at the end of the chunk
+    unsigned long long dword = 0;
+    int nd = 0;
+    auto flush_decisions = [&]() {
+      if (lane < nd && n_dec + lane < a.trace_cap) a.decisions[n_dec + lane] = (long long)dword;
+      n_dec += nd;
+      pushes += nd;
+      nd = 0;
+    };
     // the next decide's (worker, now) is fetched while this one is decided
     int i = md ? __ffs(md) - 1 : -1;
     int w = __shfl_sync(kFull, c.worker, i & 31);
@@ -845,16 +855,15 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
 #ifdef PS_SIM_PROFILE
       c_gate += clock64() - tg;
 #endif
-      pushes += 1;
-      if (r.status != PS_OK) { status = r.status; fail = i; break; }
-      if (lane == 0 && n_dec < a.trace_cap)
-        a.decisions[n_dec] = (long long)((r.released << 8) | (unsigned)r.outcome);
-      n_dec += 1;
+      if (r.status != PS_OK) { pushes += 1; status = r.status; fail = i; break; }
+      if (lane == nd) dword = (r.released << 8) | (unsigned)r.outcome;
+      nd += 1;
       prev = i + 1;
       i = ni;
       w = nw;
       now = nnow;
     }
+    flush_decisions();
     if (fail < 0) check_pulls(prev, limit);
     if (fail < 0 && limit < m) fail = limit;
     if (fail >= 0) {
