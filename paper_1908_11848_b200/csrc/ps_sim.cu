@@ -1385,6 +1385,8 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   const long long lo = (long long)dw * per < a.nv ? (long long)dw * per : a.nv;
   const long long hi = lo + per < a.nv ? lo + per : a.nv;
   float4* W = reinterpret_cast<float4*>(a.W);
+  const float4* const synth4 = reinterpret_cast<const float4*>(a.synth);
+  float4* const rep4 = reinterpret_cast<float4*>(a.rep);
   float4 wr[V];
 #pragma unroll
   for (int u = 0; u < V; ++u) {
@@ -1396,7 +1398,10 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   long long applied = 0, rejected = 0;
   int diverged = -1;  // worker of the first non-finite result seen by this warp
   bool timed_out = false;
-  struct Chunk { int wb; unsigned ma, mp; };
+  // per call: (worker << 8 | buffer), and the float4 offset of its slice in
+  // the resident updates (apply) or the replicas (pull) -- 32 bits suffice for
+  // the slice widths this path serves (V <= 4)
+  struct Chunk { int wb; unsigned ma, mp, off; };
   auto load_raw = [&](long long base) {
     const long long i = base + lane;
     return i < n ? *reinterpret_cast<const int2*>(&a.calls[i].kind) : make_int2(-1, 0);
@@ -1416,6 +1421,8 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     if (isa) buf = ((worker < 32 ? s_lo : s_hi) + rank) % nsyn;
     if (isp) buf = (worker < 32 ? g_lo : g_hi) ^ ((rank + 1) & 1);
     c.wb = (okw ? worker : 0) << 8 | buf;
+    const unsigned dv4 = (unsigned)(a.dpad >> 2);
+    c.off = isa ? (unsigned)(worker * nsyn + buf) * dv4 : isp ? (unsigned)(worker * 2 + buf) * dv4 : 0u;
     for (int q = 0; q < P; ++q) {
       const int na = __popc(__ballot_sync(kFull, isa && worker == q));
       const int np = __popc(__ballot_sync(kFull, isp && worker == q));
@@ -1444,21 +1451,17 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
           const int i = __ffs(calls) - 1;
           calls &= calls - 1;
           idx[k] = i;
-          if (((c.ma & ~rej) >> i) & 1u) {
-            const int wb = __shfl_sync(kFull, c.wb, i);
-            load_slice<V>(g[k], reinterpret_cast<const float4*>(
-                                    a.synth + ((long long)(wb >> 8) * nsyn + (wb & 255)) * a.dpad),
-                          lo, hi, lane);
-          }
+          if (((c.ma & ~rej) >> i) & 1u)
+            load_slice<V>(g[k], synth4 + __shfl_sync(kFull, c.off, i), lo, hi, lane);
         }
       }
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
         const int i = idx[k];
         const unsigned bit = i >= 0 ? (1u << i) : 0u;
-        const int wb = __shfl_sync(kFull, c.wb, i & 31);
+        const unsigned off = __shfl_sync(kFull, c.off, i & 31);
         if (c.mp & bit) {
-          float4* dst = reinterpret_cast<float4*>(a.rep + ((long long)(wb >> 8) * 2 + (wb & 255)) * a.dpad);
+          float4* dst = rep4 + off;
 #pragma unroll
           for (int u = 0; u < V; ++u) {
             const long long j = lo + lane + 32ll * u;
@@ -1908,6 +1911,9 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   if (!synthetic || n_synthetic < 1) return ps_fail(h, PS_E_VALUE, "replay needs resident updates");
   // a decision word carries the released set in bits 8..63
   if (P > 55) return ps_fail(h, PS_E_VALUE, "replay supports at most 55 workers");
+  // the data warps address a slice by a 32-bit float4 offset
+  if ((unsigned long long)P * (unsigned long long)(n_synthetic > 2 ? n_synthetic : 2) * (unsigned long long)(h->dpad / 4) >= (1ull << 32))
+    return ps_fail(h, PS_E_VALUE, "resident updates beyond 2^32 float4 (64 GB)");
   ps_sim_buffers& b = h->sim;
   int rc;
   size_t cap;
