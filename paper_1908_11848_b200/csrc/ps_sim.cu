@@ -1443,25 +1443,26 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     unsigned calls = (c.ma | c.mp) & live;
     while (calls) {
       int idx[KG];
+      unsigned offk[KG];
       float4 g[KG][V];
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
         idx[k] = -1;
+        offk[k] = 0;
         if (calls) {
           const int i = __ffs(calls) - 1;
           calls &= calls - 1;
           idx[k] = i;
-          if (((c.ma & ~rej) >> i) & 1u)
-            load_slice<V>(g[k], synth4 + __shfl_sync(kFull, c.off, i), lo, hi, lane);
+          offk[k] = __shfl_sync(kFull, c.off, i);
+          if (((c.ma & ~rej) >> i) & 1u) load_slice<V>(g[k], synth4 + offk[k], lo, hi, lane);
         }
       }
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
         const int i = idx[k];
         const unsigned bit = i >= 0 ? (1u << i) : 0u;
-        const unsigned off = __shfl_sync(kFull, c.off, i & 31);
         if (c.mp & bit) {
-          float4* dst = rep4 + off;
+          float4* dst = rep4 + offk[k];
 #pragma unroll
           for (int u = 0; u < V; ++u) {
             const long long j = lo + lane + 32ll * u;
