@@ -470,7 +470,7 @@ def e2e_drop_in(torch, ps, cfg, calls, synth_host, d):
     return updates / dt, h2d, d2h, updates
 
 
-def e2e_batched(torch, ps, calls, synth_host, d, w0, steps=10):
+def e2e_batched(torch, ps, calls, synth_host, d, w0, steps=30):
     """The same request stream through the engine's batch C-ABI call
     (ps_replay_run via DeviceReplay) with HOST buffers: every step copies its
     inputs -- the call stream and the resident updates -- from host memory and
