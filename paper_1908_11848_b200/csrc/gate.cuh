@@ -47,6 +47,20 @@ __device__ __forceinline__ int controller_grid(double lp, double pp, double ls, 
   // nearest is monotone), so |slow(k) - cand| is minimized at the last k with
   // slow(k) <= cand or the one after it: a binary search finds that pair and
   // the per-r minimum equals the brute-force min over all k bit for bit.
+  if (r_max <= 16) {
+    // small grids: the reference's brute force, literally -- r_max+1
+    // independent evaluations per lane pipeline better than the search's
+    // dependent steps (policy.py:127-132)
+    if (lane <= r_max) {
+      const double cand = __dadd_rn(lp, __dmul_rn((double)lane, ip));
+      double m = __longlong_as_double(0x7ff0000000000000ll);
+      double kf = 1.0;  // k + 1, exact
+      for (int k = 0; k <= r_max; ++k, kf += 1.0)
+        m = fmin(m, fabs(__dsub_rn(__dadd_rn(ls, __dmul_rn(kf, is)), cand)));
+      best = m;
+      best_r = lane;
+    }
+  } else
   for (int r = lane; r <= r_max; r += 32) {
     const double cand = __dadd_rn(lp, __dmul_rn((double)r, ip));
     int lo = -1, hi = r_max + 1;  // slow(lo) <= cand < slow(hi), virtual ends
