@@ -243,6 +243,16 @@ void ps_shard_destroy(ps_shard_server* h);
 const char* ps_shard_last_error(const ps_shard_server* h);
 int ps_shard_ipc_handles(ps_shard_server* h, void* out, int64_t cap); /* returns blob size */
 int ps_shard_connect(ps_shard_server* h, const void* blobs, int64_t len);
+/* Any push groups (heterogeneous schedules): row i of `groups`, with
+ * PS_SHARD_GROUP_STRIDE int32 per row, is {n pushers, pull mask, ticket
+ * order[n]} of step i -- the workers that push at that instant in the order
+ * the reference's event loop serves them (simnet.py:167-201), and the workers
+ * whose pull arrives before the next group (their replica receives the
+ * weights after this group). ps_shard_run is the homogeneous special case
+ * (every worker pushes and pulls every step). */
+#define PS_SHARD_GROUP_STRIDE 18
+int ps_shard_run_groups(ps_shard_server* h, int64_t t0, int32_t steps, const double* now,
+                        const int32_t* groups, void* dst, double* ms);
 /* The worker's update buffer (device, fp32, padded_len >= d): push source. */
 int ps_shard_update_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len);
 /* The worker's replica (device, fp32): starts as w0 and is rewritten by every

@@ -114,6 +114,7 @@ SIGNATURES = {
     "ps_shard_update_buffer": (ctypes.c_int, [_P, ctypes.POINTER(_P), _PI64]),
     "ps_shard_replica_buffer": (ctypes.c_int, [_P, ctypes.POINTER(_P), _PI64]),
     "ps_shard_run": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _PD]),
+    "ps_shard_run_groups": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _PD]),
     "ps_shard_read_shard": (ctypes.c_int, [_P, _P, _PI64]),
     "ps_shard_read_replica": (ctypes.c_int, [_P, _P]),
     "ps_shard_get_state": (ctypes.c_int, [_P, ctypes.POINTER(PSGateState)]),

@@ -50,6 +50,7 @@ using namespace dssp;
 namespace {
 
 constexpr int kMaxRanks = 16;
+constexpr int kSchedStride = 2 + kMaxRanks;  // ps_shard_run_groups row: n, pull mask, order
 constexpr int kThreads = 256;
 constexpr unsigned long long kTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
@@ -125,8 +126,12 @@ template <int G_MAX>
 __global__ void __launch_bounds__(kThreads)
 k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, ShardPtrs P, int G,
             int me, unsigned long long t0, int steps, float lr, ShardCtl* ctl, const double* now,
-            ps_trace_row* trace, long long trace_cap) {
+            ps_trace_row* trace, long long trace_cap, const int* sched) {
   const int ndata = gridDim.x - 1;
+  // sched (optional): per step {pushers n, pull mask, ticket order[kMaxRanks]}
+  // -- any push group and any set of pulling workers (heterogeneous
+  // schedules); without it every worker pushes and pulls every step and the
+  // ticket order follows the gate's previous grants (homogeneous schedule)
   // ---- the gate CTA: the replicated decisions, one group per step --------
   // They depend only on (worker, now) and the gate tables, never on the data,
   // so this CTA runs them from shared memory while the data CTAs stream.
@@ -143,7 +148,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     for (int i = 0; i < steps && status == PS_OK; ++i) {
       const unsigned long long t = t0 + i;
       const int co = (int)(t & 1);
-      if (threadIdx.x == 0) {
+      if (threadIdx.x == 0 && !sched) {
         // order[co ^ 1] is read by every data CTA at the start of step t-1
         // (into shared memory); all of them have once they arrived there
         const unsigned long long s0 = globaltimer_ns();
@@ -159,8 +164,10 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       int next[kMaxRanks];
       int n_next = 0;
       SPROF(const unsigned long long tg0 = globaltimer_ns());
-      for (int k = 0; k < G; ++k) {
-        const int p = ctl->order[co][k];
+      const int* row = sched ? sched + (long long)i * kSchedStride : nullptr;
+      const int n_push = row ? row[0] : G;
+      for (int k = 0; k < n_push; ++k) {
+        const int p = row ? row[2 + k] : ctl->order[co][k];
         const GateResult r = gate_on_push(&sg, p, now[i]);
         if (threadIdx.x == 0) {
           if (r.status != PS_OK) status = r.status;
@@ -186,9 +193,10 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       }
       if (threadIdx.x == 0) {
         // every worker must be back for the next group (homogeneous schedule)
-        if (status == PS_OK && n_next != G) status = PS_E_PROTOCOL;
+        if (!sched && status == PS_OK && n_next != G) status = PS_E_PROTOCOL;
         if (status != PS_OK) atomicCAS(&ctl->status, PS_OK, status);
-        for (int k = 0; k < n_next && k < G; ++k) ctl->order[co ^ 1][k] = next[k];
+        if (!sched)
+          for (int k = 0; k < n_next && k < G; ++k) ctl->order[co ^ 1][k] = next[k];
         st_release_u64(&ctl->gate_done, t);
         SPROF(g_prof[4] += globaltimer_ns() - tg0);
       }
@@ -221,6 +229,8 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
   __shared__ int s_last, s_stop, s_div;
   __shared__ unsigned long long s_rej;
   __shared__ int s_order[2][kMaxRanks];
+  __shared__ int s_n[2];           // pushers of the step in this slot
+  __shared__ unsigned s_pull[2];   // workers whose replica the step writes
   const long long nv = (n_local + 3) >> 2;
   const long long lo = P.lo[me];
   constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
@@ -265,13 +275,14 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
           const long long j = base + (long long)u * kThreads;
           if (j >= nv) break;
           float4 x = wsrc[j];
-          for (int i = 0; i < G; ++i) {
+          for (int i = 0; i < s_n[co]; ++i) {
             const int p = s_order[co][i];
             if (!((rej >> p) & 1ull)) x = apply4(x, lr, reinterpret_cast<const float4*>(P.upd[p] + lo)[j]);
           }
           redo_bad |= nonfinite4(x) ? 1u : 0u;
           wdst[j] = x;
-          for (int q = 0; q < G; ++q) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
+          for (int q = 0; q < G; ++q)
+            if ((s_pull[co] >> q) & 1u) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x;
         }
       redo_bad = __syncthreads_or(redo_bad);
       redo_n += 1;
@@ -306,7 +317,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     cur ^= 1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       ctl->cur = cur;
-      ctl->gate.version += G - __popcll(rej);
+      ctl->gate.version += s_n[co] - __popcll(rej);
       ctl->gate.rejected += __popcll(rej);
     }
     return true;
@@ -328,25 +339,38 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         ok = wait_flags(P.flags[me], G, t, nullptr, ctl);
       }
       // this group's ticket order is final once the gate finished step t-1
+      // (with a schedule it is given)
       const unsigned long long s0 = globaltimer_ns();
       SPROF(const unsigned long long tw0 = globaltimer_ns());
-      while (ok && ld_acquire_u64(&ctl->gate_done) + 1 < t) {
+      while (ok && !sched && ld_acquire_u64(&ctl->gate_done) + 1 < t) {
         if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); ok = false; }
         __nanosleep(32);
       }
       SPROF(if (blockIdx.x == 0) g_prof[5] += globaltimer_ns() - tw0);
-      if (ok)
-        for (int i = 0; i < G; ++i) s_order[co][i] = ctl->order[co][i];
+      if (ok) {
+        if (sched) {
+          const int* row = sched + (long long)step * kSchedStride;
+          s_n[co] = row[0];
+          s_pull[co] = (unsigned)row[1];
+          for (int i = 0; i < row[0]; ++i) s_order[co][i] = row[2 + i];
+        } else {
+          s_n[co] = G;
+          s_pull[co] = G >= 32 ? 0xffffffffu : ((1u << G) - 1u);
+          for (int i = 0; i < G; ++i) s_order[co][i] = ctl->order[co][i];
+        }
+      }
       s_stop = !ok;
     }
     __syncthreads();
     if (s_stop) return;  // watchdog fired
     const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
     float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
+    const int n_push = s_n[co];
+    const unsigned pullm = s_pull[co];
     const float4* src[G_MAX];
 #pragma unroll
     for (int i = 0; i < G_MAX; ++i)
-      src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? s_order[co][i] : 0] + lo);
+      src[i] = reinterpret_cast<const float4*>(P.upd[i < n_push ? s_order[co][i] : 0] + lo);
     unsigned dbad = 0;
     unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
     // Optimistic single pass: apply all G updates in ticket order into the
@@ -363,7 +387,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         if (j < nv) {
 #pragma unroll
           for (int i = 0; i < G_MAX; ++i)
-            if (i < G) g[u][i] = ld_stream(src[i] + j);
+            if (i < n_push) g[u][i] = ld_stream(src[i] + j);
           x[u] = wsrc[j];
         }
       }
@@ -373,7 +397,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         if (j < nv) {
 #pragma unroll
           for (int i = 0; i < G_MAX; ++i)
-            if (i < G) {
+            if (i < n_push) {
               gbad |= nonfinite4(g[u][i]) ? (1u << i) : 0u;
               x[u] = apply4(x[u], lr, g[u][i]);
             }
@@ -383,7 +407,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
           // stored straight into each replica, G-1 of them over NVLink
 #pragma unroll
           for (int q = 0; q < G_MAX; ++q)
-            if (q < G) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x[u];
+            if (q < G && ((pullm >> q) & 1u)) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x[u];
         }
       }
     }
@@ -405,7 +429,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         // last data CTA of the step: V(t) to every rank
         const unsigned b = atomicExch(&ctl->bad, 0u);
         unsigned long long v = (t << 32) | ((unsigned long long)(b >> 31) << 31);
-        for (int i = 0; i < G; ++i)
+        for (int i = 0; i < s_n[co]; ++i)
           if ((b >> i) & 1u) v |= 1ull << s_order[co][i];
         __threadfence_system();
         for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + G + me, v);
@@ -439,6 +463,8 @@ __global__ void k_shard_load(const T* src, float* dst, long long n) {
 
 struct ps_shard_server {
   ps_config cfg{};
+  int* sched_dev = nullptr;  // ps_shard_run_groups: device copy of the groups
+  size_t sched_cap = 0;
   int world = 1, rank = 0, dev = 0, sm_count = 148;
   cudaStream_t stream = nullptr;
   long long d = 0, S = 0, lo = 0, hi = 0, n_local = 0, dpad = 0;
@@ -622,6 +648,7 @@ void ps_shard_destroy(ps_shard_server* h) {
   for (void* p : h->opened) cudaIpcCloseMemHandle(p);
   cudaFree(h->w); cudaFree(h->w_alt); cudaFree(h->now_dev); cudaFree(h->upd); cudaFree(h->rep); cudaFree(h->flags); cudaFree(h->ctl);
   cudaFree(h->trace);
+  cudaFree(h->sched_dev);
   if (h->hctl) cudaFreeHost(h->hctl);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -698,8 +725,38 @@ int ps_shard_replica_buffer(ps_shard_server* h, void** ptr, int64_t* padded_len)
 // its slice of the new weights straight into each worker's (engine-owned)
 // replica; dst (device, fp32, may be NULL) additionally receives a copy of
 // this rank's replica after the last step.
+namespace {
+int shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, const int32_t* groups,
+              void* dst, double* ms);
+}  // namespace
+
 int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, void* dst,
                  double* ms) {
+  return shard_run(h, t0, steps, now, nullptr, dst, ms);
+}
+
+// Any push groups: row i of `groups` (PS_SHARD_GROUP_STRIDE int32 each) is
+// {n pushers, pull mask, ticket order[n]} of step i.
+int ps_shard_run_groups(ps_shard_server* h, int64_t t0, int32_t steps, const double* now,
+                        const int32_t* groups, void* dst, double* ms) {
+  if (steps >= 1 && !groups) return sfail(h, PS_E_VALUE, "groups missing");
+  for (int i = 0; i < steps; ++i) {
+    const int32_t* row = groups + (long long)i * kSchedStride;
+    if (row[0] < 0 || row[0] > h->world) return sfail(h, PS_E_VALUE, "group size out of range");
+    if (h->world < 32 && ((unsigned)row[1] >> h->world)) return sfail(h, PS_E_VALUE, "pull mask names an unknown worker");
+    unsigned seen = 0;
+    for (int k = 0; k < row[0]; ++k) {
+      const int p = row[2 + k];
+      if (p < 0 || p >= h->world || ((seen >> p) & 1u)) return sfail(h, PS_E_VALUE, "bad ticket order");
+      seen |= 1u << p;
+    }
+  }
+  return shard_run(h, t0, steps, now, groups, dst, ms);
+}
+
+namespace {
+int shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, const int32_t* groups,
+              void* dst, double* ms) {
   Dev guard(h->dev);
   if (steps < 1) return PS_OK;
   const long long need = (long long)(t0 + steps) * h->world + 8;
@@ -746,6 +803,18 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
     h->now_cap = steps;
   }
   SCK(h, cudaMemcpyAsync(h->now_dev, now, steps * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  const int* schedp = nullptr;
+  if (groups) {
+    const size_t need_ints = (size_t)steps * kSchedStride;
+    if (h->sched_cap < need_ints) {
+      cudaFree(h->sched_dev);
+      h->sched_dev = nullptr;
+      SCK(h, cudaMalloc(&h->sched_dev, need_ints * sizeof(int)));
+      h->sched_cap = need_ints;
+    }
+    SCK(h, cudaMemcpyAsync(h->sched_dev, groups, need_ints * sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    schedp = h->sched_dev;
+  }
   // election counter and step marks continue from ticket t0 - 1
   const unsigned long long marks[4] = {(unsigned long long)(t0 - 1) * (unsigned long long)data_ctas,
                                        (unsigned long long)(t0 - 1), (unsigned long long)(t0 - 1), 0ull};
@@ -761,7 +830,7 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   unsigned long long t0v = (unsigned long long)t0;
   float lrv = lr;
   const double* nowp = h->now_dev;
-  void* args[] = {&w0p, &w1p, &nl, &ptrs, &Gv, &mev, &t0v, &nsteps, &lrv, &ctl, &nowp, &trace, &tcap};
+  void* args[] = {&w0p, &w1p, &nl, &ptrs, &Gv, &mev, &t0v, &nsteps, &lrv, &ctl, &nowp, &trace, &tcap, &schedp};
   SCK(h, cudaEventRecord(h->ev0, h->stream));
   SCK(h, cudaLaunchCooperativeKernel(kern, dim3(total), dim3(kThreads), args, 0, h->stream));
   if (h->profile) SCK(h, cudaEventRecord(h->pev[0], h->stream));
@@ -786,6 +855,8 @@ int ps_shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* no
   if (st == PS_E_PROTOCOL) return sfail(h, PS_E_PROTOCOL, "protocol violation in the replicated gate");
   return PS_OK;
 }
+
+}  // namespace
 
 // Profiling: bracket each of the three kernels with events (serializes the
 // host with every step, so only for diagnosis, never for the timed numbers).

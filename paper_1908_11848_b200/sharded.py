@@ -53,6 +53,31 @@ def homogeneous_push_times(compute_base, comm_delay, steps):
     return out
 
 
+GROUP_STRIDE = 18  # PS_SHARD_GROUP_STRIDE (include/dssp_ps.h)
+
+
+def groups_from_trace(entries):
+    """The push groups of a trace (simnet.py:167-201): consecutive
+    push_arrive rows at one instant form a group, served in row order; every
+    pull_arrive row belongs to the group before it (the weights it snapshots
+    are the ones after that group). Pulls before the first group see w0.
+    Returns [(time, [workers], [pulling workers])]."""
+    groups = []
+    open_time = None
+    for e in entries:
+        if e.kind == "push_arrive":
+            if open_time is not None and e.time == open_time and groups:
+                groups[-1][1].append(e.worker)
+            else:
+                groups.append((e.time, [e.worker], []))
+                open_time = e.time
+        else:
+            if e.kind == "pull_arrive" and groups:
+                groups[-1][2].append(e.worker)
+            open_time = None if e.kind != "push_arrive" else open_time
+    return groups
+
+
 def exchange_blobs(mine: bytes):
     """All-gather every rank's IPC blob, ordered by rank (host plumbing)."""
     import torch.distributed as dist
@@ -152,6 +177,27 @@ class ShardedServer:
                                    dst.data_ptr() if dst is not None else None, ctypes.byref(ms))
         self._check(rc)
         self.ticket += len(now)
+        return ms.value
+
+    def run_groups(self, groups, dst=None):
+        """Heterogeneous schedules: ``groups`` is a list of (time, ticket order,
+        pulling workers) -- the workers that push at that instant in the order
+        the reference serves them, and the workers whose pull arrives before
+        the next group (see groups_from_trace). Returns the device time in ms."""
+        import torch
+        torch.cuda.current_stream(self.device).synchronize()
+        n = len(groups)
+        now = np.ascontiguousarray([float(g[0]) for g in groups], dtype=np.float64)
+        rows = np.zeros((max(n, 1), GROUP_STRIDE), dtype=np.int32)
+        for i, (_, order, pulls) in enumerate(groups):
+            rows[i, 0] = len(order)
+            rows[i, 1] = int(sum(1 << int(q) for q in set(pulls)))
+            rows[i, 2:2 + len(order)] = order
+        ms = ctypes.c_double(0)
+        rc = self.lib.ps_shard_run_groups(self._h, self.ticket, n, now.ctypes.data, rows.ctypes.data,
+                                          dst.data_ptr() if dst is not None else None, ctypes.byref(ms))
+        self._check(rc)
+        self.ticket += n
         return ms.value
 
     def read_shard(self):

@@ -94,3 +94,28 @@ def test_many_short_lived_servers(world):
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert f"stress: 60 servers x {world} ranks, 0 replica mismatches" in res.stdout, res.stdout[-3000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_heterogeneous_schedules_on_the_sharded_server(tmp_path, world):
+    """Reference runs with stragglers, mixed speeds and jitter: any push group
+    and any set of pulling workers per step (ps_shard_run_groups). Decisions
+    byte-identical to the reference, every shard the fp32 replay, every
+    replica the weights after the group of that worker's last pull."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(29560 + world), os.path.join(ROOT, "tests", "_sharded_groups_worker.py"),
+           str(tmp_path)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    files = sorted(glob.glob(str(tmp_path / "groups_rank*.json")))
+    assert len(files) == world
+    n = 0
+    for f in files:
+        for c in json.load(open(f)):
+            assert c["trace"] and c["shard"] and c["replica"], json.dumps(c)
+            assert c["version"] == c["pushes"], c
+            n += 1
+    assert n > 0
