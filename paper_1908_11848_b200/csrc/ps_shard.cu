@@ -761,10 +761,17 @@ int shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, 
   if (steps < 1) return PS_OK;
   const long long need = (long long)(t0 + steps) * h->world + 8;
   if (need > h->trace_cap) {
-    cudaFree(h->trace);
-    h->trace = nullptr;
+    // grow, keeping the rows of earlier runs (the trace is cumulative)
     const long long cap = need * 2;
-    SCK(h, cudaMalloc(&h->trace, cap * sizeof(ps_trace_row)));
+    ps_trace_row* grown = nullptr;
+    SCK(h, cudaMalloc(&grown, cap * sizeof(ps_trace_row)));
+    if (h->trace) {
+      SCK(h, cudaMemcpyAsync(grown, h->trace, h->trace_cap * sizeof(ps_trace_row), cudaMemcpyDeviceToDevice,
+                             h->stream));
+      SCK(h, cudaStreamSynchronize(h->stream));
+      cudaFree(h->trace);
+    }
+    h->trace = grown;
     h->trace_cap = cap;
   }
   const int G = h->world, me = h->rank;

@@ -282,6 +282,52 @@ def bandwidth_sweep(world, rank, local, warm, steps):
     return rows
 
 
+C4_DIM = 1_730_714  # ResNet-110 (CIFAR)
+
+
+def throttled_bench(world, rank, local):
+    """configs[3] across GPUs: one worker per GPU, throttled 1x / 2x / 4x
+    (cycling), ResNet-110-sized server. The push groups come from the
+    simulator's schedule for that cluster (the device run loop on a small
+    vector -- every rank derives the same groups); the sharded server then
+    serves them with its replicated gate: DSSP vs SSP vs BSP vs ASP, updates/s
+    and the fast worker's waiting (virtual time)."""
+    import torch
+    import torch.distributed as dist
+    from .metrics import per_worker, staleness_histogram
+    from .sim import DeviceSimulation
+
+    throttle = tuple((1, 2, 4)[q % 3] for q in range(world))
+    out = {}
+    for name, s, r in PARADIGMS:
+        cfg = validate_config(make_config(
+            paradigm=name, worker_count=world, s_lower=s, r_max=r, timing_preset="homogeneous",
+            compute_base=1.0, comm_delay=0.05, throttle=throttle, model_kind="quadratic_bowl",
+            dimension=C4_DIM, dataset_size=world * 400, batch_size=16, learning_rate=0.05,
+            epochs=1, seed=0))
+        sched = DeviceSimulation(cfg, dimension=64, device=local).run(loss_every=0, read_weights=False)
+        groups = groups_from_trace(sched.entries)
+        srv = ShardedServer(cfg, C4_DIM, rank, world, local)
+        srv.update[:C4_DIM].normal_()
+        srv.run_groups(groups[:8])  # warm-up
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(srv.run_groups(groups[8:]))
+        pushes = sum(len(g[1]) for g in groups[8:])
+        trace = srv.trace()
+        ok = [e.decision for e in trace] == [e.decision for e in sched.entries if e.kind == "push_arrive"]
+        pw = per_worker(sched.entries)
+        hist = staleness_histogram(sched.entries)
+        out[name] = {"updates_per_s": pushes / (ms * 1e-3), "groups": len(groups) - 8,
+                     "updates": pushes, "decisions_match_single_gpu_engine": ok,
+                     "fast_worker_wait_s": pw[0].wait_s, "max_staleness": max(hist) if hist else 0,
+                     "throttle": list(throttle)}
+        torch.cuda.synchronize()
+        dist.barrier()
+        srv.close()
+    return out
+
+
 def torch_workers_bench(world, rank, local, warm, steps, batch=128):
     """configs[2] with real workers: a torchvision ResNet-50 (10 classes,
     23,528,522 parameters) per GPU on synthetic 32x32x3 batches, parameters
@@ -412,6 +458,7 @@ def bench_main(args, metric):
     sweep = bandwidth_sweep(world, rank, local, warm, steps) if not getattr(args, "no_sweep", False) else []
     tw = (torch_workers_bench(world, rank, local, max(warm, 5), min(steps, 10))
           if not getattr(args, "no_sweep", False) else None)
+    c4 = throttled_bench(world, rank, local) if not getattr(args, "no_sweep", False) else None
     if sampler is not None:
         sampler.__exit__(None, None, None)
     if rank == 0:
@@ -441,6 +488,7 @@ def bench_main(args, metric):
             "cpu_baseline": None,
             "sweep": sweep,
             "torch_workers": tw,
+            "c4_throttled_sharded": c4,
             "clocks": sampler.summary() if sampler else None,
         }
         print(json.dumps(line))
