@@ -72,3 +72,27 @@ def test_replay_call_array_layout_matches_the_c_abi():
     for name in ("PS_CALL_PULL", "PS_CALL_APPLY", "PS_CALL_DECIDE"):
         assert name in header
     assert ctypes.sizeof(ctypes.c_double) + 2 * ctypes.sizeof(ctypes.c_int32) == 16
+
+
+def test_groups_from_trace_partition_pushes_and_pulls():
+    """groups_from_trace (the sharded server's schedule input) covers every
+    push once, in trace order, groups same-instant pushes exactly like
+    calls_from_trace, and gives every pull after the first group a home."""
+    from paper_1908_11848_b200.sharded import groups_from_trace
+    for run in oracle.load_golden("sim_corpus.json.gz")["runs"][:40]:
+        entries = _entries(run["trace"])
+        groups = groups_from_trace(entries)
+        pushes = [(e.time, e.worker) for e in entries if e.kind == "push_arrive"]
+        assert [(t, w) for t, order, _ in groups for w in order] == pushes
+        calls = calls_from_trace(entries)
+        decide_groups, cur = [], []
+        for c in calls:
+            if c[0] == "apply":
+                cur.append(c[1])
+            elif c[0] == "decide" and cur:
+                decide_groups.append(cur)
+                cur = []
+        assert [order for _, order, _ in groups] == decide_groups
+        first = next(i for i, e in enumerate(entries) if e.kind == "push_arrive")
+        late_pulls = sum(1 for e in entries[first:] if e.kind == "pull_arrive")
+        assert sum(len(p) for _, _, p in groups) == late_pulls
