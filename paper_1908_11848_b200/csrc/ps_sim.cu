@@ -821,9 +821,10 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
     // pulls in [from, to) must not come from a deferred worker (one vote per
     // run of pulls: the deferred set only changes at decides)
     auto check_pulls = [&](int from, int to) {
+      const unsigned long long dm = g.deferred_mask();
+      if (!dm) return;  // nobody is deferred: no pull can violate
       const unsigned rng = mp & (to >= 32 ? kFull : ((1u << to) - 1u)) & ~((1u << from) - 1u);
       if (!rng) return;
-      const unsigned long long dm = g.deferred_mask();
       const unsigned hit = __ballot_sync(kFull, ((rng >> lane) & 1u) && ((dm >> (c.worker & 63)) & 1ull));
       if (hit) fail = __ffs(hit) - 1;
     };
