@@ -493,12 +493,16 @@ def e2e_batched(torch, ps, calls, synth_host, d, w0, steps=30):
     step()
     step()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    applied = 0
+    # wall clock per step (every step ends in a host read of its results);
+    # the median step, so a host hiccup does not stand in for the engine
+    per_step, applied = [], 0
     for _ in range(steps):
-        applied += step().applied
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r = step()
+        torch.cuda.synchronize()
+        per_step.append(time.perf_counter() - t0)
+        applied = r.applied
+    dt = statistics.median(per_step)
     n_dec = sum(1 for c in calls if c[0] == "decide")
     h2d = pinned.numel() * 4 + 16 * len(calls)
     d2h = 8 * n_dec + 4 * d
