@@ -800,7 +800,15 @@ int shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, 
     SCK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kThreads, 0));
     occupancy[oi] = resident;
   }
-  const int total = h->sm_count * (per_sm_env < resident ? per_sm_env : resident);
+  int total = h->sm_count * (per_sm_env < resident ? per_sm_env : resident);
+  // no more streaming CTAs than one trip over the shard needs: idle CTAs
+  // would only lengthen every step's election and polling
+  {
+    const int U = gsel <= 2 ? 4 : gsel <= 4 ? 2 : 1;  // float4 per thread per trip (k_shard_run)
+    const long long nv = (h->n_local + 3) / 4;
+    const long long need_ctas = (nv + (long long)kThreads * U - 1) / ((long long)kThreads * U);
+    if (need_ctas + 1 < total) total = (int)(need_ctas > 0 ? need_ctas : 1) + 1;
+  }
   const int data_ctas = total - 1;
   if (data_ctas < 1) return sfail(h, PS_E_CUDA, "k_shard_run cannot be resident");
   if (h->now_cap < steps) {
