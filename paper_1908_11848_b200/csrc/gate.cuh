@@ -53,11 +53,19 @@ __device__ __forceinline__ int controller_grid(double lp, double pp, double ls, 
     // dependent steps (policy.py:127-132)
     if (lane <= r_max) {
       const double cand = __dadd_rn(lp, __dmul_rn((double)lane, ip));
-      double m = __longlong_as_double(0x7ff0000000000000ll);
-      double kf = 1.0;  // k + 1, exact
-      for (int k = 0; k <= r_max; ++k, kf += 1.0)
-        m = fmin(m, fabs(__dsub_rn(__dadd_rn(ls, __dmul_rn(kf, is)), cand)));
-      best = m;
+      const double inf = __longlong_as_double(0x7ff0000000000000ll);
+      // all distances first (independent), then a min tree: no serial chain
+      // through 17 dependent fp64 min operations
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        v[k] = k <= r_max ? fabs(__dsub_rn(__dadd_rn(ls, __dmul_rn((double)(k + 1), is)), cand)) : inf;
+#pragma unroll
+      for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+        for (int k = 0; k < w; ++k) v[k] = fmin(v[k], v[k + w]);
+      // k = 16 (r_max == 16) is the one entry the tree does not hold
+      best = r_max >= 16 ? fmin(v[0], fabs(__dsub_rn(__dadd_rn(ls, __dmul_rn(17.0, is)), cand))) : v[0];
       best_r = lane;
     }
   } else
