@@ -278,7 +278,11 @@ def reference_calls(paradigm="dssp"):
 
 def apply_sweep(torch, ps, hbm_peak):
     """configs[4]: push-apply (12 B/param) and pull (8 B/param) kernels from
-    1 MB to 1 GB of fp32 parameters; L2 flushed before every timed launch."""
+    1 MB to 1 GB of fp32 parameters; L2 flushed before every timed launch.
+    The library's profiling events bracket the op behind a 50 us device spin,
+    so each time is the op's device time (its launches, the apply's
+    flag reduction and host-mirror publish included), not the host's submit
+    gap on an idle stream."""
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     out = []
     for mb in (1, 4, 16, 64, 256, 1024):

@@ -239,6 +239,14 @@ __global__ void k_controller_batch(const double* tables, const int* r_max, int n
   if ((threadIdx.x & 31) == 0) out[row] = r;
 }
 
+constexpr unsigned long long kProfileSpinNs = 50000;
+
+__global__ void k_spin(unsigned long long ns) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) {
+  }
+}
+
 int grid_for(const ps_server* h, long long nv) {
   long long per_block = (long long)kApplyThreads * kApplyUnroll;
   long long blocks = (nv + per_block - 1) / per_block;
@@ -284,7 +292,15 @@ int finish_op(ps_server* h) {
 }
 
 int mark(ps_server* h, cudaEvent_t e) {
-  if (h->profile) PS_CK(h, cudaEventRecord(e, h->stream));
+  if (!h->profile) return PS_OK;
+  // the start event goes in behind a short device spin: the op's launches
+  // are then queued before the GPU reaches it, so ev0..ev1 is device time
+  // only, not the host's submit gap on an idle stream
+  if (e == h->ev0) {
+    k_spin<<<1, 32, 0, h->stream>>>(kProfileSpinNs);
+    PS_CK(h, cudaGetLastError());
+  }
+  PS_CK(h, cudaEventRecord(e, h->stream));
   return PS_OK;
 }
 
