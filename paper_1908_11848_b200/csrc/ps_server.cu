@@ -134,13 +134,13 @@ k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g,
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_bad) atomicOr(&ctrl->bad, s_bad);
-    __threadfence();
-    const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
+    // one GPU-scope acq_rel arrival: releases this CTA's flag bits, and the
+    // last arriver acquires every earlier CTA's (no separate fences)
+    const unsigned prev = atom_add_acq_rel_gpu_u32(&ctrl->arrive, 1u);
     s_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last || threadIdx.x >= 32) return;
-  __threadfence();
   const int lane = threadIdx.x;
   int status = PS_OK;
   if (lane == 0) {
