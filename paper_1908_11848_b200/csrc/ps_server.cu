@@ -86,8 +86,9 @@ __device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* mirror) {
 template <typename G>
 __global__ void __launch_bounds__(kApplyThreads)
 k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g, long long n,
-        float lr, Ctrl* ctrl, int fuse, int worker, double now, Ctrl* mirror) {
-  const int cur = *reinterpret_cast<volatile int*>(&ctrl->cur);
+        float lr, Ctrl* ctrl, int cur, int fuse, int worker, double now, Ctrl* mirror) {
+  // cur comes from the host (h->cur, refreshed after every op's sync -- the
+  // same value pulls read from): no dependent load ahead of the data loads
   const float4* src = reinterpret_cast<const float4*>(cur ? w1 : w0);
   float4* dst = reinterpret_cast<float4*>(cur ? w0 : w1);
   const long long nv = n >> 2;
@@ -367,10 +368,11 @@ int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_
   if ((rc = mark(h, h->ev0))) return rc;
   if (g_dtype == PS_F32)
     k_apply<float><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const float*)dg, h->d,
-                                                          lr, h->ctrl, fuse, worker, now, h->hctrl_dev);
+                                                          lr, h->ctrl, h->cur, fuse, worker, now,
+                                                          h->hctrl_dev);
   else
     k_apply<double><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const double*)dg,
-                                                           h->d, lr, h->ctrl, fuse, worker, now,
+                                                           h->d, lr, h->ctrl, h->cur, fuse, worker, now,
                                                            h->hctrl_dev);
   PS_CK(h, cudaGetLastError());
   if ((rc = mark(h, h->ev1))) return rc;
