@@ -11,9 +11,9 @@ namespace dssp {
 // Device control block of one server (lives in the server GPU's HBM).
 struct Ctrl {
   ps_gate_state gate;          // policy tables + version / rejected counters
-  int32_t cur;                 // which of the two weight buffers is current
   uint32_t arrive;             // last-CTA election counter of the apply kernel
-  uint32_t bad;                // bit0: non-finite gradient, bit1: non-finite result
+  uint32_t bad;                // per-CTA flag counts riding on the arrival (8-aligned pair)
+  int32_t cur;                 // which of the two weight buffers is current
   int32_t status;              // result of the last op (enum ps_status)
   int32_t applied;
   int32_t granted;

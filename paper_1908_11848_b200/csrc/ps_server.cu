@@ -13,6 +13,7 @@
 // (handle_push, server.py:80-82) the same last CTA then runs the gate
 // decision, so apply + clock increment + decision is one launch.
 #include <cuda_runtime.h>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -129,28 +130,36 @@ k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g,
   bad = __reduce_or_sync(kFull, bad);
   __shared__ unsigned s_bad;
   __shared__ int s_last;
+  __shared__ unsigned s_flags;
   if (threadIdx.x == 0) s_bad = 0;
   __syncthreads();
   if ((threadIdx.x & 31) == 0 && bad) atomicOr(&s_bad, bad);
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (s_bad) atomicOr(&ctrl->bad, s_bad);
-    // one GPU-scope acq_rel arrival: releases this CTA's flag bits, and the
-    // last arriver acquires every earlier CTA's (no separate fences)
-    const unsigned prev = atom_add_acq_rel_gpu_u32(&ctrl->arrive, 1u);
-    s_last = (prev == gridDim.x - 1);
+    // one 64-bit GPU-scope acq_rel arrival on the (arrive, bad) pair: the low
+    // word counts CTAs, the high word counts CTAs that saw a non-finite
+    // update (bits 0-15) or result (bits 16-31), so the last arriver holds
+    // every CTA's verdict without a second atomic
+    static_assert(offsetof(Ctrl, bad) == offsetof(Ctrl, arrive) + 4 && offsetof(Ctrl, arrive) % 8 == 0,
+                  "arrive/bad pair");
+    const unsigned long long add =
+        1ull | ((unsigned long long)((s_bad & 1u) | ((s_bad & 2u) << 15)) << 32);
+    const unsigned long long prev =
+        atom_add_acq_rel_gpu_u64(reinterpret_cast<unsigned long long*>(&ctrl->arrive), add);
+    s_last = ((unsigned)prev == gridDim.x - 1);
+    s_flags = (unsigned)((prev + add) >> 32);
   }
   __syncthreads();
   if (!s_last || threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   int status = PS_OK;
   if (lane == 0) {
-    const unsigned b = atomicAdd(&ctrl->bad, 0u);
+    const unsigned b = s_flags;
     int applied = 0;
-    if (b & 1u) {
+    if (b & 0xffffu) {
       status = PS_REJECTED;
       ctrl->gate.rejected += 1;
-    } else if (b & 2u) {
+    } else if (b >> 16) {
       status = PS_E_DIVERGED;
     } else {
       ctrl->cur = cur ^ 1;
