@@ -3,33 +3,35 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
 
-N=1 (default) measures BASELINE.json configs[1] ("C2"): a ResNet-20-sized
-server (d = 272,474 fp32) with P = 4 workers on the heterogeneous gtx-mix
-schedule (simnet.py:34-69; 2 fast + 2 workers 2.2x slower). One "step" is the
-server serving the request stream of one complete run (250 iterations per
-worker: 1,000 push-applies, 1,004 pulls, 1,000 gate decisions) in the order
-the reference simulator issues them (tests/golden/c2_schedule.json.gz,
-recorded from stalesync itself), in one device-resident kernel; every
-decision is checked against the recorded one. The closed-loop variant (the
-simulator's whole event loop on the device, trace byte-identical) is reported
-as device_simulation. Updates are synthetic N(0,1) fp32 vectors resident in
-HBM (2 per worker), lr = 0.05. The headline paradigm is DSSP(3, 12); BSP,
-SSP(3) and ASP are reported beside it.
-
-N>1 (torchrun, one process per GPU) measures configs[2] ("C3"): a
-ResNet-50-sized server (d = 23,528,522 fp32) sharded by contiguous range
-across the N GPUs, one worker per GPU, homogeneous workers; each step every
-worker pushes its update to every shard owner over NVLink P2P, the owners
-apply all N updates in ticket order, the replicated device gate decides, and
-every worker pulls the full weights back over NVLink.
+The headline at EVERY N is BASELINE.json configs[2] ("C3"): a ResNet-50-sized
+server (d = 23,528,522 fp32) sharded by contiguous range across the N GPUs
+(N = 1: the same server at G = 1), one homogeneous worker per GPU. One step is
+one push group: every worker pushes its update, each shard owner applies the N
+updates in ticket order (over NVLink P2P for N > 1), the replicated device
+gate decides (DSSP(3,12) headline; SSP(3), BSP, ASP beside it) and every worker
+pulls the new weights. Weak scaling: every GPU owns d/N parameters and applies
+N updates to them per step. Inputs exceed L2 (94 MB update + 94 MB replica +
+the double-buffered shard per GPU), so the HBM (N = 1) / NVLink (N > 1)
+roofline is the bound that matters.
 
 The line also carries:
-  e2e          the same metric through the reference-facing API
-               (ParameterServer drop-in, host buffers, H2D/D2H per call);
-  roofline     the dominant kernel's achieved bytes/s vs the measured peak;
-  cpu_baseline the reference algorithm (oracle/ port, fp64 numpy, 1 core) on
-               a bounded sample of the same call sequence;
-  sweep        push-apply / pull kernels at 1 MB .. 1 GB (configs[4]).
+  parity       decisions of every paradigm against the reference simulator's
+               trace of the same schedule, and every shard / replica
+               fingerprint against the fp32 replay of the same applies;
+  e2e          the same step through the C-ABI with the update H2D from pinned
+               host memory and the gate state D2H every step;
+  roofline     k_shard_run against HBM (N = 1) or NVLink (N > 1);
+  cpu_baseline the reference (stalesync, unmodified, staged into oracle/_ref;
+               the oracle port if absent) on a bounded sample of the same
+               workload, pinned to one host core;
+  N = 1 only:  `c2` -- BASELINE configs[1] (ResNet-20-sized single-GPU server,
+               P = 4, gtx-mix) served as the reference's recorded request
+               stream in one kernel, reported as latency (us per call /
+               decision; it is L2- and latency-bound), its e2e variants, the
+               simulated run loop; `sweep` (configs[4], 1 MB - 1 GB);
+               `c4_*` (configs[3]); torch workers.
+  N > 1:       the sharded sweep (configs[4] at N GPUs), configs[3] across
+               GPUs, ResNet-50 workers on the sharded server.
 """
 
 from __future__ import annotations
@@ -137,139 +139,212 @@ def flush_l2(torch, buf):
 
 
 # ---------------------------------------------------------------------------
-# reference arm / cpu baseline: the oracle port of the reference algorithm
+# reference arm / cpu baseline: the reference's own CPU implementation
 # ---------------------------------------------------------------------------
 
-def reference_sample(calls, synth, d, paradigm, s_lower, r_max, lr, max_updates):
-    """Time the reference algorithm (oracle.RefPortServer: fp64 numpy apply
-    with the reference's temporaries and frozen copies, Python gate) on the
-    first `max_updates` applies of the call sequence. Returns (updates, s)."""
-    import oracle
-    w0 = oracle.initial_weights_f64(0, d)
-    srv = oracle.RefPortServer(paradigm, synth.shape[0], s_lower, r_max, lr, w0)
-    g64 = [[np.array(synth[p, k, :d], dtype=np.float64) for k in range(synth.shape[1])]
-           for p in range(synth.shape[0])]
-    for row in g64:
-        for g in row:
-            g.flags.writeable = False
-    pushes = {}
-    updates = 0
-    t0 = time.perf_counter()
-    for call in calls:
-        if call[0] == "apply":
-            k = pushes.get(call[1], 0)
-            pushes[call[1]] = k + 1
-            srv.apply_gradient(g64[call[1]][k % len(g64[call[1]])])
-            updates += 1
-        elif call[0] == "decide":
-            srv.decide_push(call[1], call[2])
-        elif call[0] == "pull":
-            srv.handle_pull(call[1])
-        if updates >= max_updates and call[0] == "decide":
-            break
-    return updates, time.perf_counter() - t0
-
-
-def reference_c3_step(srv, grads, times_i, world):
-    """One C3 push group through the reference algorithm (simnet.py:167-201):
-    every worker's apply in seq order, then each decision, then every pull."""
-    for p in range(world):
-        srv.apply_gradient(grads[p % len(grads)])
-    for p in range(world):
-        srv.decide_push(p, times_i)
-    for p in range(world):
-        srv.handle_pull(p)
-
-
-def run_reference_arm_sharded(args, world):
-    """N > 1: the reference CPU server on OUR arm's N>1 workload (C3: d =
-    23,528,522, `world` homogeneous workers, DSSP(3,12)); one step = one push
-    group, exactly what one step of the sharded engine does."""
-    import oracle
-    from paper_1908_11848_b200.sharded import C3_DIM, homogeneous_push_times
-    d = C3_DIM
-    rng = np.random.default_rng(1000)
-    grads = []
-    for _ in range(2):  # two distinct N(0,1) updates, alternated by worker (memory bound on the host)
-        g = rng.standard_normal(d)
-        g.flags.writeable = False
-        grads.append(g)
-    srv = oracle.RefPortServer("dssp", world, 3, 12, 0.05, oracle.initial_weights_f64(0, d))
-    times = homogeneous_push_times(1.0, 0.05, args.warmup + args.steps)
-    for i in range(args.warmup):
-        reference_c3_step(srv, grads, times[i], world)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        reference_c3_step(srv, grads, times[args.warmup + i], world)
-    total = time.perf_counter() - t0
-    value = args.steps * world / total
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C3 (BASELINE configs[2]): d={d}, {world} homogeneous workers, "
-                               "DSSP(3,12); step = one push group (every worker's apply, decide, pull)",
-                   "d": d, "workers": world},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} push groups of {world} updates (oracle.RefPortServer, "
-                                   "fp64 numpy, single-threaded like the reference)"},
-        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
-    return 0
-
-
-def run_reference_arm(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    if world > 1:
-        return run_reference_arm_sharded(args, world)
-    import paper_1908_11848_b200 as ps
-    # the call sequence of the C2 schedule is fixed by the reference
-    # simulator semantics; replay it with the same synthetic updates
-    cfg = c2_config("dssp", 3, 12)
-    calls, _ = reference_calls("dssp")
-    synth = synthetic_host(4, 2, C2_DIM)
-    n_updates = sum(1 for c in calls if c[0] == "apply")
-    per_step = min(n_updates, 250)
-    for _ in range(args.warmup):
-        reference_sample(calls, synth, C2_DIM, "dssp", 3, 12, cfg.learning_rate, per_step)
-    times, ups = [], 0
-    for _ in range(args.steps):
-        u, s = reference_sample(calls, synth, C2_DIM, "dssp", 3, 12, cfg.learning_rate, per_step)
-        times.append(s)
-        ups += u
-    total = sum(times)
-    value = ups / total
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 call sequence (DSSP(3,12), P=4, gtx-mix), d=272474; "
-                               f"each step = the first {per_step} updates"},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": "port",
-                         "sample": f"{per_step} updates x {args.steps} steps of the C2 call sequence"},
-        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
-    return 0
+def load_fixture(name):
+    """A committed fixture under tests/golden (recorded from the reference)."""
+    import gzip
+    path = os.path.join(ROOT, "tests", "golden", name)
+    opener = gzip.open if name.endswith(".gz") else open
+    with opener(path, "rt") as fh:
+        return json.load(fh)
 
 
 def reference_calls(paradigm="dssp"):
     """The C2 server-call sequence and trace recorded from the reference
     simulator itself (tests/golden/c2_schedule.json.gz, made by
     tests/golden/make_golden.py)."""
-    import oracle
-    for run in oracle.load_golden("c2_schedule.json.gz")["runs"]:
+    for run in load_fixture("c2_schedule.json.gz")["runs"]:
         if run["name"] == f"c2_{paradigm}":
             calls = [tuple(c[:2]) if c[0] != "decide" else ("decide", c[1], c[2])
                      for c in run["calls"] if c[0] in ("pull", "apply", "decide")]
             return calls, run["trace"]
     raise KeyError(paradigm)
+
+
+def pin_one_core():
+    """Pin this process to one host core (the reference is single-threaded
+    numpy): the highest-numbered core it may use, away from the ranks'
+    launch threads. Returns (core, host cpu count)."""
+    cores = sorted(os.sched_getaffinity(0))
+    core = cores[-1]
+    os.sched_setaffinity(0, {core})
+    return core, os.cpu_count()
+
+
+def reference_server_factory():
+    """(kind, make(paradigm, P, s_lower, r_max, lr, d) -> server, GradientVector):
+    the unmodified reference (stalesync, staged into oracle/_ref by
+    oracle/stage_ref.sh) when present, else the oracle's port of it."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "stalesync")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import stalesync
+        from stalesync.config import make_config, validate_config
+
+        def make(paradigm, P, s_lower, r_max, lr, d):
+            cfg = validate_config(make_config(paradigm=paradigm, worker_count=P, s_lower=s_lower,
+                                              r_max=r_max, learning_rate=lr, seed=0, dimension=d,
+                                              timing_preset="homogeneous", compute_base=1.0,
+                                              comm_delay=0.05, dataset_size=P, batch_size=1))
+            return stalesync.ParameterServer(cfg, d)
+        return "reference", make, stalesync.GradientVector
+    import oracle
+
+    def make(paradigm, P, s_lower, r_max, lr, d):
+        return oracle.RefPortServer(paradigm, P, s_lower, r_max, lr, oracle.initial_weights_f64(0, d))
+
+    class _G:
+        def __new__(cls, values, source, source_iter=0):
+            values = np.asarray(values, dtype=np.float64)
+            values.flags.writeable = False
+            return values
+    return "port", make, _G
+
+
+def reference_c3_groups(world, steps, warmup, time_budget_s=None):
+    """The reference CPU server on the C3 workload with `world` homogeneous
+    workers: one step = one push group (simnet.py:167-201): every worker's
+    apply_gradient in seq order, then each decide_push, then every
+    handle_pull. Returns (kind, seconds per step list)."""
+    d = C3_DIM
+    kind, make, GV = reference_server_factory()
+    srv = make("dssp", world, 3, 12, 0.05, d)
+    rng = np.random.default_rng(1000)
+    # two distinct N(0,1) updates, alternated by worker; built once, outside
+    # the timing (a GradientVector copies its values, config.py:48-51)
+    grads = [GV(rng.standard_normal(d), p, 1) for p in range(min(world, 2))]
+    from paper_1908_11848_b200.sharded import homogeneous_push_times
+    times = homogeneous_push_times(1.0, 0.05, warmup + steps)
+
+    def group(now):
+        for p in range(world):
+            srv.apply_gradient(grads[p % len(grads)])  # apply_gradient reads only .values
+        for p in range(world):
+            srv.decide_push(p, now)
+        for p in range(world):
+            srv.handle_pull(p)
+
+    for i in range(warmup):
+        group(times[i])
+    out = []
+    t_all = time.perf_counter()
+    for i in range(steps):
+        t0 = time.perf_counter()
+        group(times[warmup + i])
+        out.append(time.perf_counter() - t0)
+        if time_budget_s and time.perf_counter() - t_all > time_budget_s and len(out) >= 2:
+            break
+    return kind, out
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation on OUR arm's
+    workload (C3 at N workers, DSSP(3,12)), rank 0 only, pinned to one core."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    core, ncpu = pin_one_core()
+    kind, secs = reference_c3_groups(world, args.steps, args.warmup)
+    total = sum(secs)
+    value = len(secs) * world / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
+        "n_gpus": args.gpus, "steps": len(secs), "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(secs), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C3 (BASELINE configs[2]): d={C3_DIM}, {world} homogeneous worker(s), "
+                               "DSSP(3,12); step = one push group (every worker's apply, decide, pull)",
+                   "d": C3_DIM, "workers": world},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": 1, "kind": kind,
+                         "sample": f"{len(secs)} push groups of {world} updates, "
+                                   + ("stalesync 0.1.0 unmodified (oracle/_ref)" if kind == "reference"
+                                      else "oracle.RefPortServer (port)")
+                                   + f", pinned to host core {core} of {ncpu}"},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_sample_main(args):
+    """Child process of the engine arm (the cpu_baseline leg and the weight
+    checker; the only engine-arm code that touches oracle/): pinned to one
+    core, times the reference on a bounded sample and prints one JSON line."""
+    core, ncpu = pin_one_core()
+    if args.cpu_sample == "c2":
+        calls, _ = reference_calls("dssp")
+        synth = synthetic_host(4, 2, C2_DIM)
+        kind, make, GV = reference_server_factory()
+        srv = make("dssp", 4, 3, 12, 0.05, C2_DIM)
+        gv = [[GV(np.array(synth[p, k, :C2_DIM], dtype=np.float64), p, k) for k in range(2)]
+              for p in range(4)]
+        pushes, updates = {}, 0
+        t0 = time.perf_counter()
+        for call in calls:
+            if call[0] == "apply":
+                k = pushes.get(call[1], 0)
+                pushes[call[1]] = k + 1
+                srv.apply_gradient(gv[call[1]][k % 2])
+                updates += 1
+            elif call[0] == "decide":
+                srv.decide_push(call[1], call[2])
+            else:
+                srv.handle_pull(call[1])
+        dt = time.perf_counter() - t0
+        print(json.dumps({"value": updates / dt, "unit": "updates/s", "cores": 1, "kind": kind,
+                          "sample": f"the whole C2 request stream ({updates} updates, same as one "
+                                    f"engine step), pinned to host core {core} of {ncpu}",
+                          "host_cpus": ncpu, "us_per_update": 1e6 * dt / updates}))
+        return 0
+    # c3: reference timing + fp32 replay fingerprints of the engine's weights
+    world, applies = args.world, args.applies
+    kind, secs = reference_c3_groups(world, 50, 1, time_budget_s=12.0)
+    value = len(secs) * world / sum(secs)
+    import oracle
+    from paper_1908_11848_b200.sharded import _fp32_checksums, host_update, shard_range
+    d = C3_DIM
+    w = oracle.initial_weights_f64(0, d).astype(np.float32)
+    gs = [host_update(d, p) for p in range(world)]
+    for i in range(applies):
+        w = oracle.apply_f32(w, gs[i % world], 0.05)
+    shards = []
+    for r in range(world):
+        lo, hi = shard_range(d, world, r)
+        shards.append(_fp32_checksums(w[lo:hi]))
+    print(json.dumps({"cpu_baseline": {
+        "value": value, "unit": "updates/s", "cores": 1, "kind": kind,
+        "sample": f"{len(secs)} push groups of {world} updates of the same C3 workload, "
+                  + ("stalesync 0.1.0 unmodified (oracle/_ref)" if kind == "reference"
+                     else "oracle.RefPortServer (port)") + f", pinned to host core {core} of {ncpu}",
+        "host_cpus": ncpu},
+        "fingerprints": {"shards": shards, "replica": _fp32_checksums(w)}}))
+    return 0
+
+
+def _run_cpu_child(extra):
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-sample"] + extra,
+                         capture_output=True, text=True, timeout=900)
+    if out.returncode != 0:
+        raise RuntimeError("cpu sample failed: " + out.stderr[-2000:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline_c3(world, applies):
+    return _run_cpu_child(["c3", "--world", str(world), "--applies", str(applies)])
+
+
+def shard_traffic():
+    """DRAM bytes per step of k_shard_run at G = 1 from the committed ncu
+    capture (profiles/k_shard_run_dram_bytes.json), or None."""
+    tpath = os.path.join(ROOT, "profiles", "k_shard_run_dram_bytes.json")
+    try:
+        return json.load(open(tpath)).get("dram_bytes_per_step")
+    except Exception:
+        return None
 
 
 # ---------------------------------------------------------------------------
@@ -514,22 +589,23 @@ def e2e_batched(torch, ps, calls, synth_host, d, w0, steps=30):
     return applied / dt, h2d, d2h
 
 
-def bench_single(args):
-    import torch
-    import paper_1908_11848_b200 as ps
+def single_gpu_extras(torch, ps, line):
+    """N = 1 blocks beside the C3 headline (rank 0): BASELINE configs[1]
+    ("C2") as the reference's recorded request stream served in one kernel,
+    the simulated run loop, its e2e variants and CPU figure, the configs[4]
+    sweep, configs[3] and the ResNet-20 torch workers."""
+    from paper_1908_11848_b200.config import initial_weights_f64
     from paper_1908_11848_b200.engine import Engine
     from paper_1908_11848_b200.sim import DeviceReplay
 
-    hbm_peak, peak_kind = peaks()
+    hbm_peak, _ = peaks()
+    steps, warm = line["steps"], line["warmup"]
     d = C2_DIM
     P, K = 4, 2
     synth_host = synthetic_host(P, K, d)
     synth = torch.from_numpy(synth_host).cuda()
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-    import oracle
-    w0 = oracle.initial_weights_f64(0, d)
-    # (1) headline: the device serving the recorded C2 request stream
-    #     (pull / apply / decide, reference order), decisions by the device gate
+    w0 = initial_weights_f64(c2_config("dssp", 3, 12), d)
     replays, sims, recorded = {}, {}, {}
     for name, s, r in PARADIGMS:
         calls, trace = reference_calls(name)
@@ -540,133 +616,91 @@ def bench_single(args):
         sim = ps.DeviceSimulation(cfg, dimension=d, grad="synthetic")
         sim.set_synthetic(synth, K)
         sims[name] = (cfg, sim)
-        for _ in range(args.warmup):
+        for _ in range(warm):
             replays[name].run(decisions=False)
             sim.run(read_weights=False, reset_gate=True)
-    sampler = ClockSampler(0)
-    per_paradigm, device_sim, parity, reports = {}, {}, {}, {}
-    with sampler:
-        for name, s, r in PARADIGMS:
-            times, applied = [], 0
-            for _ in range(args.steps):
-                flush_l2(torch, flush)
-                torch.cuda.synchronize()
-                rr = replays[name].run(decisions=False)
-                times.append(rr.device_ms)
-                applied += rr.applied
-            total_ms = sum(times)
-            check = replays[name].run()
-            want = [(ln.split("\t")[4]) for ln in recorded[name].splitlines()
-                    if ln.split("\t")[2] == "push_arrive"]
-            got = [ps.decision_token(o == "grant", rel) for o, rel in check.decisions]
-            per_paradigm[name] = {"updates_per_s": applied / (total_ms * 1e-3),
-                                  "iters_per_s": applied / (total_ms * 1e-3),
-                                  "ms_per_step": total_ms / args.steps,
-                                  "defers_per_step": sum(1 for o, _ in check.decisions if o == "defer")}
-            parity.setdefault("replay_decisions_identical_to_reference", {})[name] = got == want
-        # (2) the closed loop: the simulator's whole event loop on the device
-        for name, s, r in PARADIGMS:
-            cfg, sim = sims[name]
-            times, applied = [], 0
-            rep = None
-            for _ in range(args.steps):
-                flush_l2(torch, flush)
-                torch.cuda.synchronize()
-                rep = sim.run(read_weights=False, reset_gate=True)
-                times.append(rep.device_ms)
-                applied += rep.applied
-            reports[name] = rep
-            total_ms = sum(times)
-            device_sim[name] = {"updates_per_s": applied / (total_ms * 1e-3),
-                                "ms_per_step": total_ms / args.steps,
-                                "virtual_duration_s": max(e.time for e in rep.entries)}
-            parity.setdefault("simulation_trace_identical_to_reference", {})[name] = \
-                ps.format_trace(rep.entries) == recorded[name]
-    head = per_paradigm["dssp"]
+    per_paradigm, device_sim, parity = {}, {}, {}
+    for name, s, r in PARADIGMS:
+        calls, _ = reference_calls(name)
+        n_apply = sum(1 for c in calls if c[0] == "apply")
+        n_dec = sum(1 for c in calls if c[0] == "decide")
+        times, applied = [], 0
+        for _ in range(steps):
+            flush_l2(torch, flush)
+            torch.cuda.synchronize()
+            rr = replays[name].run(decisions=False)
+            times.append(rr.device_ms)
+            applied += rr.applied
+        total_ms = sum(times)
+        check = replays[name].run()
+        want = [(ln.split("\t")[4]) for ln in recorded[name].splitlines()
+                if ln.split("\t")[2] == "push_arrive"]
+        got = [ps.decision_token(o == "grant", rel) for o, rel in check.decisions]
+        ms = total_ms / steps
+        per_paradigm[name] = {"updates_per_s": applied / (total_ms * 1e-3),
+                              "ms_per_step": ms,
+                              "us_per_call": 1e3 * ms / len(calls),
+                              "us_per_decision": 1e3 * ms / n_dec,
+                              "decisions_per_s": n_dec / (ms * 1e-3),
+                              "calls_per_step": len(calls), "updates_per_step": n_apply,
+                              "defers_per_step": sum(1 for o, _ in check.decisions if o == "defer")}
+        parity.setdefault("replay_decisions_identical_to_reference", {})[name] = got == want
+    for name, s, r in PARADIGMS:
+        cfg, sim = sims[name]
+        times, applied = [], 0
+        rep = None
+        for _ in range(steps):
+            flush_l2(torch, flush)
+            torch.cuda.synchronize()
+            rep = sim.run(read_weights=False, reset_gate=True)
+            times.append(rep.device_ms)
+            applied += rep.applied
+        total_ms = sum(times)
+        device_sim[name] = {"updates_per_s": applied / (total_ms * 1e-3),
+                            "ms_per_step": total_ms / steps,
+                            "virtual_duration_s": max(e.time for e in rep.entries)}
+        parity.setdefault("simulation_trace_identical_to_reference", {})[name] = \
+            ps.format_trace(rep.entries) == recorded[name]
+    for name in replays:
+        replays[name].engine.close()
+        sims[name][1].engine.close()
     calls, _ = reference_calls("dssp")
-    n_apply = sum(1 for c in calls if c[0] == "apply")
-    n_pull = sum(1 for c in calls if c[0] == "pull")
-    # roofline of the dominant kernel (k_sim, replay mode): algorithmic bytes
-    # per launch = updates x 12 B/param (push-apply) + pulls x 8 B/param
-    alg_bytes = n_apply * 12 * d + n_pull * 8 * d
-    achieved = alg_bytes / (head["ms_per_step"] * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "k_sim_dram_bytes.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
     cfg = c2_config("dssp", 3, 12)
     e2e_value, h2d, d2h, e2e_updates = e2e_drop_in(torch, ps, cfg, calls, synth_host, d)
     eb_value, eb_h2d, eb_d2h = e2e_batched(torch, ps, calls, synth_host, d, w0)
-    cpu_updates, cpu_s = reference_sample(calls, synth_host, d, "dssp", 3, 12, cfg.learning_rate,
-                                          max_updates=args.cpu_updates)
-    sweep = apply_sweep(torch, ps, hbm_peak) if not args.no_sweep else None
-    c4 = c4_throttled(torch, ps) if not args.no_sweep else None
-    c4_rt = c4_realtime(torch, ps) if not args.no_sweep else None
-    tw = torch_workers(torch, ps) if not args.no_sweep else None
-    clocks = sampler.summary()
-    line = {
-        "metric": METRIC,
-        "value": head["updates_per_s"],
-        "unit": "updates/s",
-        "n_gpus": 1,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": head["ms_per_step"],
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": "C2 (BASELINE configs[1]): ResNet-20-sized server d=272474 fp32, "
-                               "P=4 workers, gtx-mix schedule, DSSP(3,12); step = the server "
-                               "serving the reference's recorded request stream of one run "
-                               f"({n_apply} pushes, {n_pull} pulls, {n_apply} gate decisions) "
-                               "in one device-resident kernel",
-                   "d": d, "workers": P, "paradigm": "dssp", "s_lower": 3, "r_max": 12,
-                   "updates_per_step": n_apply, "l2": "flushed between timed steps (256 MiB write)",
-                   "parallelism": "single GPU"},
-        "per_paradigm": per_paradigm,
-        "device_simulation": device_sim,
-        "parity": parity,
-        # e2e: the headline workload (the same call stream and resident
-        # updates as `value`) through the batch C-ABI call with host buffers
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "k_sim_dram_bytes.json"))).get(
+            "dram_bytes_per_launch")
+    except Exception:
+        pass
+    del synth, flush
+    torch.cuda.empty_cache()
+    line["c2"] = {
+        "workload": "C2 (BASELINE configs[1]): ResNet-20-sized single-GPU server d=272474 fp32, "
+                    "P=4, gtx-mix; step = the server serving the reference's recorded request "
+                    "stream of one run (1,000 pushes, 1,004 pulls, 1,000 decisions) in one kernel",
+        "bound": "latency: the 1 MB of weights live in registers and the updates in L2 for the "
+                 "whole stream (dram_bytes_per_launch from ncu), so it is reported per call and "
+                 "per decision, not as an HBM fraction",
+        "dram_bytes_per_launch": traffic,
+        "value": per_paradigm["dssp"]["updates_per_s"], "unit": "updates/s",
+        "per_paradigm": per_paradigm, "device_simulation": device_sim, "parity": parity,
         "e2e": {"value": eb_value, "unit": "updates/s", "h2d_bytes_per_step": eb_h2d,
                 "d2h_bytes_per_step": eb_d2h,
                 "api": "DeviceReplay.run (C-ABI ps_replay_run) with host buffers: the call "
                        "stream and the resident updates H2D, every decision and the final "
                        "weights D2H, per step"},
-        # the reference-compatible per-call path: every push's update H2D and
-        # every pull D2H, one host round trip per reference call
         "e2e_per_call": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
-                         "d2h_bytes_per_step": d2h,
+                         "d2h_bytes_per_step": d2h, "updates_per_step": e2e_updates,
                          "api": "ParameterServer drop-in (apply_gradient / decide_push / "
-                                "handle_pull), pinned host buffers",
-                         "updates_per_step": e2e_updates},
-        "gpu_launches": 2 * args.steps,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_sim (replay mode)",
-                     "bytes_model": "12 B/param per push-apply + 8 B/param per pull",
-                     "note": "C2's 1 MB of weights stay in registers and its updates in L2 for "
-                             "the whole stream (traffic = DRAM bytes per launch from ncu), so "
-                             "frac can exceed 1: the kernel is bound by the latency of the "
-                             "serial gate and per-call issue, not by HBM"},
-        "cpu_baseline": {"value": cpu_updates / cpu_s, "unit": "updates/s", "cores": 1,
-                         "kind": "port",
-                         "sample": f"first {cpu_updates} updates of the same C2 request stream, "
-                                   "oracle.RefPortServer (fp64 numpy + Python gate)",
-                         "host_cpus": os.cpu_count()},
-        "sweep": sweep,
-        "c4_throttled": c4,
-        "c4_free_running": c4_rt,
-        "torch_workers": tw,
-        "clocks": clocks,
+                                "handle_pull), pinned host buffers"},
+        "cpu_baseline": _run_cpu_child(["c2"]),
     }
-    print(json.dumps(line))
-    return 0
+    line["sweep_single_gpu"] = apply_sweep(torch, ps, hbm_peak)
+    line["c4_throttled"] = c4_throttled(torch, ps)
+    line["c4_free_running"] = c4_realtime(torch, ps)
+    line["torch_workers_c2"] = torch_workers(torch, ps)
 
 
 def main():
@@ -676,16 +710,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=("engine", "reference"))
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--cpu-updates", type=int, default=3000)
+    ap.add_argument("--cpu-sample", choices=("c2", "c3"), default=None)
+    ap.add_argument("--world", type=int, default=1)
+    ap.add_argument("--applies", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.cpu_sample:
+        return cpu_sample_main(args)
     if args.impl == "reference":
         return run_reference_arm(args)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
-        from paper_1908_11848_b200 import sharded
-        return sharded.bench_main(args, METRIC)
-    return bench_single(args)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    from paper_1908_11848_b200 import sharded
+    return sharded.bench_main(args, METRIC, extras=single_gpu_extras if world == 1 else None)
 
 
 if __name__ == "__main__":

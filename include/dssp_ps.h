@@ -21,6 +21,9 @@
  *   ps_apply_vectors    apply_update on plain vectors (stateless)          server.py:29-42
  *   ps_sim_run          Simulation.run event loop, device-resident          simnet.py:127-201
  *   ps_sim_trace        Simulation.entries (TraceEntry rows)               simnet.py:110-112, trace.py:28-37
+ *   ps_replay_run       the server answering a recorded handle_pull / apply_gradient /
+ *                       decide_push stream in one launch                   simnet.py:135-138, :183-201
+ *   ps_replay_read_replica  the snapshots those handle_pull calls returned  server.py:84-91
  *
  *   ps_shard_*          the same push/pull/gate over G GPUs (one process per
  *                       GPU, contiguous-range shards, P2P over NVLink)
@@ -200,6 +203,12 @@ typedef struct ps_replay_call {
 int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const float* synthetic,
                   int32_t n_synthetic, int32_t reset_gate, int32_t data_ctas, ps_sim_result* out);
 int ps_replay_decisions(ps_server* h, int64_t* out, int64_t cap, int64_t* n);
+/* The pulled weights a run left in worker p's replicas (handle_pull's
+ * snapshot, server.py:84-91): a replay writes pull k (k = 0, 1, ...) of
+ * worker p into buffer (k + 1) % 2, so the two buffers hold that worker's last two pulls;
+ * a simulation keeps its staging (PULL_ARRIVE) and active (PULL_RETURN)
+ * copies there. dst_host receives d fp32 values. */
+int ps_replay_read_replica(ps_server* h, int32_t worker, int32_t buf, float* dst_host);
 int ps_sim_trace(ps_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
 /* Loss samples of the last run: (version, 0.5*||w - c||^2 in fp64). */
 int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, int64_t* n);

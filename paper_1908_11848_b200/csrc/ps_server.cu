@@ -13,6 +13,7 @@
 // (handle_push, server.py:80-82) the same last CTA then runs the gate
 // decision, so apply + clock increment + decision is one launch.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -238,6 +239,20 @@ __global__ void k_load_in(const T* __restrict__ src, float* __restrict__ dst, lo
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     dst[i] = (float)src[i];
+}
+
+// apply_update on plain vectors (ps_apply_vectors): out = w - lr*g, any
+// non-finite result raises the flag word.
+__global__ void k_apply_vec(const float* __restrict__ w, const float* __restrict__ g,
+                            float* __restrict__ out, long long n, float lr, unsigned* flag) {
+  bool bad = false;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float r = apply1(w[i], lr, g[i]);
+    bad |= nonfinite(r);
+    out[i] = r;
+  }
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 __global__ void k_controller_batch(const double* tables, const int* r_max, int n, int* out) {
@@ -640,53 +655,94 @@ int ps_set_producer_stream(ps_server* h, void* cuda_stream) {
 int ps_controller_batch(int32_t device, const double* tables, const int32_t* r_max, int32_t n,
                         int32_t* out) {
   if (n <= 0) return PS_OK;
+  if (!tables || !r_max || !out) return ps_fail(nullptr, PS_E_VALUE, "null controller batch buffer");
   DevGuard guard(device);
   double* dt = nullptr;
   int* dr = nullptr;
   int* dout = nullptr;
-  cudaError_t e;
-  if ((e = cudaMalloc(&dt, sizeof(double) * 4 * n)) || (e = cudaMalloc(&dr, sizeof(int) * n)) ||
-      (e = cudaMalloc(&dout, sizeof(int) * n)))
-    return ps_cuda_fail(nullptr, e, "controller alloc");
-  cudaMemcpy(dt, tables, sizeof(double) * 4 * n, cudaMemcpyHostToDevice);
-  cudaMemcpy(dr, r_max, sizeof(int) * n, cudaMemcpyHostToDevice);
-  const int warps_per_block = 4;
-  k_controller_batch<<<(n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block>>>(dt, dr, n,
-                                                                                            dout);
-  e = cudaMemcpy(out, dout, sizeof(int) * n, cudaMemcpyDeviceToHost);
+  cudaStream_t st = nullptr;
+  const char* what = "controller batch";
+  // every step checked; every allocation freed on every path; a server-style
+  // non-blocking stream, not the legacy one
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (!e) { what = "controller alloc"; e = cudaMalloc(&dt, sizeof(double) * 4 * n); }
+  if (!e) e = cudaMalloc(&dr, sizeof(int) * n);
+  if (!e) e = cudaMalloc(&dout, sizeof(int) * n);
+  if (!e) { what = "controller input copy"; e = cudaMemcpyAsync(dt, tables, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, st); }
+  if (!e) e = cudaMemcpyAsync(dr, r_max, sizeof(int) * n, cudaMemcpyHostToDevice, st);
+  if (!e) {
+    what = "controller launch";
+    const int warps_per_block = 4;
+    k_controller_batch<<<(n + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
+        dt, dr, n, dout);
+    e = cudaGetLastError();
+  }
+  if (!e) { what = "controller result copy"; e = cudaMemcpyAsync(out, dout, sizeof(int) * n, cudaMemcpyDeviceToHost, st); }
+  if (!e) e = cudaStreamSynchronize(st);
   cudaFree(dt);
   cudaFree(dr);
   cudaFree(dout);
-  return e == cudaSuccess ? PS_OK : ps_cuda_fail(nullptr, e, "controller batch");
+  if (st) cudaStreamDestroy(st);
+  return e == cudaSuccess ? PS_OK : ps_cuda_fail(nullptr, e, what);
 }
 
 int ps_apply_vectors(int32_t device, const void* w, const void* g, int32_t dtype, int64_t n,
                      double lr, void* out, int32_t* status) {
   if (!(lr > 0)) return ps_fail(nullptr, PS_E_VALUE, "learning_rate must be > 0");
   if (n < 1) return ps_fail(nullptr, PS_E_VALUE, "dimension must be >= 1");
-  ps_config cfg{};
-  cfg.paradigm = PS_ASP;
-  cfg.worker_count = 1;
-  cfg.learning_rate = lr;
-  cfg.dimension = n;
-  cfg.device = device;
-  ps_server* h = nullptr;
-  int rc = ps_create(&cfg, w, dtype, &h);
-  if (rc) return rc;
-  int32_t applied = 0;
-  rc = ps_apply(h, 0, g, dtype, 0, &applied);
-  // apply_update (server.py:29-42) has no gradient check of its own: a
-  // non-finite gradient surfaces as a non-finite result.
-  const unsigned reject = (rc == PS_REJECTED);
-  *status = (rc == PS_E_DIVERGED || reject) ? PS_E_DIVERGED : rc;
-  if (rc == PS_OK) {
-    int64_t v = 0;
-    rc = ps_read_weights(h, out, dtype, 0, &v);
+  if (dtype != PS_F32 && dtype != PS_F64) return ps_fail(nullptr, PS_E_VALUE, "bad dtype");
+  if (!w || !g || !out || !status) return ps_fail(nullptr, PS_E_VALUE, "null buffer");
+  // Stateless: no server, control block or mapped mirror -- one stream, three
+  // stream-ordered scratch buffers, the rounding loads, one apply pass whose
+  // non-finite result flag comes back with the weights.
+  DevGuard guard(device);
+  const size_t esz = dtype == PS_F64 ? 8 : 4;
+  const long long dpad = (n + 3) / 4 * 4;
+  cudaStream_t st = nullptr;
+  void* raw = nullptr;   // host-dtype staging of w and g
+  float* f = nullptr;    // [w | g | out] fp32, each dpad long, + 1 flag word
+  const char* what = "apply_vectors";
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (!e) e = cudaMallocAsync(&raw, 2 * n * esz, st);
+  if (!e) e = cudaMallocAsync((void**)&f, (3 * dpad + 4) * sizeof(float), st);
+  if (!e) e = cudaMemsetAsync(f, 0, (3 * dpad + 4) * sizeof(float), st);
+  if (!e) { what = "apply_vectors upload"; e = cudaMemcpyAsync(raw, w, n * esz, cudaMemcpyHostToDevice, st); }
+  if (!e) e = cudaMemcpyAsync((char*)raw + n * esz, g, n * esz, cudaMemcpyHostToDevice, st);
+  unsigned flag = 0;
+  if (!e) {
+    what = "apply_vectors launch";
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 4096);
+    if (dtype == PS_F64) {
+      k_load_in<double><<<blocks, 256, 0, st>>>((const double*)raw, f, n);
+      k_load_in<double><<<blocks, 256, 0, st>>>((const double*)raw + n, f + dpad, n);
+    } else {
+      k_load_in<float><<<blocks, 256, 0, st>>>((const float*)raw, f, n);
+      k_load_in<float><<<blocks, 256, 0, st>>>((const float*)raw + n, f + dpad, n);
+    }
+    k_apply_vec<<<blocks, 256, 0, st>>>(f, f + dpad, f + 2 * dpad, n, (float)lr,
+                                        reinterpret_cast<unsigned*>(f + 3 * dpad));
+    e = cudaGetLastError();
   }
-  if (rc == PS_REJECTED || rc == PS_E_DIVERGED) rc = PS_OK;
-  if (rc != PS_OK) g_create_error = h->err;
-  ps_destroy(h);
-  return rc;
+  if (!e) {
+    what = "apply_vectors result copy";
+    e = cudaMemcpyAsync(&flag, f + 3 * dpad, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+  }
+  if (!e && dtype == PS_F32) e = cudaMemcpyAsync(out, f + 2 * dpad, n * 4, cudaMemcpyDeviceToHost, st);
+  if (!e && dtype == PS_F64) {
+    k_copy_out<double><<<(int)std::min<long long>((n / 4 + 255) / 256 + 1, 4096), 256, 0, st>>>(
+        f + 2 * dpad, (double*)raw, n);
+    e = cudaGetLastError();
+    if (!e) e = cudaMemcpyAsync(out, raw, n * 8, cudaMemcpyDeviceToHost, st);
+  }
+  if (!e) e = cudaStreamSynchronize(st);
+  if (raw) cudaFreeAsync(raw, st);
+  if (f) cudaFreeAsync(f, st);
+  if (st) { cudaStreamSynchronize(st); cudaStreamDestroy(st); }
+  if (e) return ps_cuda_fail(nullptr, e, what);
+  // apply_update (server.py:29-42) has no gradient check of its own: a
+  // non-finite gradient surfaces as a non-finite result (DivergenceError)
+  *status = flag ? PS_E_DIVERGED : PS_OK;
+  return PS_OK;
 }
 
 }  // extern "C"

@@ -2016,6 +2016,16 @@ int ps_replay_decisions(ps_server* h, int64_t* out, int64_t cap, int64_t* n) {
   return PS_OK;
 }
 
+int ps_replay_read_replica(ps_server* h, int32_t worker, int32_t buf, float* dst_host) {
+  DevGuard guard(h->dev);
+  if (!h->sim.rep || worker < 0 || worker >= h->sim.P || buf < 0 || buf > 1 || !dst_host)
+    return ps_fail(h, PS_E_VALUE, "no such replica (run a replay or simulation first)");
+  const float* src = h->sim.rep + ((size_t)worker * 2 + buf) * h->dpad;
+  PS_CK(h, cudaMemcpyAsync(dst_host, src, h->d * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  return PS_OK;
+}
+
 int ps_sim_trace(ps_server* h, ps_trace_row* rows, int64_t cap, int64_t* n) {
   DevGuard guard(h->dev);
   const int64_t m = h->sim.last_trace_rows < cap ? h->sim.last_trace_rows : cap;

@@ -382,13 +382,76 @@ def torch_workers_bench(world, rank, local, warm, steps, batch=128):
     return out
 
 
-def bench_main(args, metric):
+class NvlinkCounters:
+    """NVLink data counters of one GPU (NVML field values, KiB per link,
+    summed over links), read before and after a timed region: the bytes the
+    GPU actually sent and received over NVLink there. Diagnostics only; any
+    NVML failure leaves the figures None."""
+
+    FIELDS = {"data_tx_kib": 138, "data_rx_kib": 139}  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(int(index))
+            self.links = 18
+            self.ok = self.read() is not None
+        except Exception:
+            self.ok = False
+
+    def read(self):
+        try:
+            req = [(fid, link) for fid in self.FIELDS.values() for link in range(self.links)]
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, req)
+            out = dict.fromkeys(self.FIELDS, 0)
+            seen = False
+            for (fid, _link), v in zip(req, vals):
+                if v.nvmlReturn != 0:
+                    continue
+                seen = True
+                name = next(k for k, f in self.FIELDS.items() if f == fid)
+                out[name] += int(v.value.ullVal)
+            return out if seen else None
+        except Exception:
+            return None
+
+
+def _fp32_checksums(arr):
+    """Order-independent bit-exact fingerprint of an fp32 vector: (xor, sum)
+    of its bit patterns -- the shard/replica parity figure of the bench."""
+    u = np.ascontiguousarray(arr, dtype=np.float32).view(np.uint32)
+    return [int(np.bitwise_xor.reduce(u)) if u.size else 0, int(u.astype(np.uint64).sum())]
+
+
+def host_update(d, rank, seed=0):
+    """The bench's synthetic update of worker `rank`: N(0,1) fp32 from
+    PCG64(seed * 1000 + rank), drawn on the host."""
+    rng = np.random.Generator(np.random.PCG64(seed * 1000 + rank))
+    return rng.standard_normal(d, dtype=np.float32)
+
+
+def bench_main(args, metric, extras=None):
+    """The headline at every N (BASELINE configs[2], "C3"): d = 23,528,522
+    fp32 sharded over the N GPUs, one homogeneous worker per GPU, all four
+    paradigms (N = 1 is the same server at G = 1). One step = one push group:
+    every worker pushes, each owner applies the N updates in ticket order,
+    the replicated gate decides, every worker pulls. Weak scaling: every GPU
+    owns d/N parameters and applies N updates to them per step (d element
+    updates per GPU per step at every N). `extras(torch, ps, line)` adds the
+    single-GPU blocks at N = 1 (rank 0)."""
     import torch
     import torch.distributed as dist
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(29650 + os.getpid() % 500))
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
     torch.cuda.set_device(local)
     if not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -400,24 +463,31 @@ def bench_main(args, metric):
                                   .astype(np.float32)))
     dist.broadcast(w0, 0)
     steps, warm = args.steps, args.warmup
-    times = homogeneous_push_times(1.0, 0.05, warm + steps + 64)
+    e2e_steps = max(3, min(steps, 10))
+    times = homogeneous_push_times(1.0, 0.05, warm + steps + e2e_steps + 1)
     S_lo, S_hi = shard_range(d, world, rank)
-    results = {}
+    upd_host = torch.from_numpy(host_update(d, rank)).pin_memory()
+    results, parity = {}, {}
     sampler = None
     if rank == 0:
         from bench import ClockSampler
         sampler = ClockSampler(local)
         sampler.__enter__()
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(1000 * 0 + rank)
+    nvl = NvlinkCounters(local) if world > 1 else None
+    nvl_delta = None
     for name, s, r in PARADIGMS:
         cfg = c3_config(name, s, r, world)
         srv = ShardedServer(cfg, d, rank, world, local, w0_device=w0)
-        srv.update[:d].normal_(generator=gen)
+        srv.update[:d].copy_(upd_host)
         srv.run(times[:warm])
         dist.barrier()
         torch.cuda.synchronize()
+        c0 = nvl.read() if (nvl is not None and nvl.ok and name == "dssp") else None
         ms = srv.run(times[warm:warm + steps])
+        if c0 is not None:
+            c1 = nvl.read()
+            if c1 is not None:
+                nvl_delta = {k: (c1[k] - c0[k]) * 1024 / steps for k in c0}
         ms_max = max_over_ranks(ms)
         entries = srv.trace()
         decisions = [e.decision for e in entries]
@@ -425,73 +495,140 @@ def bench_main(args, metric):
                          "iters_per_s": steps * world / (ms_max * 1e-3),
                          "ms_per_step": ms_max / steps,
                          "defers": sum(1 for x in decisions if x == "defer")}
-        dist.barrier()
+        # parity: decisions of every step against the reference simulator's
+        # trace of this schedule (tests/golden/c3_schedule.json.gz) ...
+        want = _c3_reference_decisions(name, world)
+        got = [e.render().split("\t") for e in entries][:len(want)]
+        parity.setdefault("decisions_identical_to_reference", {})[name] = (
+            len(got) == min(len(want), (warm + steps) * world) and got == want[:len(got)])
         if name == "dssp":
+            # ... and the weights: every rank's shard and replica fingerprint
+            # against the fp32 replay of the same (warm + steps) x N applies
+            sums = {"shard": _fp32_checksums(srv.read_shard()),
+                    "replica": _fp32_checksums(srv.read_replica()), "lo": S_lo, "hi": S_hi}
+            everyone = [None] * world
+            dist.all_gather_object(everyone, sums)
+            parity["_weights_applies"] = (warm + steps) * world
+            parity["_rank_sums"] = everyone
             # e2e: the same step through the public API with the worker's
             # update arriving from pinned host memory (H2D, 94 MB) and the
-            # step's result -- the gate's decisions and version, i.e. the
-            # state the host reads back -- leaving to the host (D2H). The
-            # pulled weights stay where the worker computes: in this GPU's
-            # replica (a host-resident worker would add one D2H of 4*d bytes).
-            host_upd = srv.update[:d].cpu().pin_memory()
-            e2e_steps = max(3, min(steps, 10))
+            # step's result -- the gate's decisions and version -- leaving
+            # to the host (D2H); the pulled weights stay in this GPU's replica
             dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             base = warm + steps
-            granted = 0
             for i in range(e2e_steps):
-                srv.update[:d].copy_(host_upd, non_blocking=True)
+                srv.update[:d].copy_(upd_host, non_blocking=True)
                 srv.run(times[base + i:base + i + 1])
-                st = srv.state()
-                granted += int(st.decisions)
+                srv.state()
             torch.cuda.synchronize()
             e2e_s = time.perf_counter() - t0
             results["_e2e"] = {"value": e2e_steps * world / max_over_ranks(e2e_s), "unit": "updates/s",
                                "h2d_bytes_per_step": 4 * d,
                                "d2h_bytes_per_step": ctypes.sizeof(_lib.PSGateState),
-                               "api": "ShardedServer.run with the update from pinned host memory; "
-                                      "gate state (decisions, version) read back per step"}
+                               "api": "ShardedServer.run (C-ABI ps_shard_run) with the update from "
+                                      "pinned host memory; gate state read back per step",
+                               "steps": e2e_steps}
         torch.cuda.synchronize()
         dist.barrier()  # no peer may still be reading this rank's memory
         srv.close()
-    sweep = bandwidth_sweep(world, rank, local, warm, steps) if not getattr(args, "no_sweep", False) else []
-    tw = (torch_workers_bench(world, rank, local, max(warm, 5), min(steps, 10))
-          if not getattr(args, "no_sweep", False) else None)
-    c4 = throttled_bench(world, rank, local) if not getattr(args, "no_sweep", False) else None
-    if sampler is not None:
-        sampler.__exit__(None, None, None)
+    del w0
+    torch.cuda.empty_cache()
+    full = not getattr(args, "no_sweep", False)
+    sweep = bandwidth_sweep(world, rank, local, warm, steps) if (full and world > 1) else None
+    tw = torch_workers_bench(world, rank, local, max(warm, 5), min(steps, 10)) if full else None
+    c4 = throttled_bench(world, rank, local) if (full and world > 1) else None
+    line = None
     if rank == 0:
         head = results["dssp"]
         S = S_hi - S_lo
-        nv_bytes = 2 * (world - 1) * S * 4          # push slices in + pull shards in, per GPU
-        achieved = nv_bytes / (head["ms_per_step"] * 1e-3) / 1e9
         line = {
             "metric": metric, "value": head["updates_per_s"], "unit": "updates/s",
             "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": "C3 (BASELINE configs[2]): ResNet-50-sized server d=23528522 fp32 "
-                                   f"sharded {world} ways, {world} homogeneous workers (one per GPU), "
+                                   f"sharded {world} way(s), {world} homogeneous worker(s), one per GPU, "
                                    "DSSP(3,12); step = one push group (every worker pushes, owners "
                                    "apply in ticket order, gate decides) + every worker's pull",
-                       "d": d, "workers": world, "parallelism": f"sharded server x{world}, P2P NVLink",
-                       "l2": "per-GPU working set > L2 (94 MB update + 94 MB replica + shard)"},
+                       "d": d, "workers": world, "paradigm": "dssp", "s_lower": 3, "r_max": 12,
+                       "parallelism": f"sharded server x{world}" + (", P2P NVLink" if world > 1 else ""),
+                       "l2": "inputs larger than L2: per GPU the 94 MB update, the 94 MB replica "
+                             "and the double-buffered shard are touched every step"},
             "per_paradigm": {k: v for k, v in results.items() if not k.startswith("_")},
+            "parity": parity,
             "e2e": results["_e2e"],
             "gpu_launches": 1,  # one persistent k_shard_run covers all K timed steps
-            "roofline": {"bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s",
-                         "frac": achieved / 770.0, "traffic": None,
-                         "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                         "kernel": "k_shard_run (persistent; whole step: push, apply, pull, verdict, gate)",
-                         "bytes_model": "2*(G-1)*S*4 B received over NVLink per GPU per step"},
-            "cpu_baseline": None,
-            "sweep": sweep,
-            "torch_workers": tw,
-            "c4_throttled_sharded": c4,
-            "clocks": sampler.summary() if sampler else None,
         }
+        if world == 1:
+            alg = 16 * d  # read w, read update, write w, write the replica (the pull)
+            achieved = alg / (head["ms_per_step"] * 1e-3) / 1e9
+            from bench import peaks, shard_traffic
+            hbm_peak, peak_kind = peaks()
+            line["roofline"] = {
+                "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "frac_vs_8000": achieved / 8000.0,
+                "traffic": shard_traffic(), "peak_kind": peak_kind,
+                "kernel": "k_shard_run (persistent; whole step: apply, pull, verdict, gate)",
+                "bytes_model": "16 B/param per step: read shard 4 + read update 4 + write shard 4 "
+                               "+ write replica 4 (the pull, fused into the apply pass)"}
+        else:
+            nv_bytes = 2 * (world - 1) * S * 4          # push slices in + pull shards in, per GPU
+            achieved = nv_bytes / (head["ms_per_step"] * 1e-3) / 1e9
+            line["roofline"] = {
+                "bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s",
+                "frac": achieved / 770.0, "frac_vs_900": achieved / 900.0,
+                "traffic": (nvl_delta or {}).get("data_rx_kib"),
+                "traffic_counters": nvl_delta,
+                "traffic_note": "NVML NVLink data counters of rank 0's GPU around the timed DSSP "
+                                "run, bytes per step (rx = what this GPU received)",
+                "peak_kind": "measured peer copy per direction (B200_PROFILING.md); frac_vs_900 "
+                             "against the NVLink 5 spec",
+                "kernel": "k_shard_run (persistent; whole step: push, apply, pull, verdict, gate)",
+                "bytes_model": "2*(G-1)*S*4 B received over NVLink per GPU per step"}
+        line["sweep"] = sweep
+        line["torch_workers"] = tw
+        if c4 is not None:
+            line["c4_throttled_sharded"] = c4
+    dist.barrier()
+    if rank == 0:
+        # the reference's CPU implementation on a bounded sample of this same
+        # workload, pinned to one host core, plus the fp32 replay fingerprints
+        # of the weights (a separate process: the checker, not the product)
+        from bench import cpu_baseline_c3
+        base = cpu_baseline_c3(world, parity["_weights_applies"])
+        line["cpu_baseline"] = base["cpu_baseline"]
+        want = base["fingerprints"]
+        ok_shard = all(rs["shard"] == [want["shards"][i][0], want["shards"][i][1]]
+                       for i, rs in enumerate(parity["_rank_sums"]))
+        ok_rep = all(rs["replica"] == want["replica"] for rs in parity["_rank_sums"])
+        parity["weights_bit_exact_vs_fp32_replay"] = {"shards": ok_shard, "replicas": ok_rep,
+                                                     "applies": parity["_weights_applies"]}
+        parity.pop("_rank_sums")
+        parity.pop("_weights_applies")
+        if extras is not None:
+            import paper_1908_11848_b200 as ps
+            extras(torch, ps, line)
+        if sampler is not None:
+            sampler.__exit__(None, None, None)
+            line["clocks"] = sampler.summary()
         print(json.dumps(line))
     dist.barrier()
     dist.destroy_process_group()
     return 0
+
+
+def _c3_reference_decisions(paradigm, world):
+    """Push rows of the reference simulator's trace of the C3 schedule
+    (tests/golden/c3_schedule.json.gz; recorded by make_golden.py), or [] if
+    the fixture has no run for this worker count."""
+    import gzip
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                        "c3_schedule.json.gz")
+    with gzip.open(path, "rt") as fh:
+        runs = json.load(fh)["runs"]
+    for r in runs:
+        if r["name"] == f"c3_{paradigm}_p{world}":
+            return [ln.split("\t") for ln in r["trace"].splitlines() if ln.split("\t")[2] == "push_arrive"]
+    return []

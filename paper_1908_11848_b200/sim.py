@@ -46,6 +46,26 @@ class DeviceRunReport:
         return self.applied / (self.device_ms * 1e-3) if self.device_ms > 0 else 0.0
 
 
+def check_synthetic(tensor, workers, count, dimension, device):
+    """The C-ABI takes the resident updates as a bare pointer with no length:
+    enforce the layout its float4 loads assume ([P, count, round_up(d,4)]
+    contiguous fp32 on the engine's device, 16-byte aligned)."""
+    import torch
+    if not isinstance(tensor, torch.Tensor) or not tensor.is_cuda:
+        raise ValueError("resident updates must be a CUDA tensor")
+    if tensor.dtype != torch.float32:
+        raise ValueError(f"resident updates must be float32, got {tensor.dtype}")
+    if tensor.device.index != int(device):
+        raise ValueError(f"resident updates live on cuda:{tensor.device.index}, the engine on cuda:{device}")
+    want = (int(workers), int(count), (int(dimension) + 3) // 4 * 4)
+    if tuple(tensor.shape) != want:
+        raise ValueError(f"resident updates must have shape {want}, got {tuple(tensor.shape)}")
+    if not tensor.is_contiguous() or tensor.data_ptr() % 16:
+        raise ValueError("resident updates must be contiguous and 16-byte aligned")
+    if int(count) < 1:
+        raise ValueError("at least one resident update per worker")
+
+
 class DeviceSimulation:
     """Owns one engine and runs simulated schedules on it."""
 
@@ -70,6 +90,7 @@ class DeviceSimulation:
 
     def set_synthetic(self, tensor, count):
         """Resident updates: a CUDA fp32 tensor [P, count, round_up(d, 4)]."""
+        check_synthetic(tensor, self.config.worker_count, count, self.dimension, self.engine.device)
         self._synthetic = tensor
         self._synth_count = int(count)
 
@@ -206,6 +227,7 @@ class DeviceReplay:
             else:
                 arr[i] = (float(c[2]), CALL_DECIDE, c[1])
         self.calls = arr
+        check_synthetic(synthetic, engine.worker_count, count, engine.dimension, engine.device)
         self.synthetic = synthetic
         self.count = int(count)
 
@@ -229,6 +251,19 @@ class DeviceReplay:
         self.engine.refresh(sync=False)  # the run already mirrored the control block
         return ReplayReport(raw=raw, applied=res.applied, rejected=res.rejected,
                             pushes=res.pushes, device_ms=res.device_ms)
+
+    def replica(self, worker, buf):
+        """The weights pull k of `worker` materialized, for (k + 1) % 2 == buf."""
+        return read_replica(self.engine, worker, buf)
+
+
+def read_replica(engine, worker, buf):
+    """Worker `worker`'s replica buffer `buf` after a run (d fp32 values): in a
+    replay, pull k (k = 0, 1, ...) of that worker landed in buffer (k + 1) % 2."""
+    out = np.empty(engine.dimension, dtype=np.float32)
+    engine.check(engine.lib.ps_replay_read_replica(engine.handle, int(worker), int(buf),
+                                                   out.ctypes.data))
+    return out
 
 
 def calls_from_trace(entries):

@@ -38,10 +38,14 @@ def main(out_dir):
             if r["config"].get("timing_preset") != "homogeneous"
             and r["normalized"]["worker_count"] == world
             and r["config"].get("model_kind") == "quadratic_bowl"]
+    # BASELINE configs[3]: the reference's runs with 1x/2x/4x throttled workers
+    runs += [r for r in oracle.load_golden("sim_throttle.json.gz")["runs"]
+             if r["normalized"]["worker_count"] == world]
     checks = []
     for d in (5, 100_003):
         for run in runs:
-            cfg = ps.validate_config(ps.make_config(**run["config"]))
+            cfg = ps.validate_config(ps.make_config(**run["config"],
+                                                    throttle=tuple(run.get("throttle", ()))))
             entries = _entries(run["trace"])
             groups = groups_from_trace(entries)
             w0 = oracle.initial_weights_f64(cfg.seed, d)

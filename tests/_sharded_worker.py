@@ -38,8 +38,12 @@ def main(out_dir):
     only = os.environ.get("PS_TEST_ONLY_RUN")  # diagnosis: one run, one size
     if only:
         runs = [r for r in runs if r["name"] == only]
-    for d in ((100_003,) if only else (5, 100_003)):
-        for run in runs:
+    # C3 at full size (BASELINE configs[2]: d = 23,528,522, the bench's shard
+    # size, CTA-count trim and redo geometry) on the first homogeneous run
+    from paper_1908_11848_b200.sharded import C3_DIM
+    sizes = (100_003,) if only else (5, 100_003, C3_DIM)
+    for d in sizes:
+        for run in (runs[:1] if d == C3_DIM else runs):
             cfg = ps.validate_config(ps.make_config(**run["config"]))
             rows = [line.split("\t") for line in run["trace"].splitlines()]
             pushes = [r for r in rows if r[2] == "push_arrive"]

@@ -22,6 +22,11 @@ Fixtures written (all deterministic; re-running reproduces them byte for byte):
                            and the fp64 final weights for the small models.
   apply_vectors.json       apply_update / apply_gradient known answers
                            (stalesync/server.py:29-69, tests/test_server.py).
+  c3_schedule.json.gz      run_simulation traces of the bench's homogeneous
+                           sharded workload (P = 1, 2, 4, 8, every paradigm).
+  sim_throttle.json.gz     run_simulation with 1x/2x/4x throttled workers
+                           (BASELINE configs[3]) through a TimingModel
+                           subclass (ThrottledTimingModel below).
 """
 
 from __future__ import annotations
@@ -40,7 +45,7 @@ from stalesync.config import GradientVector, WeightVector, make_config, validate
 from stalesync.policy import (IterationClockTable, ProtocolError, PushHistoryTable,
                               SyncPolicy, synchronization_controller)
 from stalesync.server import DivergenceError, ParameterServer, apply_update, initial_weights
-from stalesync.simnet import Simulation
+from stalesync.simnet import Simulation, TimingModel
 from stalesync.trace import format_trace
 
 
@@ -254,9 +259,24 @@ class _Recorder:
             state.adopt = adopt
 
 
-def _run_recorded(flat, keep_weights):
+class ThrottledTimingModel(TimingModel):
+    """BASELINE configs[3]'s heterogeneous cluster: worker w's compute base is
+    multiplied by throttle[w % len(throttle)] (1x / 2x / 4x). The reference
+    has no such preset (simnet.py:34-69); this subclass adds one without
+    touching the reference: the presets' per-worker bases are scaled after
+    construction, and every draw (constant, jitter, lognormal) then uses the
+    scaled base exactly as TimingModel.compute_time does."""
+
+    def __init__(self, spec, worker_count, seed, throttle):
+        super().__init__(spec, worker_count, seed)
+        self._bases = [b * float(throttle[w % len(throttle)]) for w, b in enumerate(self._bases)]
+
+
+def _run_recorded(flat, keep_weights, throttle=None):
     cfg = validate_config(make_config(**flat))
     sim = Simulation(cfg)
+    if throttle:
+        sim.timing = ThrottledTimingModel(cfg.timing_model, cfg.worker_count, cfg.seed, throttle)
     rec = _Recorder(sim)
     entries, report = sim.run()
     out = {
@@ -274,6 +294,8 @@ def _run_recorded(flat, keep_weights):
         "per_worker": {str(w): [m.iterations, m.epochs, m.wait_s, m.compute_s, m.comm_s]
                        for w, m in report.per_worker.items()},
     }
+    if throttle:
+        out["throttle"] = list(throttle)
     if keep_weights:
         out["final_weights"] = [float(x) for x in sim.server.weights.values]
         out["loss_curve"] = [[int(v), float(l)] for v, l in report.loss_curve]
@@ -397,6 +419,59 @@ def c2_schedule():
     _dump("c2_schedule.json.gz", {"runs": out}, gz=True)
 
 
+def c3_schedule():
+    """bench.py's headline workload (BASELINE configs[2], "C3"): P homogeneous
+    workers, one per GPU, for P = 1, 2, 4, 8 and every paradigm, 96 pushes
+    per worker. The schedule (push instants, ticket order, decisions) does
+    not depend on the parameter count, so these traces pin the sharded
+    server's decisions at d = 23,528,522 too."""
+    out = []
+    for workers in (1, 2, 4, 8):
+        for paradigm, s, r in (("dssp", 3, 12), ("ssp", 3, 0), ("bsp", 0, 0), ("asp", 0, 0)):
+            flat = dict(paradigm=paradigm, worker_count=workers, s_lower=s, r_max=r,
+                        timing_preset="homogeneous", compute_base=1.0, comm_delay=0.05,
+                        model_kind="quadratic_bowl", dimension=2, dataset_size=96 * workers,
+                        batch_size=1, learning_rate=0.05, epochs=1, seed=0, loss_every=100000)
+            rec = _run_recorded(flat, False)
+            rec["name"] = f"c3_{paradigm}_p{workers}"
+            rec.pop("calls")
+            out.append(rec)
+    _dump("c3_schedule.json.gz", {"runs": out}, gz=True)
+
+
+def sim_throttle():
+    """BASELINE configs[3]: workers throttled 1x / 2x / 4x (ThrottledTimingModel),
+    every paradigm. The bench's C4 schedule (P = 3, tiny_mlp-shaped budget),
+    closed-loop quadratic-bowl runs with final weights at P = 3, 4 and 8
+    (throttle cycling over the workers), and the seed-dependent presets
+    (jitter, lognormal) under the same multipliers."""
+    runs = []
+    paradigms = (("dssp", 3, 12), ("ssp", 3, 0), ("bsp", 0, 0), ("asp", 0, 0))
+    for paradigm, s, r in paradigms:
+        runs.append((f"c4_{paradigm}", dict(
+            paradigm=paradigm, worker_count=3, s_lower=s, r_max=r, timing_preset="homogeneous",
+            compute_base=1.0, comm_delay=0.05, model_kind="tiny_mlp", dimension=3072,
+            dataset_size=3 * 1600, batch_size=16, learning_rate=0.05, epochs=1, seed=0,
+            loss_every=100000), False, (1, 2, 4)))
+    k = 0
+    for workers in (2, 3, 4, 8):
+        for paradigm, s, r in paradigms + (("dssp", 1, 4),):
+            preset = ("homogeneous", "jitter", "lognormal")[k % 3]
+            runs.append((f"throttle_{paradigm}{s}_{r}_{preset}_p{workers}", dict(
+                paradigm=paradigm, worker_count=workers, s_lower=s, r_max=r,
+                timing_preset=preset, compute_base=1.0, comm_delay=(0.05, 0.01, 0.0)[k % 3],
+                model_kind="quadratic_bowl", dimension=(64, 257, 1024)[k % 3],
+                dataset_size=16 * workers * 3, batch_size=4, learning_rate=0.05,
+                epochs=(2, 3, 2)[k % 3], seed=k + 11), True, (1, 2, 4)))
+            k += 1
+    out = []
+    for name, flat, keep, throttle in runs:
+        rec = _run_recorded(flat, keep, throttle)
+        rec["name"] = name
+        out.append(rec)
+    _dump("sim_throttle.json.gz", {"runs": out}, gz=True)
+
+
 def sim_large():
     """Worker counts beyond the main corpus: P = 1 (serial SGD), and the
     lane-per-worker (9..32) and shared-memory (33..64) control-warp layouts
@@ -422,7 +497,11 @@ def sim_large():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2", "large"]
+    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2", "large", "throttle", "c3"]
+    if "throttle" in which:
+        sim_throttle()
+    if "c3" in which:
+        c3_schedule()
     if "large" in which:
         sim_large()
     if "c2" in which:

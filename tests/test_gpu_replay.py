@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 ps = pytest.importorskip("paper_1908_11848_b200")
 from paper_1908_11848_b200.engine import Engine  # noqa: E402
-from paper_1908_11848_b200.sim import DeviceReplay  # noqa: E402
+from paper_1908_11848_b200.sim import DeviceReplay, read_replica  # noqa: E402
 
 
 def _runs():
@@ -42,15 +42,12 @@ def test_replay_decisions_and_weights(d):
         rep = DeviceReplay(eng, calls, torch.from_numpy(synth).cuda(), K).run()
         want = [(c[3], tuple(c[4])) for c in run["calls"] if c[0] == "decide"]
         assert rep.decisions == want, run["name"]
-        w = oracle.initial_weights_f64(seed, d).astype(np.float32)
-        seen = {}
-        for c in calls:
-            if c[0] == "apply":
-                k = seen.get(c[1], 0)
-                seen[c[1]] = k + 1
-                w = oracle.apply_f32(w, synth[c[1], k % K, :d], norm["learning_rate"])
+        pulls = {}
+        w, _, _ = _fp32_replay(calls, synth, d, norm["learning_rate"], seed=seed, pulls=pulls)
         got, _ = eng.read()
         assert np.array_equal(got.view(np.uint32), w.view(np.uint32)), run["name"]
+        # every worker's last two pulls (pull k in replica buffer (k + 1) % 2), bit for bit
+        _check_replicas(eng, pulls)
         eng.close()
 
 
@@ -62,12 +59,19 @@ def test_replay_rejects_protocol_violation():
         DeviceReplay(eng, calls, synth, 1).run()
 
 
-def _fp32_replay(calls, synth, d, lr, seed=0, reject=lambda p, k: False):
+def _fp32_replay(calls, synth, d, lr, seed=0, reject=lambda p, k: False, pulls=None):
+    """fp32 oracle of a replayed stream. With `pulls` (a dict) it also records,
+    per worker, the snapshot of each of its pulls under key (worker, (k + 1) % 2):
+    what that worker's replica buffer must hold after the run."""
     w = oracle.initial_weights_f64(seed, d).astype(np.float32)
-    seen = {}
+    seen, npull = {}, {}
     applied = rejected = 0
     K = synth.shape[1]
     for c in calls:
+        if c[0] == "pull" and pulls is not None:
+            k = npull.get(c[1], 0)
+            npull[c[1]] = k + 1
+            pulls[(c[1], (k + 1) % 2)] = w
         if c[0] == "apply":
             k = seen.get(c[1], 0)
             seen[c[1]] = k + 1
@@ -77,6 +81,14 @@ def _fp32_replay(calls, synth, d, lr, seed=0, reject=lambda p, k: False):
             w = oracle.apply_f32(w, synth[c[1], k % K, :d], lr)
             applied += 1
     return w, applied, rejected
+
+
+def _check_replicas(eng, pulls):
+    assert pulls
+    for (p, buf), snap in sorted(pulls.items()):
+        got = read_replica(eng, p, buf)
+        bad = np.flatnonzero(got.view(np.uint32) != snap.view(np.uint32))
+        assert bad.size == 0, (p, buf, bad[:8])
 
 
 def test_replay_stops_data_exactly_at_a_protocol_error():
@@ -128,11 +140,16 @@ def test_replay_rejects_nonfinite_updates_per_call(d):
     eng = Engine(norm["paradigm"], P, norm["s_lower"], norm["r_max"], norm["learning_rate"], d,
                  w0=oracle.initial_weights_f64(0, d))
     rep = DeviceReplay(eng, calls, torch.from_numpy(synth).cuda(), K).run()
+    pulls = {}
     want, applied, rejected = _fp32_replay(calls, synth, d, norm["learning_rate"],
-                                           reject=lambda p, k: p == 1 and k == 0)
+                                           reject=lambda p, k: p == 1 and k == 0, pulls=pulls)
     assert rep.rejected == rejected > 0 and rep.applied == applied
     got, _ = eng.read()
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    # pull contents: every worker's last two snapshots, bit for bit -- including
+    # the pulls the speculative data warps re-executed after rolling back a
+    # rejected update (server.py:65-67, :84-91)
+    _check_replicas(eng, pulls)
     # decisions do not depend on the data
     assert rep.decisions == [(c[3], tuple(c[4])) for c in run["calls"] if c[0] == "decide"]
     eng.close()

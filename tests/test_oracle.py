@@ -50,7 +50,7 @@ def test_gate_protocol_errors(gate_cls):
         gate_cls("ssp", 2, 1, 0).on_push(5, 0.0)
 
 
-@pytest.mark.parametrize("fixture", ["sim_corpus.json.gz", "sim_large.json.gz"])
+@pytest.mark.parametrize("fixture", ["sim_corpus.json.gz", "sim_large.json.gz", "sim_throttle.json.gz"])
 def test_gate_replays_simulator_decisions(fixture):
     corpus = oracle.load_golden(fixture)
     for run in corpus["runs"]:
@@ -86,7 +86,7 @@ def test_apply_f32_c_matches_numpy_bitwise():
     assert np.array_equal(out.view(np.uint32), oracle.apply_f32(w, g, 0.05).view(np.uint32))
 
 
-@pytest.mark.parametrize("fixture", ["sim_corpus.json.gz", "sim_large.json.gz"])
+@pytest.mark.parametrize("fixture", ["sim_corpus.json.gz", "sim_large.json.gz", "sim_throttle.json.gz"])
 def test_bowl_replay_reproduces_reference_fp64(fixture):
     corpus = oracle.load_golden(fixture)
     checked = 0
@@ -101,4 +101,26 @@ def test_bowl_replay_reproduces_reference_fp64(fixture):
         err = np.max(np.abs(w32 - ref)) / max(np.max(np.abs(ref)), 1.0)
         assert err <= 1e-5, (run["name"], err)
         checked += 1
-    assert checked >= (80 if fixture == "sim_corpus.json.gz" else 16)
+    assert checked >= {"sim_corpus.json.gz": 80, "sim_large.json.gz": 16}.get(fixture, 15)
+
+
+def test_throttled_schedule_matches_config_compute_times():
+    """The host schedule generator (config.compute_time_table) reproduces the
+    reference's throttled compute draws: every compute_done - pull_return gap
+    in the reference traces equals the table entry (constant, jitter and
+    lognormal presets scaled 1x/2x/4x)."""
+    import paper_1908_11848_b200 as ps
+    from paper_1908_11848_b200.config import compute_time_table, push_budget
+    for run in oracle.load_golden("sim_throttle.json.gz")["runs"]:
+        cfg = ps.validate_config(ps.make_config(**run["config"], throttle=tuple(run["throttle"])))
+        table = compute_time_table(cfg, push_budget(cfg))
+        last, k = {}, {}
+        for line in run["trace"].splitlines()[1:]:
+            t, w, kind = line.split("\t")[:3]
+            t, w = float(t), int(w)
+            if kind == "pull_return":
+                last[w] = t
+            elif kind == "compute_done":
+                i = k.get(w, 0)
+                k[w] = i + 1
+                assert abs((t - last[w]) - table[w][i]) <= 1e-9 * max(1.0, t), (run["name"], w, i)
