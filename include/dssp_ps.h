@@ -24,6 +24,8 @@
  *   ps_replay_run       the server answering a recorded handle_pull / apply_gradient /
  *                       decide_push stream in one launch                   simnet.py:135-138, :183-201
  *   ps_replay_read_replica  the snapshots those handle_pull calls returned  server.py:84-91
+ *   ps_workers_* / ps_bind_worker_stream / ps_enqueue_iteration
+ *                       ThreadedRun worker loop, lock and release events  runner.py:168-291
  *
  *   ps_shard_*          the same push/pull/gate over G GPUs (one process per
  *                       GPU, contiguous-range shards, P2P over NVLink)
@@ -226,6 +228,75 @@ int ps_set_profiling(ps_server* h, int32_t on);
  * is stream-ordered after the work already enqueued there (an event edge, no
  * host synchronization). */
 int ps_set_producer_stream(ps_server* h, void* cuda_stream);
+
+/* ------------------------------------------------------------------------
+ * Free-running workers on device flags (the threaded runner without the host:
+ * runner.py:168-291). Every worker is a CUDA stream; an iteration is the
+ * worker's own forward/backward, then ps_enqueue_iteration's three stream
+ * items: a push kernel (ticket, apply in ticket order, gate decision at the
+ * device clock -- apply_gradient -> decide_push under the runner's lock,
+ * runner.py:226-249 -- and the go flags of the granted / released workers,
+ * policy.py:197-206), a stream memory wait on the worker's go flag (a
+ * deferred worker's stream blocks there, runner.py:255-263, occupying no SM
+ * and no host thread), and a pull kernel (ticket, the weights into the bound
+ * parameter buffer, runner.py:273-284). All state is device-resident and per
+ * worker, so the iteration can be captured once in a CUDA graph and replayed
+ * with no host work. The per-op calls above must not be used while workers
+ * run. Streams that wait must not share a hardware queue with streams they
+ * wait for: raise CUDA_DEVICE_MAX_CONNECTIONS (e.g. 32) before CUDA starts.
+ * ---------------------------------------------------------------------- */
+typedef struct ps_workers_report {
+  int64_t tickets;             /* pushes + pulls served */
+  int64_t decisions;           /* pushes decided */
+  int64_t pulls;
+  uint64_t go_mask;            /* workers currently allowed past their wait */
+  int32_t status;              /* PS_OK, PS_E_DIVERGED, PS_E_PROTOCOL, PS_E_TIMEOUT */
+  int32_t diverged_worker;
+  int32_t aborted;
+  int32_t _pad;
+} ps_workers_report;
+
+typedef struct ps_worker_decision {   /* one decided push, in ticket order */
+  uint64_t ticket;
+  double now;                  /* gate seconds since ps_workers_start (device clock x scale) */
+  int32_t worker;
+  int32_t outcome;             /* 0 grant, 1 defer */
+  uint64_t released;           /* bit q: worker q released by this grant */
+  int64_t version;             /* weights version after this push */
+  int32_t applied;             /* 0: non-finite update, rejected (server.py:65-67) */
+  int32_t _pad;
+} ps_worker_decision;
+
+typedef struct ps_worker_pull {
+  uint64_t ticket;
+  double now;
+  int32_t worker;
+  int32_t _pad;
+  int64_t version;             /* version of the snapshot the worker received */
+} ps_worker_pull;
+
+/* Reset the ticket counter, go flags and logs (log_cap rows each) and start
+ * the gate clock: now = (device time since this call) x time_scale seconds. */
+int ps_workers_start(ps_server* h, int64_t log_cap, double time_scale);
+/* Bind worker p to its stream and flat fp32 buffers (device, 16-B aligned,
+ * >= round_up(d,4) floats): the push reads `grad`, the pull writes `params`. */
+int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const float* grad,
+                          float* params);
+/* Enqueue push -> wait(go[p]) -> pull on `cuda_stream` (NULL: the bound one;
+ * pass the capturing stream inside a CUDA-graph capture). throttle_ns > 0
+ * first busy-waits that long on the device (runner.py:185-189 spin_compute;
+ * the 1x/2x/4x throttle of BASELINE configs[3]). */
+int ps_enqueue_iteration(ps_server* h, int32_t worker, void* cuda_stream, uint64_t throttle_ns);
+/* Diagnostics: copy every update worker p pushes into ring[k % capacity]
+ * (device, [capacity][round_up(d,4)] fp32); NULL turns it off. */
+int ps_worker_record(ps_server* h, int32_t worker, float* ring, int64_t capacity);
+int ps_workers_status(ps_server* h, ps_workers_report* out);
+int ps_workers_log(ps_server* h, ps_worker_decision* dec, int64_t dec_cap, ps_worker_pull* pulls,
+                   int64_t pull_cap, int64_t* n_dec, int64_t* n_pull);
+/* Abort a free-running run from the host (ThreadedRun.abort, runner.py:110-111):
+ * raises every go flag so no stream stays blocked; later kernels only
+ * advance the ticket. */
+int ps_workers_abort(ps_server* h);
 
 /* ------------------------------------------------------------------------
  * Sharded server: G GPUs, one process (rank) per GPU, one worker per rank.

@@ -105,6 +105,13 @@ SIGNATURES = {
     "ps_last_kernel_ms": (ctypes.c_int, [_P, _PD]),
     "ps_set_profiling": (ctypes.c_int, [_P, _I32]),
     "ps_set_producer_stream": (ctypes.c_int, [_P, _P]),
+    "ps_workers_start": (ctypes.c_int, [_P, _I64, _D]),
+    "ps_bind_worker_stream": (ctypes.c_int, [_P, _I32, _P, _P, _P]),
+    "ps_enqueue_iteration": (ctypes.c_int, [_P, _I32, _P, ctypes.c_uint64]),
+    "ps_worker_record": (ctypes.c_int, [_P, _I32, _P, _I64]),
+    "ps_workers_status": (ctypes.c_int, [_P, _P]),
+    "ps_workers_log": (ctypes.c_int, [_P, _P, _I64, _P, _I64, _PI64, _PI64]),
+    "ps_workers_abort": (ctypes.c_int, [_P]),
     "ps_shard_create": (ctypes.c_int, [ctypes.POINTER(PSConfig), _I32, _I32, _P, _I64,
                                        ctypes.POINTER(_P)]),
     "ps_shard_ipc_handles": (ctypes.c_int, [_P, _P, _I64]),

@@ -64,6 +64,13 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_gpu_u32(unsigned* p, unsign
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ int ld_volatile_s32_(const int* p) {
+  return *reinterpret_cast<const volatile int*>(p);
+}
+// System scope: also observed by stream memory operations (cuStreamWaitValue32)
+__device__ __forceinline__ void st_release_u32_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -1,0 +1,554 @@
+// ps_workers.cu -- free-running workers gated by device flags (north star (4)).
+//
+// The reference's threaded runner (runner.py:168-291) runs one OS thread per
+// worker around ONE lock: apply_gradient -> decide_push(w, now) under the lock
+// (runner.py:226-249), a deferred worker parks on its release Event until a
+// granting push sets it (runner.py:243-263), and the pull happens under the
+// lock again (runner.py:273-284). Here every worker is a CUDA stream and the
+// host is out of the per-iteration loop:
+//
+//   worker stream p:  ... backward (writes the bound gradient buffer)
+//                     k_wpush(p)   take a ticket, wait for the turn, apply,
+//                                  decide at the device clock, write go flags
+//                     wait go[p]   cuStreamWaitValue32(go[p] == 1): the stream
+//                                  blocks WITHOUT occupying an SM or the host
+//                     k_wpull(p)   take a ticket, wait for the turn, copy the
+//                                  weights into the bound parameter buffer,
+//                                  clear go[p]
+//                     ... next forward
+//
+// The ticket order is the lock: every push and pull takes the next ticket when
+// its first CTA starts and waits until `served` reaches it, so applies, gate
+// decisions and pulls are serialized exactly like the runner's critical
+// sections, in device arrival order. A grant sets go[p]; _release's released
+// workers get go[q] (policy.py:197-206). All state is device-resident and
+// indexed by worker, so an iteration can be captured in a CUDA graph once and
+// replayed with no host work at all.
+//
+// Weights are double buffered as in k_apply: a non-finite update is rejected
+// and counted (server.py:65-67), a non-finite result aborts the run with the
+// weights unchanged (server.py:38-41): every go flag is raised so no stream
+// stays blocked, and later kernels only advance the ticket.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "gate.cuh"
+#include "server.h"
+
+using namespace dssp;
+
+namespace {
+
+constexpr int kWThreads = 256;
+
+struct WSlot {                    // per worker; reset by the last CTA of each kernel
+  unsigned start;                 // CTAs that have started (first one takes the ticket)
+  unsigned _pad;
+  unsigned long long ticket;      // ticket + 1 once taken (0 = not yet)
+  unsigned long long arrive;      // low: CTAs done, high: non-finite flag counts
+  long long pushes;               // pushes of this worker so far (record ring index)
+  long long pulls;
+};
+
+struct WCtl {
+  unsigned long long next_ticket;
+  unsigned long long served;      // tickets completed (the turn)
+  unsigned go[PS_MAX_WORKERS];    // 1: the worker may pull (granted / released)
+  int aborted;                    // a non-finite result: the run is over
+  int status;                     // first error (PS_E_DIVERGED / PS_E_PROTOCOL)
+  int diverged_worker;
+  int _pad;
+  unsigned long long t0;          // %globaltimer at ps_workers_start
+  double time_scale;              // gate seconds per wall-clock second
+  long long n_dec, n_pull;        // log lengths
+  WSlot slot[PS_MAX_WORKERS];
+};
+
+struct WDec {                     // one decided push, in ticket order
+  unsigned long long ticket;
+  double now;
+  int worker;
+  int outcome;                    // 0 grant, 1 defer
+  unsigned long long released;
+  long long version;              // after this push's apply
+  int applied;                    // 0: rejected (non-finite update)
+  int _pad;
+};
+
+struct WPull {
+  unsigned long long ticket;
+  double now;
+  int worker;
+  int _pad;
+  long long version;              // the snapshot's version
+};
+
+struct WArgs {
+  WCtl* c;
+  Ctrl* ctrl;                     // the server's control block (gate tables, cur, version)
+  float* w0;
+  float* w1;
+  long long n, nv;
+  float lr;
+  int worker;
+  const float* grad;              // bound gradient (push source)
+  float* params;                  // bound parameters (pull destination)
+  float* record;                  // optional [cap][dpad] ring of pushed updates
+  long long record_cap, dpad;
+  WDec* dec;
+  WPull* pull;
+  long long dec_cap, pull_cap;
+  unsigned long long timeout_ns;
+};
+
+// First CTA to start takes the next global ticket; every CTA then waits for
+// the turn. Returns the ticket (thread 0 of every CTA; broadcast via smem).
+__device__ __forceinline__ unsigned long long take_turn(const WArgs& a, WSlot* s) {
+  __shared__ unsigned long long s_t;
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    if (atomicAdd(&s->start, 1u) == 0u) {
+      t = atomicAdd(&a.c->next_ticket, 1ull);
+      st_release_u64(&s->ticket, t + 1);
+    } else {
+      unsigned long long v;
+      while ((v = ld_acquire_u64(&s->ticket)) == 0ull) __nanosleep(64);
+      t = v - 1;
+    }
+    const unsigned long long start = globaltimer_ns();
+    unsigned backoff = 32;
+    while (ld_acquire_u64(&a.c->served) != t) {
+      __nanosleep(backoff);
+      backoff = backoff < 1024 ? backoff * 2 : 1024;
+      if (globaltimer_ns() - start > a.timeout_ns) {  // watchdog: never hang the box
+        atomicCAS(&a.c->status, PS_OK, PS_E_TIMEOUT);
+        a.c->aborted = 1;
+        break;
+      }
+    }
+    s_t = t;
+  }
+  __syncthreads();
+  return s_t;
+}
+
+// Arrival at the end of a kernel: returns true in the last CTA (all CTAs'
+// writes acquired), with the accumulated flag counts in *flags.
+__device__ __forceinline__ bool arrive_last(WSlot* s, unsigned bad, unsigned* flags) {
+  __shared__ unsigned s_bad;
+  __shared__ int s_last;
+  __shared__ unsigned s_flags;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  bad = __reduce_or_sync(kFull, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicOr(&s_bad, bad);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long add = 1ull | ((unsigned long long)((s_bad & 1u) | ((s_bad & 2u) << 15)) << 32);
+    const unsigned long long prev = atom_add_acq_rel_gpu_u64(&s->arrive, add);
+    s_last = ((unsigned)prev == gridDim.x - 1);
+    s_flags = (unsigned)((prev + add) >> 32);
+  }
+  __syncthreads();
+  *flags = s_flags;
+  return s_last;
+}
+
+__device__ __forceinline__ void finish_turn(const WArgs& a, WSlot* s, unsigned long long t) {
+  s->start = 0;
+  s->ticket = 0;
+  s->arrive = 0;
+  __threadfence();
+  st_release_u64(&a.c->served, t + 1);
+}
+
+__device__ __forceinline__ void raise_all(WCtl* c, int P) {
+  for (int q = 0; q < P; ++q) st_release_u32_sys(&c->go[q], 1u);
+}
+
+// handle_push on the device (runner.py:226-252): apply in ticket order, then
+// the gate decision at the device clock, then release flags.
+__global__ void __launch_bounds__(kWThreads) k_wpush(WArgs a) {
+  WSlot* s = &a.c->slot[a.worker];
+  const unsigned long long t = take_turn(a, s);
+  const bool skip = ld_volatile_s32_(&a.c->aborted) != 0;
+  const int cur = ld_volatile_s32_(&a.ctrl->cur);
+  const float4* src = reinterpret_cast<const float4*>(cur ? a.w1 : a.w0);
+  float4* dst = reinterpret_cast<float4*>(cur ? a.w0 : a.w1);
+  const float4* g4 = reinterpret_cast<const float4*>(a.grad);
+  float4* rec = nullptr;
+  if (a.record && a.record_cap > 0)
+    rec = reinterpret_cast<float4*>(a.record + (s->pushes % a.record_cap) * a.dpad);
+  unsigned bad = 0;
+  if (!skip) {
+    const long long stride = (long long)gridDim.x * kWThreads;
+    for (long long j = (long long)blockIdx.x * kWThreads + threadIdx.x; j < a.nv; j += stride) {
+      const float4 g = ld_stream(g4 + j);
+      const float4 r = apply4(src[j], a.lr, g);
+      bad |= nonfinite4(g) ? 1u : 0u;
+      bad |= nonfinite4(r) ? 2u : 0u;
+      dst[j] = r;
+      if (rec) rec[j] = g;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (a.n & 3)) {
+      const long long i = (a.nv << 2) + threadIdx.x;
+      const float* sw = cur ? a.w1 : a.w0;
+      float* dw = cur ? a.w0 : a.w1;
+      const float gi = a.grad[i];
+      const float r = apply1(sw[i], a.lr, gi);
+      bad |= nonfinite(gi) ? 1u : 0u;
+      bad |= nonfinite(r) ? 2u : 0u;
+      dw[i] = r;
+      if (rec) reinterpret_cast<float*>(rec)[i] = gi;
+    }
+  }
+  unsigned flags = 0;
+  if (!arrive_last(s, bad, &flags) || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  WCtl* c = a.c;
+  ps_gate_state* gs = &a.ctrl->gate;
+  const int P = gs->worker_count;
+  if (skip) {
+    if (lane == 0) { s->pushes += 1; raise_all(c, P); finish_turn(a, s, t); }
+    return;
+  }
+  int applied = 0, diverged = 0;
+  if (lane == 0) {
+    if (flags & 0xffffu) {
+      gs->rejected += 1;                       // server.py:65-67
+    } else if (flags >> 16) {
+      diverged = 1;                            // server.py:38-41: weights unchanged
+    } else {
+      a.ctrl->cur = cur ^ 1;
+      gs->version += 1;
+      applied = 1;
+    }
+  }
+  diverged = __shfl_sync(kFull, diverged, 0);
+  if (diverged) {
+    if (lane == 0) {
+      if (atomicCAS(&c->status, PS_OK, PS_E_DIVERGED) == PS_OK) c->diverged_worker = a.worker;
+      c->aborted = 1;
+      s->pushes += 1;
+      raise_all(c, P);
+      finish_turn(a, s, t);
+    }
+    return;
+  }
+  // runner.py:234: the decision's timestamp is taken at decision time
+  double now = 0.0;
+  if (lane == 0) now = (double)(globaltimer_ns() - c->t0) * 1e-9 * c->time_scale;
+  now = __shfl_sync(kFull, now, 0);
+  const GateResult r = gate_on_push(gs, a.worker, now);
+  if (lane == 0) {
+    if (r.status != PS_OK) {
+      atomicCAS(&c->status, PS_OK, r.status);
+      c->aborted = 1;
+      raise_all(c, P);
+    } else {
+      if (r.outcome == 0) st_release_u32_sys(&c->go[a.worker], 1u);
+      for (unsigned long long m = r.released; m; m &= m - 1)
+        st_release_u32_sys(&c->go[__ffsll((long long)m) - 1], 1u);
+    }
+    const long long k = c->n_dec;
+    if (k < a.dec_cap) {
+      WDec e;
+      e.ticket = t; e.now = now; e.worker = a.worker; e.outcome = r.outcome;
+      e.released = r.released; e.version = gs->version; e.applied = applied; e._pad = 0;
+      a.dec[k] = e;
+    }
+    c->n_dec = k + 1;
+    s->pushes += 1;
+    finish_turn(a, s, t);
+  }
+}
+
+// handle_pull on the device (runner.py:273-284): the weights at this ticket
+// into the worker's parameters; clears the worker's go flag.
+__global__ void __launch_bounds__(kWThreads) k_wpull(WArgs a) {
+  WSlot* s = &a.c->slot[a.worker];
+  const unsigned long long t = take_turn(a, s);
+  const bool skip = ld_volatile_s32_(&a.c->aborted) != 0;
+  if (!skip) {
+    const int cur = ld_volatile_s32_(&a.ctrl->cur);
+    const float4* src = reinterpret_cast<const float4*>(cur ? a.w1 : a.w0);
+    float4* dst = reinterpret_cast<float4*>(a.params);
+    const long long stride = (long long)gridDim.x * kWThreads;
+    for (long long j = (long long)blockIdx.x * kWThreads + threadIdx.x; j < a.nv; j += stride)
+      dst[j] = src[j];
+    if (blockIdx.x == 0 && threadIdx.x < (a.n & 3)) {
+      const long long i = (a.nv << 2) + threadIdx.x;
+      a.params[i] = (cur ? a.w1 : a.w0)[i];
+    }
+  }
+  unsigned flags = 0;
+  if (!arrive_last(s, 0u, &flags) || threadIdx.x != 0) return;
+  WCtl* c = a.c;
+  if (!skip) {
+    const long long k = c->n_pull;
+    if (k < a.pull_cap) {
+      WPull e;
+      e.ticket = t;
+      e.now = (double)(globaltimer_ns() - c->t0) * 1e-9 * c->time_scale;
+      e.worker = a.worker; e._pad = 0;
+      e.version = a.ctrl->gate.version;
+      a.pull[k] = e;
+    }
+    c->n_pull = k + 1;
+    c->go[a.worker] = 0u;   // consumed: the next wait blocks until the next grant
+  }
+  s->pulls += 1;
+  finish_turn(a, s, t);
+}
+
+// Fallback blocking (PS_WORKERS_SPIN=1, or where stream memory operations are
+// unavailable): one warp polls go[p]. Occupies one warp slot while deferred.
+__global__ void k_wwait(const unsigned* go, const int* aborted) {
+  if (threadIdx.x != 0) return;
+  unsigned backoff = 64;
+  while (ld_acquire_u32(go) == 0u && ld_volatile_s32_(aborted) == 0) {
+    __nanosleep(backoff);
+    backoff = backoff < 4096 ? backoff * 2 : 4096;
+  }
+}
+
+// Device busy-wait of `ns` on the worker's stream (the runner's spin_compute,
+// runner.py:185-189): the 1x/2x/4x throttle of BASELINE configs[3].
+__global__ void k_wspin(unsigned long long ns) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+
+__global__ void k_wstart(WCtl* c, double time_scale) {
+  c->t0 = globaltimer_ns();
+  c->time_scale = time_scale;
+}
+
+}  // namespace
+
+struct ps_worker_rt {
+  WCtl* c = nullptr;
+  WDec* dec = nullptr;
+  WPull* pull = nullptr;
+  long long dec_cap = 0, pull_cap = 0;
+  int ctas = 0;
+  int spin_wait = 0;
+  struct Bind {
+    cudaStream_t stream = nullptr;
+    const float* grad = nullptr;
+    float* params = nullptr;
+    float* record = nullptr;
+    long long record_cap = 0;
+  } bind[PS_MAX_WORKERS];
+};
+
+void ps_workers_free(ps_server* h) {
+  if (!h->wrt) return;
+  cudaFree(h->wrt->c);
+  cudaFree(h->wrt->dec);
+  cudaFree(h->wrt->pull);
+  delete h->wrt;
+  h->wrt = nullptr;
+}
+
+namespace {
+
+struct DevGuardW {
+  int prev = 0;
+  explicit DevGuardW(int d) { cudaGetDevice(&prev); cudaSetDevice(d); }
+  ~DevGuardW() { cudaSetDevice(prev); }
+};
+
+WArgs make_args(ps_server* h, int worker) {
+  ps_worker_rt* rt = h->wrt;
+  WArgs a{};
+  a.c = rt->c;
+  a.ctrl = h->ctrl;
+  a.w0 = h->w[0];
+  a.w1 = h->w[1];
+  a.n = h->d;
+  a.nv = h->d >> 2;
+  a.lr = (float)h->cfg.learning_rate;
+  a.worker = worker;
+  a.grad = rt->bind[worker].grad;
+  a.params = rt->bind[worker].params;
+  a.record = rt->bind[worker].record;
+  a.record_cap = rt->bind[worker].record_cap;
+  a.dpad = h->dpad;
+  a.dec = rt->dec;
+  a.pull = rt->pull;
+  a.dec_cap = rt->dec_cap;
+  a.pull_cap = rt->pull_cap;
+  a.timeout_ns = 60ull * 1000 * 1000 * 1000;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ps_workers_start(ps_server* h, int64_t log_cap, double time_scale) {
+  DevGuardW guard(h->dev);
+  if (log_cap < 1) return ps_fail(h, PS_E_VALUE, "log capacity must be >= 1");
+  if (!(time_scale > 0)) return ps_fail(h, PS_E_VALUE, "time_scale must be > 0");
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  if (!h->wrt) {
+    h->wrt = new ps_worker_rt();
+    ps_worker_rt* rt = h->wrt;
+    PS_CK(h, cudaMalloc(&rt->c, sizeof(WCtl)));
+    int sms = h->sm_count;
+    // a small server footprint: the workers' own kernels keep the GPU
+    rt->ctas = sms / 8 > 4 ? sms / 8 : 4;
+    const char* v = getenv("PS_WORKERS_SPIN");
+    rt->spin_wait = v && v[0] == '1';
+  }
+  ps_worker_rt* rt = h->wrt;
+  if (rt->dec_cap < log_cap) {
+    cudaFree(rt->dec);
+    cudaFree(rt->pull);
+    rt->dec = nullptr;
+    rt->pull = nullptr;
+    PS_CK(h, cudaMalloc(&rt->dec, log_cap * sizeof(WDec)));
+    PS_CK(h, cudaMalloc(&rt->pull, log_cap * sizeof(WPull)));
+    rt->dec_cap = rt->pull_cap = log_cap;
+  }
+  PS_CK(h, cudaMemsetAsync(rt->c, 0, sizeof(WCtl), h->stream));
+  k_wstart<<<1, 1, 0, h->stream>>>(rt->c, time_scale);
+  PS_CK(h, cudaGetLastError());
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  return PS_OK;
+}
+
+int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const float* grad,
+                          float* params) {
+  if (!h->wrt) return ps_fail(h, PS_E_VALUE, "call ps_workers_start first");
+  if (worker < 0 || worker >= h->cfg.worker_count)
+    return ps_fail(h, PS_E_PROTOCOL, "unknown worker " + std::to_string(worker));
+  if (!grad || !params || ((uintptr_t)grad & 15u) || ((uintptr_t)params & 15u))
+    return ps_fail(h, PS_E_VALUE, "gradient / parameter buffers must be 16-byte aligned device memory");
+  auto& b = h->wrt->bind[worker];
+  b.stream = (cudaStream_t)cuda_stream;
+  b.grad = grad;
+  b.params = params;
+  return PS_OK;
+}
+
+int ps_worker_record(ps_server* h, int32_t worker, float* ring, int64_t capacity) {
+  if (!h->wrt) return ps_fail(h, PS_E_VALUE, "call ps_workers_start first");
+  if (worker < 0 || worker >= h->cfg.worker_count) return ps_fail(h, PS_E_PROTOCOL, "unknown worker");
+  if (ring && ((uintptr_t)ring & 15u)) return ps_fail(h, PS_E_VALUE, "record ring must be 16-byte aligned");
+  h->wrt->bind[worker].record = ring;
+  h->wrt->bind[worker].record_cap = ring ? capacity : 0;
+  return PS_OK;
+}
+
+// cuStreamWaitValue32 through the runtime's driver entry point: the library
+// then has no link-time dependency on libcuda (it loads on a GPU-less host).
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValue32Fn wait_value32() {
+  static WaitValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<WaitValue32Fn>(p);
+  }();
+  return fn;
+}
+
+int ps_enqueue_iteration(ps_server* h, int32_t worker, void* cuda_stream, uint64_t throttle_ns) {
+  DevGuardW guard(h->dev);
+  ps_worker_rt* rt = h->wrt;
+  if (!rt) return ps_fail(h, PS_E_VALUE, "call ps_workers_start first");
+  if (worker < 0 || worker >= h->cfg.worker_count)
+    return ps_fail(h, PS_E_PROTOCOL, "unknown worker " + std::to_string(worker));
+  auto& b = rt->bind[worker];
+  if (!b.grad) return ps_fail(h, PS_E_VALUE, "worker " + std::to_string(worker) + " is not bound");
+  cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : b.stream;
+  WArgs a = make_args(h, worker);
+  if (throttle_ns) {
+    k_wspin<<<1, 32, 0, st>>>(throttle_ns);
+    PS_CK(h, cudaGetLastError());
+  }
+  k_wpush<<<rt->ctas, kWThreads, 0, st>>>(a);
+  PS_CK(h, cudaGetLastError());
+  if (rt->spin_wait) {
+    k_wwait<<<1, 32, 0, st>>>(&rt->c->go[worker], &rt->c->aborted);
+    PS_CK(h, cudaGetLastError());
+  } else {
+    WaitValue32Fn wait = wait_value32();
+    if (!wait) return ps_fail(h, PS_E_CUDA, "cuStreamWaitValue32 unavailable (set PS_WORKERS_SPIN=1)");
+    CUresult r = wait((CUstream)st, (CUdeviceptr)&rt->c->go[worker], 1u, CU_STREAM_WAIT_VALUE_EQ);
+    if (r != CUDA_SUCCESS)
+      return ps_fail(h, PS_E_CUDA, "cuStreamWaitValue32 failed with CUresult " + std::to_string((int)r));
+  }
+  k_wpull<<<rt->ctas, kWThreads, 0, st>>>(a);
+  PS_CK(h, cudaGetLastError());
+  return PS_OK;
+}
+
+int ps_workers_status(ps_server* h, ps_workers_report* out) {
+  DevGuardW guard(h->dev);
+  ps_worker_rt* rt = h->wrt;
+  if (!rt) return ps_fail(h, PS_E_VALUE, "call ps_workers_start first");
+  WCtl c;
+  PS_CK(h, cudaMemcpyAsync(&c, rt->c, sizeof(WCtl), cudaMemcpyDeviceToHost, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  std::memset(out, 0, sizeof(*out));
+  out->tickets = (int64_t)c.served;
+  out->decisions = c.n_dec;
+  out->pulls = c.n_pull;
+  out->status = c.status;
+  out->diverged_worker = c.status == PS_E_DIVERGED ? c.diverged_worker : -1;
+  out->aborted = c.aborted;
+  for (int q = 0; q < PS_MAX_WORKERS; ++q) out->go_mask |= (uint64_t)(c.go[q] ? 1u : 0u) << q;
+  PS_CK(h, cudaMemcpyAsync(h->hctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  h->cur = h->hctrl->cur;
+  return PS_OK;
+}
+
+int ps_workers_log(ps_server* h, ps_worker_decision* dec, int64_t dec_cap, ps_worker_pull* pulls,
+                   int64_t pull_cap, int64_t* n_dec, int64_t* n_pull) {
+  DevGuardW guard(h->dev);
+  ps_worker_rt* rt = h->wrt;
+  if (!rt) return ps_fail(h, PS_E_VALUE, "call ps_workers_start first");
+  static_assert(sizeof(WDec) == sizeof(ps_worker_decision), "decision row layout");
+  static_assert(sizeof(WPull) == sizeof(ps_worker_pull), "pull row layout");
+  WCtl c;
+  PS_CK(h, cudaMemcpyAsync(&c, rt->c, sizeof(WCtl), cudaMemcpyDeviceToHost, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  const long long nd = c.n_dec < rt->dec_cap ? c.n_dec : rt->dec_cap;
+  const long long np = c.n_pull < rt->pull_cap ? c.n_pull : rt->pull_cap;
+  *n_dec = c.n_dec;
+  *n_pull = c.n_pull;
+  if (dec && dec_cap > 0 && nd > 0)
+    PS_CK(h, cudaMemcpy(dec, rt->dec, (nd < dec_cap ? nd : dec_cap) * sizeof(WDec), cudaMemcpyDeviceToHost));
+  if (pulls && pull_cap > 0 && np > 0)
+    PS_CK(h, cudaMemcpy(pulls, rt->pull, (np < pull_cap ? np : pull_cap) * sizeof(WPull), cudaMemcpyDeviceToHost));
+  return PS_OK;
+}
+
+int ps_workers_abort(ps_server* h) {
+  DevGuardW guard(h->dev);
+  ps_worker_rt* rt = h->wrt;
+  if (!rt) return PS_OK;
+  // a separate stream: the worker streams may be blocked; raise every flag
+  cudaStream_t st;
+  PS_CK(h, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  int one = 1;
+  unsigned ones[PS_MAX_WORKERS];
+  for (int q = 0; q < PS_MAX_WORKERS; ++q) ones[q] = 1u;
+  cudaError_t e = cudaMemcpyAsync(&rt->c->aborted, &one, sizeof(int), cudaMemcpyHostToDevice, st);
+  if (!e) e = cudaMemcpyAsync(rt->c->go, ones, sizeof(ones), cudaMemcpyHostToDevice, st);
+  if (!e) e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e) return ps_cuda_fail(h, e, "ps_workers_abort");
+  return PS_OK;
+}
+
+}  // extern "C"

@@ -25,6 +25,8 @@ struct ps_sim_buffers {
   int64_t last_trace_rows = 0, last_loss_samples = 0, last_loss_every = 0, last_base_version = 0;
 };
 
+struct ps_worker_rt;  // ps_workers.cu: free-running workers on device flags
+
 struct ps_server {
   ps_config cfg{};
   int dev = 0;
@@ -48,7 +50,10 @@ struct ps_server {
   int sm_count = 148;
   std::string err;
   ps_sim_buffers sim;
+  ps_worker_rt* wrt = nullptr;
 };
+
+void ps_workers_free(ps_server* h);
 
 int ps_fail(ps_server* h, int code, const std::string& msg);
 // Order h->stream after the caller's producer stream (ps_set_producer_stream).

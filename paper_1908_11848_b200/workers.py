@@ -113,6 +113,16 @@ class TorchWorker:
         """handle_pull straight into the parameters (server.py:84-91)."""
         server.handle_pull(self.worker, out=self.params[:self.dimension])
 
+    def step(self):
+        """Forward + backward on the current stream into the flat gradient
+        buffer (one static batch: the body of a captured iteration graph,
+        freerun.FreeRunningCluster)."""
+        x, y = self.batches[0]
+        self.grads.zero_()
+        loss = F.cross_entropy(self.model(x), y)
+        loss.backward()
+        self.iterations += 1
+
     def begin_iteration(self):
         """engine.py:263-272: next batch, loss and gradient at the local weights."""
         x, y = self.batches[self.cursor]
@@ -123,6 +133,23 @@ class TorchWorker:
         self.iterations += 1
         self.last_loss = loss.detach()
         return GradientVector(self.grads[:self.dimension], self.worker, self.iterations)
+
+
+class SyntheticWorker:
+    """A worker whose "backward" writes the next of K resident updates into its
+    gradient buffer (device-side index, so the step is graph-capturable):
+    push k carries ring[k % K]. For parity runs of the free-running path."""
+
+    def __init__(self, ring, device="cuda"):
+        self.ring = ring                                   # [K, dpad] fp32
+        self.K, self.dpad = ring.shape
+        self.params = torch.zeros(self.dpad, dtype=torch.float32, device=device)
+        self.grads = torch.zeros(self.dpad, dtype=torch.float32, device=device)
+        self.idx = torch.zeros(1, dtype=torch.long, device=device)
+
+    def step(self):
+        self.grads.copy_(self.ring.index_select(0, self.idx).squeeze(0))
+        self.idx.add_(1).remainder_(self.K)
 
 
 def synthetic_cifar(n_batches, batch, seed, device="cuda"):
