@@ -49,6 +49,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# free-running worker streams block on device flags: give every stream its own
+# hardware queue (must precede CUDA initialization)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback
@@ -323,6 +326,92 @@ def cpu_sample_main(args):
         "host_cpus": ncpu},
         "fingerprints": {"shards": shards, "replica": _fp32_checksums(w)}}))
     return 0
+
+
+def gate_check_main(path):
+    """Child: feed every recorded free-running decision sequence to the CPU
+    oracle gate (test infrastructure) and report which match."""
+    import oracle
+    runs = json.load(open(path))
+    out = {}
+    for key, run in runs.items():
+        g = oracle.CGate(run["paradigm"], run["P"], run["s"], run["r"])
+        ok = True
+        for w, now, outcome, released in run["seq"]:
+            if g.on_push(w, now) != (outcome, tuple(released)):
+                ok = False
+                break
+        out[key] = ok
+    print(json.dumps(out))
+    return 0
+
+
+def gate_check(runs):
+    """{key: {paradigm, P, s, r, seq}} -> {key: decisions identical to the oracle gate}."""
+    import tempfile
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as fh:
+        json.dump(runs, fh)
+        path = fh.name
+    try:
+        return _run_cpu_child(["gate", "--log", path])
+    finally:
+        os.unlink(path)
+
+
+def free_running(torch, ps, depth, P, mults, iters, batch=128):
+    """Real CIFAR ResNet-`depth` workers on ONE GPU gated by device flags
+    (freerun.FreeRunningCluster): each worker's iteration -- forward/backward,
+    throttle busy-wait, push kernel, stream wait on its go flag, pull kernel
+    -- is one captured CUDA graph; all iterations are enqueued up front, one
+    host sync at the end. `mults` are the per-worker slowdowns (the device
+    busy-wait adds (m - 1) x the measured single-worker iteration time).
+    Returns iterations/s, the fast worker's gate wait, defers, staleness and
+    the oracle-gate parity per paradigm."""
+    from paper_1908_11848_b200.engine import Engine
+    from paper_1908_11848_b200.freerun import FreeRunningCluster
+    from paper_1908_11848_b200.workers import CifarResNet, TorchWorker, synthetic_cifar
+    torch.manual_seed(0)
+    workers = [TorchWorker(p, CifarResNet(depth), synthetic_cifar(1, batch, seed=p)) for p in range(P)]
+    d = workers[0].dimension
+    w0 = workers[0].params[:d].detach().cpu().numpy().astype(np.float64)
+    # single-worker iteration time (the throttle's unit)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            workers[0].step()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            workers[0].step()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(10):
+            g.replay()
+        e1.record(st)
+    torch.cuda.synchronize()
+    base_ms = e0.elapsed_time(e1) / 10
+    del g
+    out, seqs = {}, {}
+    for name, s, r in PARADIGMS:
+        for wk in workers:
+            wk.params.copy_(workers[0].params)
+        eng = Engine(name, P, s, r, 0.01, d, w0=w0)
+        cl = FreeRunningCluster(eng, workers, throttle_ns=[int((m - 1) * base_ms * 1e6) for m in mults])
+        cl.capture(warmup=1)
+        rep = cl.run(iters)
+        seqs[name] = {"paradigm": name, "P": P, "s": s, "r": r,
+                      "seq": [[w, now, o, list(rel)] for w, now, o, rel in rep.decision_sequence()]}
+        out[name] = {"iters_per_s": rep.iters_per_s, "wall_s": rep.wall_s, "iterations": rep.pushes,
+                     "fast_worker_wait_s": rep.wait_s(0), "defers": rep.defers(),
+                     "max_staleness": rep.max_staleness(),
+                     "final_weights_finite": bool(torch.isfinite(workers[0].params[:d]).all().item())}
+        del cl
+        eng.close()
+    parity = gate_check(seqs)
+    for name in out:
+        out[name]["decisions_identical_to_oracle_gate"] = parity[name]
+    return {"model": f"CIFAR ResNet-{depth} ({d:,} params)", "workers": P, "batch": batch,
+            "slowdowns": list(mults), "single_worker_iteration_ms": base_ms,
+            "host_syncs_per_run": 1, "per_paradigm": out}
 
 
 def _run_cpu_child(extra):
@@ -701,6 +790,11 @@ def single_gpu_extras(torch, ps, line):
     line["c4_throttled"] = c4_throttled(torch, ps)
     line["c4_free_running"] = c4_realtime(torch, ps)
     line["torch_workers_c2"] = torch_workers(torch, ps)
+    # north star (4): real workers blocked and released by device flags, the
+    # host out of the iteration loop -- C2-shaped (4 x ResNet-20, 2 of them
+    # 2.2x slower like gtx-mix) and configs[3] (3 x ResNet-110 at 1x/2x/4x)
+    line["free_running_c2"] = free_running(torch, ps, 20, 4, (1.0, 1.0, 2.2, 2.2), 40)
+    line["free_running_c4"] = free_running(torch, ps, 110, 3, (1.0, 2.0, 4.0), 24)
 
 
 def main():
@@ -710,11 +804,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=("engine", "reference"))
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--cpu-sample", choices=("c2", "c3"), default=None)
+    ap.add_argument("--cpu-sample", choices=("c2", "c3", "gate"), default=None)
+    ap.add_argument("--log", default=None)
     ap.add_argument("--world", type=int, default=1)
     ap.add_argument("--applies", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.cpu_sample == "gate":
+        return gate_check_main(args.log)
     if args.cpu_sample:
         return cpu_sample_main(args)
     if args.impl == "reference":
