@@ -358,7 +358,7 @@ def gate_check(runs):
         os.unlink(path)
 
 
-def free_running(torch, ps, depth, P, mults, iters, batch=128):
+def free_running(torch, ps, depth, P, mults, iters, batch=128, devices=None):
     """Real CIFAR ResNet-`depth` workers on ONE GPU gated by device flags
     (freerun.FreeRunningCluster): each worker's iteration -- forward/backward,
     throttle busy-wait, push kernel, stream wait on its go flag, pull kernel
@@ -371,7 +371,9 @@ def free_running(torch, ps, depth, P, mults, iters, batch=128):
     from paper_1908_11848_b200.freerun import FreeRunningCluster
     from paper_1908_11848_b200.workers import CifarResNet, TorchWorker, synthetic_cifar
     torch.manual_seed(0)
-    workers = [TorchWorker(p, CifarResNet(depth), synthetic_cifar(1, batch, seed=p)) for p in range(P)]
+    devices = devices or [0] * P
+    workers = [TorchWorker(p, CifarResNet(depth), synthetic_cifar(1, batch, seed=p, device=f"cuda:{devices[p]}"),
+                           device=f"cuda:{devices[p]}") for p in range(P)]
     d = workers[0].dimension
     w0 = workers[0].params[:d].detach().cpu().numpy().astype(np.float64)
     # single-worker iteration time (the throttle's unit)
@@ -393,8 +395,8 @@ def free_running(torch, ps, depth, P, mults, iters, batch=128):
     out, seqs = {}, {}
     for name, s, r in PARADIGMS:
         for wk in workers:
-            wk.params.copy_(workers[0].params)
-        eng = Engine(name, P, s, r, 0.01, d, w0=w0)
+            wk.params.copy_(workers[0].params.to(wk.params.device))
+        eng = Engine(name, P, s, r, 0.01, d, w0=w0, device=devices[0])
         cl = FreeRunningCluster(eng, workers, throttle_ns=[int((m - 1) * base_ms * 1e6) for m in mults])
         cl.capture(warmup=1)
         rep = cl.run(iters)
@@ -410,6 +412,7 @@ def free_running(torch, ps, depth, P, mults, iters, batch=128):
     for name in out:
         out[name]["decisions_identical_to_oracle_gate"] = parity[name]
     return {"model": f"CIFAR ResNet-{depth} ({d:,} params)", "workers": P, "batch": batch,
+            "worker_gpus": list(devices), "server_gpu": devices[0],
             "slowdowns": list(mults), "single_worker_iteration_ms": base_ms,
             "host_syncs_per_run": 1, "per_paradigm": out}
 

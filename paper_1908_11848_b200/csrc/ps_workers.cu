@@ -25,6 +25,15 @@
 // indexed by worker, so an iteration can be captured in a CUDA graph once and
 // replayed with no host work at all.
 //
+// Workers may sit on other GPUs of the box (one process, peer access over
+// NVLink): the server's weights, gate tables, ticket counters and logs stay in
+// the server GPU's HBM; a worker's push / pull kernels run on the worker's
+// own GPU and reach them with P2P loads, stores and system-scope atomics; its
+// go flag lives in its own GPU's memory (the stream waits on local memory) and
+// is raised remotely by whichever GPU runs the granting push. Ticket hand-off
+// then uses fence.sc.sys + system-scope release / acquire instead of the
+// GPU-scope pair.
+//
 // Weights are double buffered as in k_apply: a non-finite update is rejected
 // and counted (server.py:65-67), a non-finite result aborts the run with the
 // weights unchanged (server.py:38-41): every go flag is raised so no stream
@@ -56,7 +65,7 @@ struct WSlot {                    // per worker; reset by the last CTA of each k
 struct WCtl {
   unsigned long long next_ticket;
   unsigned long long served;      // tickets completed (the turn)
-  unsigned go[PS_MAX_WORKERS];    // 1: the worker may pull (granted / released)
+  unsigned* go[PS_MAX_WORKERS];   // worker q's go flag (on q's GPU): 1 = may pull
   int aborted;                    // a non-finite result: the run is over
   int status;                     // first error (PS_E_DIVERGED / PS_E_PROTOCOL)
   int diverged_worker;
@@ -102,7 +111,13 @@ struct WArgs {
   WPull* pull;
   long long dec_cap, pull_cap;
   unsigned long long timeout_ns;
+  unsigned* my_go;                // this worker's go flag (local to the launching GPU)
+  int sys;                        // 1: the cluster spans GPUs (system-scope hand-off)
 };
+
+__device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p, int sys) {
+  return sys ? ld_acquire_sys_u64(p) : ld_acquire_u64(p);
+}
 
 // First CTA to start takes the next global ticket; every CTA then waits for
 // the turn. Returns the ticket (thread 0 of every CTA; broadcast via smem).
@@ -110,17 +125,18 @@ __device__ __forceinline__ unsigned long long take_turn(const WArgs& a, WSlot* s
   __shared__ unsigned long long s_t;
   if (threadIdx.x == 0) {
     unsigned long long t;
-    if (atomicAdd(&s->start, 1u) == 0u) {
-      t = atomicAdd(&a.c->next_ticket, 1ull);
-      st_release_u64(&s->ticket, t + 1);
+    if (atomicAdd_system(&s->start, 1u) == 0u) {
+      t = atomicAdd_system(&a.c->next_ticket, 1ull);
+      if (a.sys) st_release_sys_u64(&s->ticket, t + 1);
+      else st_release_u64(&s->ticket, t + 1);
     } else {
       unsigned long long v;
-      while ((v = ld_acquire_u64(&s->ticket)) == 0ull) __nanosleep(64);
+      while ((v = ld_acq(&s->ticket, a.sys)) == 0ull) __nanosleep(64);
       t = v - 1;
     }
     const unsigned long long start = globaltimer_ns();
     unsigned backoff = 32;
-    while (ld_acquire_u64(&a.c->served) != t) {
+    while (ld_acq(&a.c->served, a.sys) != t) {
       __nanosleep(backoff);
       backoff = backoff < 1024 ? backoff * 2 : 1024;
       if (globaltimer_ns() - start > a.timeout_ns) {  // watchdog: never hang the box
@@ -157,16 +173,28 @@ __device__ __forceinline__ bool arrive_last(WSlot* s, unsigned bad, unsigned* fl
   return s_last;
 }
 
+// The last CTA holds (acquired) every CTA's writes: the next ticket holder,
+// possibly on another GPU, acquires them through `served`.
 __device__ __forceinline__ void finish_turn(const WArgs& a, WSlot* s, unsigned long long t) {
   s->start = 0;
   s->ticket = 0;
   s->arrive = 0;
-  __threadfence();
-  st_release_u64(&a.c->served, t + 1);
+  if (a.sys) {
+    __threadfence_system();
+    st_release_sys_u64(&a.c->served, t + 1);
+  } else {
+    __threadfence();
+    st_release_u64(&a.c->served, t + 1);
+  }
+}
+
+__device__ __forceinline__ void raise_go(WCtl* c, int q) {
+  unsigned* g = c->go[q];
+  if (g) st_release_u32_sys(g, 1u);
 }
 
 __device__ __forceinline__ void raise_all(WCtl* c, int P) {
-  for (int q = 0; q < P; ++q) st_release_u32_sys(&c->go[q], 1u);
+  for (int q = 0; q < P; ++q) raise_go(c, q);
 }
 
 // handle_push on the device (runner.py:226-252): apply in ticket order, then
@@ -238,20 +266,38 @@ __global__ void __launch_bounds__(kWThreads) k_wpush(WArgs a) {
     }
     return;
   }
+  // the gate tables, possibly in a peer GPU's memory, run from shared memory:
+  // one coalesced copy in, the decision, the live entries back
+  __shared__ ps_gate_state sg;
+  {
+    const unsigned long long* src8 = reinterpret_cast<const unsigned long long*>(gs);
+    unsigned long long* dst8 = reinterpret_cast<unsigned long long*>(&sg);
+    for (int i = lane; i < (int)(sizeof(ps_gate_state) / 8); i += 32) dst8[i] = src8[i];
+  }
+  __syncwarp();
   // runner.py:234: the decision's timestamp is taken at decision time
   double now = 0.0;
   if (lane == 0) now = (double)(globaltimer_ns() - c->t0) * 1e-9 * c->time_scale;
   now = __shfl_sync(kFull, now, 0);
-  const GateResult r = gate_on_push(gs, a.worker, now);
+  const GateResult r = gate_on_push(&sg, a.worker, now);
+  __syncwarp();
+  for (int q = lane; q < P; q += 32) {
+    gs->clocks[q] = sg.clocks[q];
+    gs->latest[q] = sg.latest[q];
+    gs->previous[q] = sg.previous[q];
+    gs->populated[q] = sg.populated[q];
+    gs->credits[q] = sg.credits[q];
+  }
   if (lane == 0) {
+    gs->deferred = sg.deferred;
+    gs->decisions = sg.decisions;
     if (r.status != PS_OK) {
       atomicCAS(&c->status, PS_OK, r.status);
       c->aborted = 1;
       raise_all(c, P);
     } else {
-      if (r.outcome == 0) st_release_u32_sys(&c->go[a.worker], 1u);
-      for (unsigned long long m = r.released; m; m &= m - 1)
-        st_release_u32_sys(&c->go[__ffsll((long long)m) - 1], 1u);
+      if (r.outcome == 0) raise_go(c, a.worker);
+      for (unsigned long long m = r.released; m; m &= m - 1) raise_go(c, __ffsll((long long)m) - 1);
     }
     const long long k = c->n_dec;
     if (k < a.dec_cap) {
@@ -298,7 +344,7 @@ __global__ void __launch_bounds__(kWThreads) k_wpull(WArgs a) {
       a.pull[k] = e;
     }
     c->n_pull = k + 1;
-    c->go[a.worker] = 0u;   // consumed: the next wait blocks until the next grant
+    *a.my_go = 0u;          // consumed: the next wait blocks until the next grant
   }
   s->pulls += 1;
   finish_turn(a, s, t);
@@ -336,17 +382,25 @@ struct ps_worker_rt {
   long long dec_cap = 0, pull_cap = 0;
   int ctas = 0;
   int spin_wait = 0;
+  int sys = 0;                    // some worker sits on another GPU
+  double time_scale = 1.0;
   struct Bind {
     cudaStream_t stream = nullptr;
+    int dev = -1;
     const float* grad = nullptr;
     float* params = nullptr;
     float* record = nullptr;
     long long record_cap = 0;
+    unsigned* go = nullptr;       // the worker's go flag, in its own GPU's memory
+    int ctas = 0;
   } bind[PS_MAX_WORKERS];
 };
 
 void ps_workers_free(ps_server* h) {
   if (!h->wrt) return;
+  for (auto& b : h->wrt->bind)
+    if (b.go) { cudaSetDevice(b.dev); cudaFree(b.go); }
+  cudaSetDevice(h->dev);
   cudaFree(h->wrt->c);
   cudaFree(h->wrt->dec);
   cudaFree(h->wrt->pull);
@@ -383,7 +437,30 @@ WArgs make_args(ps_server* h, int worker) {
   a.dec_cap = rt->dec_cap;
   a.pull_cap = rt->pull_cap;
   a.timeout_ns = 60ull * 1000 * 1000 * 1000;
+  a.my_go = rt->bind[worker].go;
+  a.sys = rt->sys;
   return a;
+}
+
+// Reset the run state: counters, slots and logs zeroed, every bound worker's
+// go flag cleared, the go-pointer table rewritten, the gate clock started.
+int reset_run(ps_server* h) {
+  ps_worker_rt* rt = h->wrt;
+  WCtl hc;
+  std::memset(&hc, 0, sizeof(hc));
+  hc.time_scale = rt->time_scale;
+  for (int q = 0; q < PS_MAX_WORKERS; ++q) hc.go[q] = rt->bind[q].go;
+  PS_CK(h, cudaMemcpyAsync(rt->c, &hc, sizeof(WCtl), cudaMemcpyHostToDevice, h->stream));
+  k_wstart<<<1, 1, 0, h->stream>>>(rt->c, rt->time_scale);
+  PS_CK(h, cudaGetLastError());
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  for (int q = 0; q < PS_MAX_WORKERS; ++q) {
+    auto& b = rt->bind[q];
+    if (!b.go) continue;
+    DevGuardW g(b.dev);
+    PS_CK(h, cudaMemset(b.go, 0, sizeof(unsigned)));
+  }
+  return PS_OK;
 }
 
 }  // namespace
@@ -399,9 +476,6 @@ int ps_workers_start(ps_server* h, int64_t log_cap, double time_scale) {
     h->wrt = new ps_worker_rt();
     ps_worker_rt* rt = h->wrt;
     PS_CK(h, cudaMalloc(&rt->c, sizeof(WCtl)));
-    int sms = h->sm_count;
-    // a small server footprint: the workers' own kernels keep the GPU
-    rt->ctas = sms / 8 > 4 ? sms / 8 : 4;
     const char* v = getenv("PS_WORKERS_SPIN");
     rt->spin_wait = v && v[0] == '1';
   }
@@ -415,11 +489,8 @@ int ps_workers_start(ps_server* h, int64_t log_cap, double time_scale) {
     PS_CK(h, cudaMalloc(&rt->pull, log_cap * sizeof(WPull)));
     rt->dec_cap = rt->pull_cap = log_cap;
   }
-  PS_CK(h, cudaMemsetAsync(rt->c, 0, sizeof(WCtl), h->stream));
-  k_wstart<<<1, 1, 0, h->stream>>>(rt->c, time_scale);
-  PS_CK(h, cudaGetLastError());
-  PS_CK(h, cudaStreamSynchronize(h->stream));
-  return PS_OK;
+  rt->time_scale = time_scale;
+  return reset_run(h);
 }
 
 int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const float* grad,
@@ -429,10 +500,50 @@ int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const
     return ps_fail(h, PS_E_PROTOCOL, "unknown worker " + std::to_string(worker));
   if (!grad || !params || ((uintptr_t)grad & 15u) || ((uintptr_t)params & 15u))
     return ps_fail(h, PS_E_VALUE, "gradient / parameter buffers must be 16-byte aligned device memory");
-  auto& b = h->wrt->bind[worker];
+  // the worker's GPU is where its buffers live; a peer GPU reaches the
+  // server's memory over NVLink (and the server GPU the worker's go flag)
+  cudaPointerAttributes pa;
+  PS_CK(h, cudaPointerGetAttributes(&pa, grad));
+  if (pa.type != cudaMemoryTypeDevice) return ps_fail(h, PS_E_VALUE, "gradient buffer is not device memory");
+  const int wdev = pa.device;
+  ps_worker_rt* rt = h->wrt;
+  auto& b = rt->bind[worker];
+  // every GPU of the cluster must reach every other one: the server's memory
+  // from each worker GPU, and each worker's go flag from whichever GPU runs a
+  // granting push
+  for (int other = -1; other < PS_MAX_WORKERS; ++other) {
+    const int odev = other < 0 ? h->dev : rt->bind[other].dev;
+    if (odev < 0 || odev == wdev || (other >= 0 && !rt->bind[other].grad)) continue;
+    int ok = 0;
+    PS_CK(h, cudaDeviceCanAccessPeer(&ok, wdev, odev));
+    if (!ok) return ps_fail(h, PS_E_VALUE, "worker GPU cannot reach GPU " + std::to_string(odev) + " (no peer access)");
+    for (int pass = 0; pass < 2; ++pass) {
+      DevGuardW g(pass ? odev : wdev);
+      cudaError_t e = cudaDeviceEnablePeerAccess(pass ? wdev : odev, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e) return ps_cuda_fail(h, e, "cudaDeviceEnablePeerAccess");
+    }
+    rt->sys = 1;
+  }
+  if (b.go && b.dev != wdev) {
+    DevGuardW g(b.dev);
+    cudaFree(b.go);
+    b.go = nullptr;
+  }
+  if (!b.go) {
+    DevGuardW g(wdev);
+    PS_CK(h, cudaMalloc(&b.go, 256));
+    PS_CK(h, cudaMemset(b.go, 0, 256));
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wdev);
+  b.ctas = sms / 8 > 4 ? sms / 8 : 4;   // a small footprint: the workers keep their GPU
+  b.dev = wdev;
   b.stream = (cudaStream_t)cuda_stream;
   b.grad = grad;
   b.params = params;
+  DevGuardW guard(h->dev);
+  PS_CK(h, cudaMemcpy(&rt->c->go[worker], &b.go, sizeof(unsigned*), cudaMemcpyHostToDevice));
   return PS_OK;
 }
 
@@ -461,32 +572,32 @@ static WaitValue32Fn wait_value32() {
 }
 
 int ps_enqueue_iteration(ps_server* h, int32_t worker, void* cuda_stream, uint64_t throttle_ns) {
-  DevGuardW guard(h->dev);
   ps_worker_rt* rt = h->wrt;
   if (!rt) return ps_fail(h, PS_E_VALUE, "call ps_workers_start first");
   if (worker < 0 || worker >= h->cfg.worker_count)
     return ps_fail(h, PS_E_PROTOCOL, "unknown worker " + std::to_string(worker));
   auto& b = rt->bind[worker];
   if (!b.grad) return ps_fail(h, PS_E_VALUE, "worker " + std::to_string(worker) + " is not bound");
+  DevGuardW guard(b.dev);   // the worker's kernels run on the worker's GPU
   cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : b.stream;
   WArgs a = make_args(h, worker);
   if (throttle_ns) {
     k_wspin<<<1, 32, 0, st>>>(throttle_ns);
     PS_CK(h, cudaGetLastError());
   }
-  k_wpush<<<rt->ctas, kWThreads, 0, st>>>(a);
+  k_wpush<<<b.ctas, kWThreads, 0, st>>>(a);
   PS_CK(h, cudaGetLastError());
   if (rt->spin_wait) {
-    k_wwait<<<1, 32, 0, st>>>(&rt->c->go[worker], &rt->c->aborted);
+    k_wwait<<<1, 32, 0, st>>>(b.go, &rt->c->aborted);
     PS_CK(h, cudaGetLastError());
   } else {
     WaitValue32Fn wait = wait_value32();
     if (!wait) return ps_fail(h, PS_E_CUDA, "cuStreamWaitValue32 unavailable (set PS_WORKERS_SPIN=1)");
-    CUresult r = wait((CUstream)st, (CUdeviceptr)&rt->c->go[worker], 1u, CU_STREAM_WAIT_VALUE_EQ);
+    CUresult r = wait((CUstream)st, (CUdeviceptr)b.go, 1u, CU_STREAM_WAIT_VALUE_EQ);
     if (r != CUDA_SUCCESS)
       return ps_fail(h, PS_E_CUDA, "cuStreamWaitValue32 failed with CUresult " + std::to_string((int)r));
   }
-  k_wpull<<<rt->ctas, kWThreads, 0, st>>>(a);
+  k_wpull<<<b.ctas, kWThreads, 0, st>>>(a);
   PS_CK(h, cudaGetLastError());
   return PS_OK;
 }
@@ -505,7 +616,14 @@ int ps_workers_status(ps_server* h, ps_workers_report* out) {
   out->status = c.status;
   out->diverged_worker = c.status == PS_E_DIVERGED ? c.diverged_worker : -1;
   out->aborted = c.aborted;
-  for (int q = 0; q < PS_MAX_WORKERS; ++q) out->go_mask |= (uint64_t)(c.go[q] ? 1u : 0u) << q;
+  for (int q = 0; q < PS_MAX_WORKERS; ++q) {
+    const auto& b = rt->bind[q];
+    if (!b.go) continue;
+    unsigned v = 0;
+    DevGuardW g(b.dev);
+    PS_CK(h, cudaMemcpy(&v, b.go, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    out->go_mask |= (uint64_t)(v ? 1u : 0u) << q;
+  }
   PS_CK(h, cudaMemcpyAsync(h->hctrl, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
   PS_CK(h, cudaStreamSynchronize(h->stream));
   h->cur = h->hctrl->cur;
@@ -534,20 +652,30 @@ int ps_workers_log(ps_server* h, ps_worker_decision* dec, int64_t dec_cap, ps_wo
 }
 
 int ps_workers_abort(ps_server* h) {
-  DevGuardW guard(h->dev);
   ps_worker_rt* rt = h->wrt;
   if (!rt) return PS_OK;
-  // a separate stream: the worker streams may be blocked; raise every flag
-  cudaStream_t st;
-  PS_CK(h, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  // separate streams: the worker streams may be blocked; raise every flag
   int one = 1;
-  unsigned ones[PS_MAX_WORKERS];
-  for (int q = 0; q < PS_MAX_WORKERS; ++q) ones[q] = 1u;
-  cudaError_t e = cudaMemcpyAsync(&rt->c->aborted, &one, sizeof(int), cudaMemcpyHostToDevice, st);
-  if (!e) e = cudaMemcpyAsync(rt->c->go, ones, sizeof(ones), cudaMemcpyHostToDevice, st);
-  if (!e) e = cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
-  if (e) return ps_cuda_fail(h, e, "ps_workers_abort");
+  unsigned ones = 1u;
+  {
+    DevGuardW g(h->dev);
+    cudaStream_t st;
+    PS_CK(h, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaError_t e = cudaMemcpyAsync(&rt->c->aborted, &one, sizeof(int), cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (e) return ps_cuda_fail(h, e, "ps_workers_abort");
+  }
+  for (auto& b : rt->bind) {
+    if (!b.go) continue;
+    DevGuardW g(b.dev);
+    cudaStream_t st;
+    PS_CK(h, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaError_t e = cudaMemcpyAsync(b.go, &ones, sizeof(unsigned), cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (e) return ps_cuda_fail(h, e, "ps_workers_abort");
+  }
   return PS_OK;
 }
 

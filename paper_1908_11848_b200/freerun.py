@@ -103,11 +103,13 @@ class FreeRunReport:
 
 
 class FreeRunningCluster:
-    """P workers on one GPU behind one engine, gated by device flags.
+    """P workers behind one engine, gated by device flags.
 
     ``workers`` are objects with ``.params`` / ``.grads`` (flat fp32 CUDA
     buffers, 16-byte aligned) and ``.step()`` (forward + backward writing the
-    gradient buffer on the current stream), e.g. workers.TorchWorker.
+    gradient buffer on the current stream), e.g. workers.TorchWorker. A worker
+    runs on the GPU its buffers live on: the engine's GPU, or a peer GPU of the
+    same box (its push / pull kernels then reach the server over NVLink).
     """
 
     def __init__(self, engine, workers, throttle_ns=None, graphs=True, time_scale=1.0,
@@ -123,7 +125,8 @@ class FreeRunningCluster:
         self.graphs = graphs
         self.time_scale = float(time_scale)
         self.log_cap = int(log_cap)
-        self.streams = [torch.cuda.Stream(device=engine.device) for _ in range(self.P)]
+        self.devices = [wk.params.device for wk in self.workers]
+        self.streams = [torch.cuda.Stream(device=dev) for dev in self.devices]
         self._graphs = [None] * self.P
         self._check(self.lib.ps_workers_start(engine.handle, self.log_cap, self.time_scale))
         for p, wk in enumerate(self.workers):
@@ -149,18 +152,24 @@ class FreeRunningCluster:
         server, then capture one iteration per worker as a CUDA graph."""
         import torch
         for p, wk in enumerate(self.workers):
-            with torch.cuda.stream(self.streams[p]):
+            with torch.cuda.device(self.devices[p]), torch.cuda.stream(self.streams[p]):
                 for _ in range(warmup):
                     wk.step()
-        torch.cuda.synchronize()
+        self._sync_all()
         if not self.graphs:
             return
         for p in range(self.P):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=self.streams[p]):
-                self._iteration(p, torch.cuda.current_stream().cuda_stream)
+            with torch.cuda.device(self.devices[p]):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.streams[p]):
+                    self._iteration(p, torch.cuda.current_stream().cuda_stream)
             self._graphs[p] = g
-        torch.cuda.synchronize()
+        self._sync_all()
+
+    def _sync_all(self):
+        import torch
+        for dev in sorted({d.index for d in self.devices} | {self.engine.device}):
+            torch.cuda.synchronize(dev)
 
     def run(self, iterations, restart=True):
         """`iterations` per worker, every launch enqueued up front, one host
@@ -168,16 +177,16 @@ class FreeRunningCluster:
         import torch
         if restart:
             self._check(self.lib.ps_workers_start(self.engine.handle, self.log_cap, self.time_scale))
-        torch.cuda.synchronize()
+        self._sync_all()
         t0 = time.perf_counter()
         for _ in range(int(iterations)):
             for p in range(self.P):
-                with torch.cuda.stream(self.streams[p]):
+                with torch.cuda.device(self.devices[p]), torch.cuda.stream(self.streams[p]):
                     if self._graphs[p] is not None:
                         self._graphs[p].replay()
                     else:
                         self._iteration(p, self.streams[p].cuda_stream)
-        torch.cuda.synchronize()
+        self._sync_all()
         wall = time.perf_counter() - t0
         return self.report(wall)
 

@@ -58,14 +58,16 @@ def _replay(rep, rings, d, w0, lr):
     return w, snaps
 
 
-def _synthetic_cluster(paradigm, s, r, P, d, K, throttle_us, graphs=True, seed=9):
+def _synthetic_cluster(paradigm, s, r, P, d, K, throttle_us, graphs=True, seed=9, devices=None):
     rings_h = []
     for p in range(P):
         ring = np.zeros((K, (d + 3) // 4 * 4), dtype=np.float32)
         for k in range(K):
             ring[k, :d] = oracle.synthetic_update(seed, p, k, d)
         rings_h.append(ring)
-    workers = [SyntheticWorker(torch.from_numpy(rg).cuda()) for rg in rings_h]
+    devices = devices or [0] * P
+    workers = [SyntheticWorker(torch.from_numpy(rg).to(f"cuda:{devices[p]}"), device=f"cuda:{devices[p]}")
+               for p, rg in enumerate(rings_h)]
     eng = Engine(paradigm, P, s, r, 0.05, d, w0=oracle.initial_weights_f64(0, d))
     cl = FreeRunningCluster(eng, workers, throttle_ns=[int(t * 1000) for t in throttle_us],
                             graphs=graphs)
@@ -73,7 +75,7 @@ def _synthetic_cluster(paradigm, s, r, P, d, K, throttle_us, graphs=True, seed=9
     # capture ran no iteration; every worker's ring index is back at 0
     for wk in workers:
         wk.idx.zero_()
-    torch.cuda.synchronize()
+    cl._sync_all()
     return eng, cl, workers, rings_h
 
 
@@ -107,6 +109,32 @@ def test_free_running_synthetic_workers(paradigm, s, r, graphs):
         assert rep.defers() > 0
     if paradigm == "asp":
         assert rep.defers() == 0
+    eng.close()
+
+
+@pytest.mark.parametrize("paradigm,s,r", PARADIGMS)
+def test_free_running_workers_on_peer_gpus(paradigm, s, r):
+    """Workers on every GPU of the box, the server on GPU 0: push / pull
+    kernels on the worker's GPU reach the weights, gate and tickets over
+    NVLink; go flags are raised remotely. Same parity as on one GPU."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    P, d, K, iters = 4, 70_001, 3, 30
+    devices = [p % n for p in range(P)]
+    eng, cl, workers, rings = _synthetic_cluster(paradigm, s, r, P, d, K, [0, 20, 60, 120],
+                                                 devices=devices)
+    rep = cl.run(iters)
+    assert rep.pushes == P * iters
+    _check_gate(rep, paradigm, P, s, r)
+    w, snaps = _replay(rep, rings, d, oracle.initial_weights_f64(0, d).astype(np.float32), 0.05)
+    assert np.array_equal(eng.read()[0].view(np.uint32), w.view(np.uint32))
+    for p in range(P):
+        last = rep.pulls[rep.pulls["worker"] == p][-1]
+        mine = workers[p].params[:d].cpu().numpy()
+        assert np.array_equal(mine.view(np.uint32), snaps[int(last["version"])].view(np.uint32)), p
+    if paradigm in ("bsp", "ssp"):
+        assert rep.defers() > 0
     eng.close()
 
 
