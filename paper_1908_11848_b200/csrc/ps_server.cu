@@ -85,7 +85,7 @@ __device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* mirror) {
 // One streaming pass w[cur^1] = w[cur] - lr*g with flag reduction; the last CTA
 // publishes the result and (fuse=1) runs the gate decision. g may live in
 // device memory or in pinned host memory (read over PCIe, zero-copy).
-template <typename G>
+template <typename G, int kApplyUnroll>
 __global__ void __launch_bounds__(kApplyThreads)
 k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g, long long n,
         float lr, Ctrl* ctrl, int cur, int fuse, int worker, double now, Ctrl* mirror) {
@@ -272,8 +272,8 @@ __global__ void k_spin(unsigned long long ns) {
   }
 }
 
-int grid_for(const ps_server* h, long long nv) {
-  long long per_block = (long long)kApplyThreads * kApplyUnroll;
+int grid_for(const ps_server* h, long long nv, int unroll = kApplyUnroll) {
+  long long per_block = (long long)kApplyThreads * unroll;
   long long blocks = (nv + per_block - 1) / per_block;
   long long cap = (long long)h->sm_count * 8;
   if (blocks < 1) blocks = 1;
@@ -350,6 +350,17 @@ bool host_dma() {
   return on;
 }
 
+// float4 per thread per trip of the apply on small vectors (PS_APPLY_SMALL_U,
+// an A/B knob; the large-vector path keeps kApplyUnroll)
+int apply_small_unroll() {
+  static const int u = [] {
+    const char* v = getenv("PS_APPLY_SMALL_U");
+    const int x = v ? atoi(v) : 1;
+    return (x == 1 || x == 2 || x == 4) ? x : 1;
+  }();
+  return u;
+}
+
 // Pinned (page-locked, UVA-mapped) host memory can be read and written by
 // kernels directly over PCIe; pageable memory has to be staged.
 bool pinned_host(const void* p) {
@@ -390,14 +401,22 @@ int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_
   const float lr = (float)h->cfg.learning_rate;
   const int grid = grid_for(h, h->nv);
   if ((rc = mark(h, h->ev0))) return rc;
-  if (g_dtype == PS_F32)
-    k_apply<float><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const float*)dg, h->d,
-                                                          lr, h->ctrl, h->cur, fuse, worker, now,
-                                                          h->hctrl_dev);
-  else
-    k_apply<double><<<grid, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const double*)dg,
-                                                           h->d, lr, h->ctrl, h->cur, fuse, worker, now,
-                                                           h->hctrl_dev);
+  // small vectors: one float4 per thread per trip over more CTAs (the op is
+  // latency-bound there: spread it over every SM); large ones: four in flight
+  const int small_u = apply_small_unroll();
+  const bool small = h->nv <= (long long)h->sm_count * kApplyThreads * 8;
+  const int U = small ? small_u : kApplyUnroll;
+  const int grid2 = grid_for(h, h->nv, U);
+  (void)grid;
+#define PS_LAUNCH_APPLY(T, UU)                                                                      \
+  k_apply<T, UU><<<grid2, kApplyThreads, 0, h->stream>>>(h->w[0], h->w[1], (const T*)dg, h->d, lr, \
+                                                        h->ctrl, h->cur, fuse, worker, now, h->hctrl_dev)
+  if (g_dtype == PS_F32) {
+    if (U == 1) PS_LAUNCH_APPLY(float, 1); else if (U == 2) PS_LAUNCH_APPLY(float, 2); else PS_LAUNCH_APPLY(float, 4);
+  } else {
+    if (U == 1) PS_LAUNCH_APPLY(double, 1); else if (U == 2) PS_LAUNCH_APPLY(double, 2); else PS_LAUNCH_APPLY(double, 4);
+  }
+#undef PS_LAUNCH_APPLY
   PS_CK(h, cudaGetLastError());
   if ((rc = mark(h, h->ev1))) return rc;
   return finish_op(h);

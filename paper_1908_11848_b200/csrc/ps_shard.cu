@@ -37,6 +37,7 @@
 // on the waiter's later work, so the protocol cannot deadlock; every spin has a
 // watchdog that aborts the kernel instead of hanging the GPU.
 #include <cuda_runtime.h>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -52,6 +53,9 @@ namespace {
 constexpr int kMaxRanks = 16;
 constexpr int kSchedStride = 2 + kMaxRanks;  // ps_shard_run_groups row: n, pull mask, order
 constexpr int kThreads = 256;
+// per-rank flag words written by peers: ready[G] | V(t) by step parity [2][G]
+// | F(t) redo done [G] | D first diverged step [G]
+constexpr int kFlagWords = 5 * kMaxRanks;
 constexpr unsigned long long kTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
 struct ShardPtrs {
@@ -79,6 +83,10 @@ struct ShardCtl {
   unsigned long long gate_done;     // last step whose decisions and next order are written
   unsigned long long committed;     // unused (kept for the host marks layout)
   unsigned long long redo_total;    // data-CTA arrivals at rejection redos (election)
+  unsigned long long arrive_par[2]; // data-CTA arrivals of this run's even / odd steps
+  uint32_t badp[2];                 // per-parity step verdict bits (see k_shard_run)
+  int32_t div_sticky;               // a step of this server diverged
+  int32_t no_lag;                   // PS_SHARD_NO_LAG: resolve every step in full
 };
 
 __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
@@ -123,8 +131,8 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
 }
 
 template <int G_MAX>
-__global__ void __launch_bounds__(kThreads)
-k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, ShardPtrs P, int G,
+__global__ void __launch_bounds__(kThreads, 2)
+k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ w2, long long n_local, ShardPtrs P, int G,
             int me, unsigned long long t0, int steps, float lr, ShardCtl* ctl, const double* now,
             ps_trace_row* trace, long long trace_cap, const int* sched) {
   const int ndata = gridDim.x - 1;
@@ -152,7 +160,9 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         // order[co ^ 1] is read by every data CTA at the start of step t-1
         // (into shared memory); all of them have once they arrived there
         const unsigned long long s0 = globaltimer_ns();
-        while (ld_acquire_u64(&ctl->arrive_total) < (t - 1) * (unsigned long long)ndata) {
+        // every data CTA arrived at step i-1 of this run (per-parity counters)
+        while (i > 0 && ld_acquire_u64(&ctl->arrive_par[(i - 1) & 1]) <
+                            (unsigned long long)((i - 1) / 2 + 1) * (unsigned long long)ndata) {
           // the data side stopped (divergence / a peer's watchdog): so do we
           if (ld_relaxed_s32(&ctl->status) != PS_OK) { status = PS_E_TIMEOUT; break; }
           if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); break; }
@@ -221,13 +231,24 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
   // V(t) = (t << 32 | diverged << 31 | rejected-worker bits seen in its slice)
   // into every rank's flag array. V(t) from every owner is, at once, "every
   // pull of step t has landed" (s wrote its slice into every replica before
-  // the release) and the global verdict (the union of the bits): the next
-  // step starts on it and commits step t first -- flip the buffers, or in the
-  // rare rejection case redo step t's slice without the rejected updates and
-  // exchange F(t) before any worker pushes again.
+  // the release) and the global verdict (the union of the bits).
+  //
+  // The shard is triple buffered: step k of the run reads buffer (c0 + k) % 3
+  // and writes (c0 + k + 1) % 3. The first step of a run is resolved in full
+  // before the second starts (the rejected set R of this run's update buffers
+  // is then known -- they do not change during a run -- and a rejection is
+  // redone without the rejected updates, server.py:65-67). In the homogeneous
+  // schedule every later step skips R up front and needs only the divergence
+  // verdict, so it is resolved one step LATE: step k starts once every owner
+  // finished step k-2, overlapping the tail of step k-1 (the slowest CTAs, the
+  // election, the fence and the cross-GPU flag hop) with step k's streaming.
+  // A non-finite result at step j (server.py:38-41) is published in D[s] = j
+  // before V(j); every rank then stops with the weights of buffer
+  // (c0 + j - t0) % 3 -- intact, because no step past j + 1 can have started.
+  // Heterogeneous schedules (sched != nullptr) resolve every step in full.
   __shared__ unsigned s_bits;
-  __shared__ int s_last, s_stop, s_div;
-  __shared__ unsigned long long s_rej;
+  __shared__ int s_stop, s_div;
+  __shared__ unsigned long long s_rej, s_tdiv;
   __shared__ int s_order[2][kMaxRanks];
   __shared__ int s_n[2];           // pushers of the step in this slot
   __shared__ unsigned s_pull[2];   // workers whose replica the step writes
@@ -236,11 +257,33 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
   constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
   const long long stride = (long long)ndata * kThreads * U;
   const long long first = (long long)blockIdx.x * kThreads * U + threadIdx.x;
-  int cur = ld_relaxed_s32(&ctl->cur);  // the committed buffer at launch, identical in every CTA
-  long long redo_n = 0;                 // redo rounds so far (election targets)
+  // buffer i of the rotation, by selects (a dynamically indexed array would
+  // live in local memory)
+  auto wb = [&](int i) -> float* { return i == 0 ? w0 : (i == 1 ? w1 : w2); };
+  const int c0 = ld_relaxed_s32(&ctl->cur);  // the committed buffer at launch, identical in every CTA
+  long long redo_n = 0;                      // redo rounds so far (election targets)
   const int steps_total = steps;
-  // Wait for V(t) of every owner and commit step t (see above). Returns false
-  // when the run must stop (watchdog or divergence).
+  const bool lag = (sched == nullptr) && steps > 2 && ld_relaxed_s32(&ctl->no_lag) == 0;
+  unsigned long long R = 0;                  // rejected workers of this run (lag mode)
+  // commit step t (relative index k): buffer (c0 + k + 1) % 3 becomes current
+  auto commit = [&](unsigned long long t, unsigned long long rej) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const int k = (int)(t - t0);
+      ctl->cur = (c0 + k + 1) % 3;
+      const int co = (int)(t & 1);
+      ctl->gate.version += s_n[co] - __popcll(rej);
+      ctl->gate.rejected += __popcll(rej);
+    }
+  };
+  auto stop_diverged = [&](unsigned long long tdiv) {
+    // the weights stay at the input of step tdiv (server.py:38-41)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctl->cur = (c0 + (int)(tdiv - t0)) % 3;
+      atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);
+    }
+  };
+  // Full resolve of step t: wait for V(t) of every owner; redo this CTA's part
+  // of the slice without rejected updates if any; stop on divergence; commit.
   auto resolve = [&](unsigned long long t) -> bool {
     if (threadIdx.x == 0) {
       SPROF(const unsigned long long tr0 = globaltimer_ns());
@@ -249,7 +292,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       const unsigned long long s0 = globaltimer_ns();
       for (int s = 0; s < G && !stop; ++s) {
         unsigned long long v;
-        while (((v = ld_acquire_sys_u64(P.flags[me] + G + s)) >> 32) < t) {
+        while (((v = ld_acquire_sys_u64(P.flags[me] + G + (int)(t & 1) * G + s)) >> 32) < t) {
           if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
           __nanosleep(20);
         }
@@ -263,12 +306,13 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     if (s_stop) return false;
     const unsigned long long rej = s_rej;
     const int co = (int)(t & 1);
+    const int k = (int)(t - t0);
     if (rej) {
       // rare path: this CTA's part of the slice again, without the rejected
       // updates (server.py:65-67), into the back buffer and every replica;
       // the optimistic pass's divergence bit is void (it included them)
-      const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
-      float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
+      const float4* wsrc = reinterpret_cast<const float4*>(wb((c0 + k) % 3));
+      float4* wdst = reinterpret_cast<float4*>(wb((c0 + k + 1) % 3));
       unsigned redo_bad = 0;
       for (long long base = first; base < nv; base += stride)
         for (int u = 0; u < U; ++u) {
@@ -292,13 +336,13 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         if (prev == (unsigned long long)(redo_n * ndata) - 1) {  // last CTA: F(t) to every rank
           const unsigned long long dv = atomicExch(&ctl->bad, 0u) & 1u;
           __threadfence_system();
-          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + 2 * G + me, (t << 32) | dv);
+          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + 3 * G + me, (t << 32) | dv);
         }
         int div = 0, stop = 0;
         const unsigned long long s0 = globaltimer_ns();
         for (int s = 0; s < G && !stop; ++s) {
           unsigned long long v;
-          while (((v = ld_acquire_sys_u64(P.flags[me] + 2 * G + s)) >> 32) < t) {
+          while (((v = ld_acquire_sys_u64(P.flags[me] + 3 * G + s)) >> 32) < t) {
             if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
             __nanosleep(20);
           }
@@ -310,22 +354,59 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       if (s_stop) return false;
     }
     if (s_div) {
-      // a non-finite result (server.py:38-41): the weights stay at w[cur]
-      if (blockIdx.x == 0 && threadIdx.x == 0) atomicCAS(&ctl->status, PS_OK, PS_E_DIVERGED);
+      stop_diverged(t);
       return false;
     }
-    cur ^= 1;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      ctl->cur = cur;
-      ctl->gate.version += s_n[co] - __popcll(rej);
-      ctl->gate.rejected += __popcll(rej);
-    }
+    R |= rej;
+    commit(t, rej);
     return true;
   };
+  // Lagged resolve of step t (lag mode, t > t0): wait for V(>= t) of every
+  // owner; a divergence at or before t stops the run at its first step.
+  auto resolve_lag = [&](unsigned long long t) -> bool {
+    if (threadIdx.x == 0) {
+      SPROF(const unsigned long long tr0 = globaltimer_ns());
+      int stop = 0;
+      unsigned long long tdiv = 0;
+      const unsigned long long s0 = globaltimer_ns();
+      for (int s = 0; s < G && !stop; ++s) {
+        unsigned long long v;
+        while (((v = ld_acquire_sys_u64(P.flags[me] + G + (int)(t & 1) * G + s)) >> 32) < t) {
+          if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
+          __nanosleep(20);
+        }
+        if ((v >> 31) & 1ull) {
+          // sticky: owner s diverged at step D[s] <= v's step (published first)
+          const unsigned long long d = ld_acquire_sys_u64(P.flags[me] + 4 * G + s);
+          if (d && d <= t && (!tdiv || d < tdiv)) tdiv = d;
+        }
+      }
+      s_tdiv = tdiv; s_stop = stop;
+      SPROF(if (blockIdx.x == 0) { const unsigned long long tn = globaltimer_ns(); g_prof[0] += tn - tr0; g_t_resolved = tn; })
+    }
+    __syncthreads();
+    if (s_stop) return false;
+    if (s_tdiv) {
+      stop_diverged(s_tdiv);
+      return false;
+    }
+    commit(t, R);
+    return true;
+  };
+  unsigned long long resolved = t0 - 1;  // last step resolved by this CTA
   for (int step = 0; step < steps_total; ++step) {
     const unsigned long long t = t0 + step;
     const int co = (int)(t & 1);
-    if (step > 0 && !resolve(t - 1)) return;
+    if (!lag) {
+      if (step > 0 && !resolve(t - 1)) return;
+      resolved = t - 1;
+    } else if (step == 1) {
+      if (!resolve(t0)) return;
+      resolved = t0;
+    } else if (step >= 2) {
+      if (!resolve_lag(t - 2)) return;
+      resolved = t - 2;
+    }
     if (threadIdx.x == 0) {
       s_bits = 0;
       bool ok = true;
@@ -344,6 +425,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
       SPROF(const unsigned long long tw0 = globaltimer_ns());
       while (ok && !sched && ld_acquire_u64(&ctl->gate_done) + 1 < t) {
         if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); ok = false; }
+        if (ld_relaxed_s32(&ctl->status) != PS_OK) ok = false;  // the gate stopped (protocol)
         __nanosleep(32);
       }
       SPROF(if (blockIdx.x == 0) g_prof[5] += globaltimer_ns() - tw0);
@@ -363,14 +445,20 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     }
     __syncthreads();
     if (s_stop) return;  // watchdog fired
-    const float4* wsrc = reinterpret_cast<const float4*>(cur ? w1 : w0);
-    float4* wdst = reinterpret_cast<float4*>(cur ? w0 : w1);
+    const float4* wsrc = reinterpret_cast<const float4*>(wb((c0 + step) % 3));
+    float4* wdst = reinterpret_cast<float4*>(wb((c0 + step + 1) % 3));
     const int n_push = s_n[co];
     const unsigned pullm = s_pull[co];
+    // in lag mode the rejected workers of this run are known after step 0:
+    // their slices are not even loaded (rejected every push, server.py:65-67)
+    unsigned live = 0;
     const float4* src[G_MAX];
 #pragma unroll
-    for (int i = 0; i < G_MAX; ++i)
-      src[i] = reinterpret_cast<const float4*>(P.upd[i < n_push ? s_order[co][i] : 0] + lo);
+    for (int i = 0; i < G_MAX; ++i) {
+      const int p = i < n_push ? s_order[co][i] : 0;
+      src[i] = reinterpret_cast<const float4*>(P.upd[p] + lo);
+      if (i < n_push && !((R >> p) & 1ull)) live |= 1u << i;
+    }
     unsigned dbad = 0;
     unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
     // Optimistic single pass: apply all G updates in ticket order into the
@@ -387,7 +475,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         if (j < nv) {
 #pragma unroll
           for (int i = 0; i < G_MAX; ++i)
-            if (i < n_push) g[u][i] = ld_stream(src[i] + j);
+            if ((live >> i) & 1u) g[u][i] = ld_stream(src[i] + j);
           x[u] = wsrc[j];
         }
       }
@@ -397,7 +485,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
         if (j < nv) {
 #pragma unroll
           for (int i = 0; i < G_MAX; ++i)
-            if (i < n_push) {
+            if ((live >> i) & 1u) {
               gbad |= nonfinite4(g[u][i]) ? (1u << i) : 0u;
               x[u] = apply4(x[u], lr, g[u][i]);
             }
@@ -416,30 +504,47 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, long long n_local, S
     if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (s_bits) atomicOr(&ctl->bad, s_bits);
+      // per-parity verdict words and arrival counters: in lag mode CTAs of
+      // steps t and t+1 arrive interleaved, never those of t and t+2
+      if (s_bits) atomicOr(&ctl->badp[co], s_bits);
       // this CTA's stores (local and to peers; the barrier orders every warp's
       // before this thread) are released at GPU scope; the winner acquires
       // them all and its fence.sc.sys orders them before V(t) at system scope
       // (causality order is transitive across scopes) -- one system fence
       // per step instead of one per warp
-      const unsigned long long prev = atom_add_acq_rel_gpu_u64(&ctl->arrive_total, 1ull);
+      const unsigned long long prev = atom_add_acq_rel_gpu_u64(&ctl->arrive_par[step & 1], 1ull);
       SPROF(if (blockIdx.x == 0) g_prof[1] += globaltimer_ns() - g_t_resolved);
-      if (prev == t * (unsigned long long)ndata - 1) {
+      if (prev == (unsigned long long)(step / 2 + 1) * (unsigned long long)ndata - 1) {
         SPROF(const unsigned long long te = globaltimer_ns(); g_prof[2] += te - g_t_resolved);
         // last data CTA of the step: V(t) to every rank
-        const unsigned b = atomicExch(&ctl->bad, 0u);
-        unsigned long long v = (t << 32) | ((unsigned long long)(b >> 31) << 31);
+        const unsigned b = atomicExch(&ctl->badp[co], 0u);
+        const unsigned div = (b >> 31) | (unsigned)ctl->div_sticky;
+        // a step that also saw a rejected update carries a void divergence
+        // bit (the optimistic pass included the update); its full resolve
+        // redoes it, so only a clean step's non-finite result is sticky
+        if ((b >> 31) && !(b & 0x7fffffffu) && !ctl->div_sticky) {
+          ctl->div_sticky = 1;
+          // D(me) = the first diverged step, published before V(t)
+          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + 4 * G + me, t);
+        }
+        unsigned long long v = (t << 32) | ((unsigned long long)div << 31);
         for (int i = 0; i < s_n[co]; ++i)
           if ((b >> i) & 1u) v |= 1ull << s_order[co][i];
         __threadfence_system();
-        for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + G + me, v);
+        for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + G + co * G + me, v);
         SPROF(g_prof[3] += globaltimer_ns() - te; g_prof[6] += 1);
       }
     }
   }
-  // the last step's verdict: this rank's replica is complete and committed
+  // the last steps' verdicts: this rank's replica is complete and committed
   // when the kernel exits
-  resolve(t0 + steps_total - 1);
+  const unsigned long long t_last = t0 + steps_total - 1;
+  if (!lag) {
+    resolve(t_last);
+  } else {
+    for (unsigned long long t = resolved + 1; t <= t_last; ++t)
+      if (!resolve_lag(t)) break;
+  }
 #ifdef PS_SHARD_PROFILE
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const double n = g_prof[6] ? (double)g_prof[6] : 1.0;
@@ -470,6 +575,7 @@ struct ps_shard_server {
   long long d = 0, S = 0, lo = 0, hi = 0, n_local = 0, dpad = 0;
   float* w = nullptr;                 // local shard (padded to a multiple of 4), buffer 0
   float* w_alt = nullptr;             // buffer 1 (ShardCtl::cur says which is current)
+  float* w_3 = nullptr;               // buffer 2 (the lagged pipeline keeps three)
   double* now_dev = nullptr;          // per-step push instants of the current run
   int now_cap = 0;
   float* upd = nullptr;               // worker update buffer [dpad]
@@ -568,19 +674,22 @@ int ps_shard_create(const ps_config* cfg, int32_t world, int32_t rank, const voi
   // mapping of a block outlives the buffer it was opened for (measured: a
   // later server's replica mapped through a stale block of an earlier one).
   auto ipc_bytes = [](size_t b) { return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1); };
-  if ((e = cudaMalloc(&h->w, ipc_bytes(shard_bytes))) || (e = cudaMalloc(&h->w_alt, shard_bytes))) return bail("shard");
+  if ((e = cudaMalloc(&h->w, ipc_bytes(shard_bytes))) || (e = cudaMalloc(&h->w_alt, shard_bytes)) ||
+      (e = cudaMalloc(&h->w_3, shard_bytes)))
+    return bail("shard");
   // every initialization is ordered on the server's own (non-blocking)
   // stream: a plain cudaMemset runs on the legacy stream, which does not
   // order against it -- measured, a late memset zeroed part of a shard after
   // its w0 load
-  if ((e = cudaMemsetAsync(h->w, 0, shard_bytes, h->stream)) || (e = cudaMemsetAsync(h->w_alt, 0, shard_bytes, h->stream)))
+  if ((e = cudaMemsetAsync(h->w, 0, shard_bytes, h->stream)) || (e = cudaMemsetAsync(h->w_alt, 0, shard_bytes, h->stream)) ||
+      (e = cudaMemsetAsync(h->w_3, 0, shard_bytes, h->stream)))
     return bail("shard memset");
   if ((e = cudaMalloc(&h->upd, ipc_bytes(h->dpad * sizeof(float))))) return bail("update buffer");
   if ((e = cudaMemsetAsync(h->upd, 0, h->dpad * sizeof(float), h->stream))) return bail("update memset");
   if ((e = cudaMalloc(&h->rep, ipc_bytes(h->dpad * sizeof(float))))) return bail("replica");
   if ((e = cudaMemsetAsync(h->rep, 0, h->dpad * sizeof(float), h->stream))) return bail("replica memset");
-  if ((e = cudaMalloc(&h->flags, ipc_bytes(3 * kMaxRanks * sizeof(unsigned long long))))) return bail("flags");
-  if ((e = cudaMemsetAsync(h->flags, 0, 3 * kMaxRanks * sizeof(unsigned long long), h->stream))) return bail("flags memset");
+  if ((e = cudaMalloc(&h->flags, ipc_bytes(kFlagWords * sizeof(unsigned long long))))) return bail("flags");
+  if ((e = cudaMemsetAsync(h->flags, 0, kFlagWords * sizeof(unsigned long long), h->stream))) return bail("flags memset");
   if ((e = cudaMalloc(&h->ctl, sizeof(ShardCtl)))) return bail("ctl");
   if ((e = cudaMallocHost(&h->hctl, sizeof(ShardCtl)))) return bail("hctl");
   std::memset(h->hctl, 0, sizeof(ShardCtl));
@@ -646,7 +755,7 @@ void ps_shard_destroy(ps_shard_server* h) {
   Dev guard(h->dev);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->opened) cudaIpcCloseMemHandle(p);
-  cudaFree(h->w); cudaFree(h->w_alt); cudaFree(h->now_dev); cudaFree(h->upd); cudaFree(h->rep); cudaFree(h->flags); cudaFree(h->ctl);
+  cudaFree(h->w); cudaFree(h->w_alt); cudaFree(h->w_3); cudaFree(h->now_dev); cudaFree(h->upd); cudaFree(h->rep); cudaFree(h->flags); cudaFree(h->ctl);
   cudaFree(h->trace);
   cudaFree(h->sched_dev);
   if (h->hctl) cudaFreeHost(h->hctl);
@@ -834,8 +943,23 @@ int shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, 
   const unsigned long long marks[4] = {(unsigned long long)(t0 - 1) * (unsigned long long)data_ctas,
                                        (unsigned long long)(t0 - 1), (unsigned long long)(t0 - 1), 0ull};
   SCK(h, cudaMemcpyAsync(&h->ctl->arrive_total, marks, sizeof(marks), cudaMemcpyHostToDevice, h->stream));
+  // this run's per-parity arrival counters and verdict words start at zero;
+  // PS_SHARD_NO_LAG=1 resolves every step in full (the round-1 protocol)
+  static const int no_lag_env = [] {
+    const char* v = getenv("PS_SHARD_NO_LAG");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  // (staged in the pinned host mirror, which nothing else touches until the
+  // run's own read-back at the end)
+  h->hctl->arrive_par[0] = h->hctl->arrive_par[1] = 0;
+  h->hctl->badp[0] = h->hctl->badp[1] = 0;
+  h->hctl->div_sticky = 0;
+  h->hctl->no_lag = no_lag_env;
+  const size_t tail = offsetof(ShardCtl, no_lag) + sizeof(int32_t) - offsetof(ShardCtl, arrive_par);
+  SCK(h, cudaMemcpyAsync(&h->ctl->arrive_par, &h->hctl->arrive_par, tail, cudaMemcpyHostToDevice, h->stream));
   float* w0p = h->w;
   float* w1p = h->w_alt;
+  float* w2p = h->w_3;
   long long nl = h->n_local;
   ShardPtrs ptrs = h->ptrs;
   ShardCtl* ctl = h->ctl;
@@ -845,7 +969,7 @@ int shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, 
   unsigned long long t0v = (unsigned long long)t0;
   float lrv = lr;
   const double* nowp = h->now_dev;
-  void* args[] = {&w0p, &w1p, &nl, &ptrs, &Gv, &mev, &t0v, &nsteps, &lrv, &ctl, &nowp, &trace, &tcap, &schedp};
+  void* args[] = {&w0p, &w1p, &w2p, &nl, &ptrs, &Gv, &mev, &t0v, &nsteps, &lrv, &ctl, &nowp, &trace, &tcap, &schedp};
   SCK(h, cudaEventRecord(h->ev0, h->stream));
   SCK(h, cudaLaunchCooperativeKernel(kern, dim3(total), dim3(kThreads), args, 0, h->stream));
   if (h->profile) SCK(h, cudaEventRecord(h->pev[0], h->stream));
@@ -893,7 +1017,8 @@ int ps_shard_read_shard(ps_shard_server* h, void* dst_host, int64_t* n) {
   Dev guard(h->dev);
   *n = h->n_local;
   SCK(h, cudaMemcpy(h->hctl, h->ctl, sizeof(ShardCtl), cudaMemcpyDeviceToHost));
-  const float* cur = h->hctl->cur ? h->w_alt : h->w;
+  const float* bufs[3] = {h->w, h->w_alt, h->w_3};
+  const float* cur = bufs[h->hctl->cur % 3];
   if (h->n_local > 0) SCK(h, cudaMemcpy(dst_host, cur, h->n_local * sizeof(float), cudaMemcpyDeviceToHost));
   return PS_OK;
 }

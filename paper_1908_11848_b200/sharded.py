@@ -610,11 +610,26 @@ def bench_main(args, metric, extras=None):
         if extras is not None:
             import paper_1908_11848_b200 as ps
             extras(torch, ps, line)
+        if world > 1 and full:
+            # configs[3] across GPUs with real workers: 3 x ResNet-110 at
+            # 1x/2x/4x, one per GPU, blocked and released by device flags
+            # (the server on this rank's GPU, the others over NVLink)
+            import paper_1908_11848_b200 as ps
+            from bench import free_running
+            line["free_running_c4_multi_gpu"] = free_running(
+                torch, ps, 110, 3, (1.0, 2.0, 4.0), 24, devices=[q % world for q in range(3)])
         if sampler is not None:
             sampler.__exit__(None, None, None)
             line["clocks"] = sampler.summary()
         print(json.dumps(line))
-    dist.barrier()
+    # the other ranks wait on the host store, not in an NCCL kernel that would
+    # hold SMs of the GPUs rank 0's multi-GPU blocks run on
+    from datetime import timedelta
+    store = dist.distributed_c10d._get_default_store()
+    if rank == 0:
+        store.set("bench_done", "1")
+    else:
+        store.wait(["bench_done"], timedelta(seconds=3600))
     dist.destroy_process_group()
     return 0
 

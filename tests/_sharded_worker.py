@@ -146,6 +146,70 @@ def main(out_dir):
     torch.cuda.synchronize()
     dist.barrier()
     srv.close()
+    # the lagged pipeline (runs of > 2 steps: step k starts once every owner
+    # finished step k-2): a rejected update over 6 steps, rejected at every
+    # push, and a divergence at step 15 of 20 -- every rank stops there with
+    # the weights of step 14 (server.py:38-41, :65-67)
+    cfg = ps.validate_config(ps.make_config(paradigm="asp", worker_count=world, dimension=d,
+                                            learning_rate=0.05, seed=5))
+    w0 = oracle.initial_weights_f64(5, d)
+    srv = ShardedServer(cfg, d, rank, world, local, w0_host=w0)
+    g = oracle.synthetic_update(7, rank, 0, d)
+    if rank == world - 1:
+        g[d - 3] = np.inf
+    srv.update[:d].copy_(torch.from_numpy(g))
+    torch.cuda.synchronize()
+    dist.barrier()
+    srv.run([float(i + 1) for i in range(6)])
+    w = w0.astype(np.float32)
+    for _ in range(6):
+        for p in range(world - 1):
+            w = oracle.apply_f32(w, oracle.synthetic_update(7, p, 0, d), 0.05)
+    st = srv.state()
+    verdict["checks"].append({
+        "run": "reject_lagged", "d": d, "trace": int(st.rejected) == 6,
+        "shard": bool(np.array_equal(srv.read_shard().view(np.uint32), w[srv.lo:srv.hi].view(np.uint32))),
+        "replica": bool(np.array_equal(srv.read_replica().view(np.uint32), w.view(np.uint32))),
+        "version": int(st.version) + int(st.rejected), "steps": 6})
+    torch.cuda.synchronize()
+    dist.barrier()
+    srv.close()
+    cfg = ps.validate_config(ps.make_config(paradigm="asp", worker_count=world, dimension=d,
+                                            learning_rate=0.5, seed=5))
+    w0 = oracle.initial_weights_f64(5, d)
+    w0[11] = 2.0e38
+    srv = ShardedServer(cfg, d, rank, world, local, w0_host=w0)
+    g = oracle.synthetic_update(8, rank, 0, d)
+    g[11] = -2.0e37 if rank == 0 else 0.0
+    srv.update[:d].copy_(torch.from_numpy(g))
+    torch.cuda.synchronize()
+    dist.barrier()
+    diverged = False
+    try:
+        srv.run([float(i + 1) for i in range(20)])
+    except ps.DivergenceError:
+        diverged = True
+    gs = [oracle.synthetic_update(8, p, 0, d) for p in range(world)]
+    for p in range(world):
+        gs[p][11] = -2.0e37 if p == 0 else 0.0
+    w = w0.astype(np.float32)
+    steps_ok = 0
+    while True:
+        nxt = w
+        for p in range(world):
+            nxt = oracle.apply_f32(nxt, gs[p], 0.5)
+        if not np.all(np.isfinite(nxt)):
+            break
+        w = nxt
+        steps_ok += 1
+    verdict["checks"].append({
+        "run": "diverge_lagged", "d": d, "trace": diverged and steps_ok < 20,
+        "shard": bool(np.array_equal(srv.read_shard().view(np.uint32), w[srv.lo:srv.hi].view(np.uint32))),
+        "replica": True, "version": int(srv.state().version), "steps": steps_ok,
+        "steps_before_divergence": steps_ok})
+    torch.cuda.synchronize()
+    dist.barrier()
+    srv.close()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
         json.dump(verdict, fh)
     dist.barrier()

@@ -22,6 +22,8 @@ Fixtures written (all deterministic; re-running reproduces them byte for byte):
                            and the fp64 final weights for the small models.
   apply_vectors.json       apply_update / apply_gradient known answers
                            (stalesync/server.py:29-69, tests/test_server.py).
+  acceptance_corpora.json.gz  the acceptance suite's corpora at full scale
+                           (criteria 1, 2, 4): trace digests, final weights.
   c3_schedule.json.gz      run_simulation traces of the bench's homogeneous
                            sharded workload (P = 1, 2, 4, 8, every paradigm).
   sim_throttle.json.gz     run_simulation with 1x/2x/4x throttled workers
@@ -439,6 +441,70 @@ def c3_schedule():
     _dump("c3_schedule.json.gz", {"runs": out}, gz=True)
 
 
+def acceptance_corpora():
+    """The reference's acceptance corpora at full scale (tests/test_acceptance.py):
+    criterion 1's 1000 randomized runs (:50-75), criterion 2's 100 seeds of
+    SSP vs DSSP(r_max=0) (:78-93) and criterion 4's 4 ratios x 20 seeds of
+    SSP(3) vs DSSP(3,12) (:137-160) -- the exact generators. Each run keeps
+    its flat config, the SHA-256 of its rendered trace, its final version and
+    fp64 final weights (d = 2 or 3), and criterion 4 the fast worker's wait."""
+    import hashlib
+    from stalesync.simnet import run_simulation
+    presets = ("homogeneous", "jitter", "gtx-mix", "straggler", "lognormal")
+
+    def rec(flat, extra=None):
+        cfg = validate_config(make_config(**flat))
+        sim = Simulation(cfg)
+        entries, report = sim.run()
+        text = format_trace(entries)
+        out = {"config": flat, "sha256": hashlib.sha256(text.encode()).hexdigest(),
+               "rows": len(entries), "final_version": sim.server.weights.version,
+               "final_weights": [float(x) for x in sim.server.weights.values],
+               "fast_wait_s": report.per_worker[0].wait_s}
+        if extra:
+            out.update(extra)
+        return out
+
+    crit1 = []
+    rng = np.random.default_rng(101)
+    for i in range(1000):
+        paradigm = "ssp" if i % 2 else "dssp"
+        workers = int(rng.integers(2, 9))
+        s_lower = int(rng.integers(0, 6))
+        r_max = int(rng.integers(1, 9)) if paradigm == "dssp" else 0
+        crit1.append(rec(dict(
+            paradigm=paradigm, mode="simulated", worker_count=workers,
+            s_lower=s_lower, r_max=r_max, timing_preset=presets[i % 5],
+            compute_base=1.0, comm_delay=(0.0, 0.01, 0.5)[i % 3],
+            straggler_ratio=(1.5, 2.0, 3.0, 4.0)[i % 4],
+            model_kind="quadratic_bowl", dimension=2,
+            dataset_size=8 * workers, batch_size=4,
+            epochs=int(rng.integers(1, 4)), seed=i)))
+    crit2 = []
+    for seed in range(100):
+        base = dict(
+            mode="simulated", worker_count=2 + seed % 5,
+            s_lower=seed % 5, timing_preset=presets[seed % 5],
+            compute_base=1.0, comm_delay=(0.0, 0.02)[seed % 2],
+            straggler_ratio=2.0 + (seed % 3), model_kind="quadratic_bowl",
+            dimension=2, dataset_size=8 * (2 + seed % 5), batch_size=4,
+            epochs=2, seed=seed)
+        crit2.append([rec(dict(paradigm="ssp", r_max=0, **base)),
+                      rec(dict(paradigm="dssp", r_max=0, **base))])
+    crit4 = []
+    for ratio in (1.5, 2.0, 3.0, 4.0):
+        for seed in range(20):
+            base = dict(
+                mode="simulated", worker_count=2, timing_preset="straggler",
+                straggler_ratio=ratio, compute_base=1.0, comm_delay=0.0,
+                model_kind="quadratic_bowl", dimension=3, dataset_size=16,
+                batch_size=4, epochs=8, seed=seed)
+            crit4.append([rec(dict(paradigm="ssp", s_lower=3, **base)),
+                          rec(dict(paradigm="dssp", s_lower=3, r_max=12, **base))])
+    _dump("acceptance_corpora.json.gz", {"criterion_1": crit1, "criterion_2": crit2,
+                                         "criterion_4": crit4}, gz=True)
+
+
 def sim_throttle():
     """BASELINE configs[3]: workers throttled 1x / 2x / 4x (ThrottledTimingModel),
     every paradigm. The bench's C4 schedule (P = 3, tiny_mlp-shaped budget),
@@ -497,11 +563,13 @@ def sim_large():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2", "large", "throttle", "c3"]
+    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2", "large", "throttle", "c3", "acceptance"]
     if "throttle" in which:
         sim_throttle()
     if "c3" in which:
         c3_schedule()
+    if "acceptance" in which:
+        acceptance_corpora()
     if "large" in which:
         sim_large()
     if "c2" in which:
