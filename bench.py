@@ -595,7 +595,10 @@ def torch_workers(torch, ps, iters=48, batch=128):
                 done += 1
             torch.cuda.synchronize()
             wall = time.perf_counter() - t0
-        out[name] = {"iters_per_s": done / wall, "ps_share_of_wall": ps_s / wall,
+        # host wall time inside the drop-in's calls (each ends in a stream sync,
+        # so it includes waiting for the worker's own backward): an upper
+        # bound on the server's share, not a device measurement
+        out[name] = {"iters_per_s": done / wall, "host_time_in_server_calls_share": ps_s / wall,
                      "model": "CIFAR ResNet-20 (272,474 params)", "batch": batch, "workers": 4}
     return out
 

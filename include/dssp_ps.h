@@ -229,6 +229,17 @@ int ps_set_profiling(ps_server* h, int32_t on);
  * host synchronization). */
 int ps_set_producer_stream(ps_server* h, void* cuda_stream);
 
+/* Resident mode: `ctas` > 0 keeps a persistent kernel of that many CTAs on
+ * the GPU that serves ps_apply / ps_decide / ps_push / ps_pull /
+ * ps_read_weights from a pinned, host-mapped mailbox -- no launch and no
+ * stream synchronization per call (the reference's per-call API,
+ * server.py:58-91, at mailbox latency). 0 turns it off. The kernel retires
+ * itself after ~2 s without requests and the next call relaunches it; every
+ * other entry point (state writes, run loops, free-running workers) pauses
+ * it first. Device updates from a producer stream are waited for on the host
+ * (an event synchronization), since no launch carries the stream edge. */
+int ps_set_resident(ps_server* h, int32_t ctas);
+
 /* ------------------------------------------------------------------------
  * Free-running workers on device flags (the threaded runner without the host:
  * runner.py:168-291). Every worker is a CUDA stream; an iteration is the

@@ -105,6 +105,7 @@ SIGNATURES = {
     "ps_last_kernel_ms": (ctypes.c_int, [_P, _PD]),
     "ps_set_profiling": (ctypes.c_int, [_P, _I32]),
     "ps_set_producer_stream": (ctypes.c_int, [_P, _P]),
+    "ps_set_resident": (ctypes.c_int, [_P, _I32]),
     "ps_workers_start": (ctypes.c_int, [_P, _I64, _D]),
     "ps_bind_worker_stream": (ctypes.c_int, [_P, _I32, _P, _P, _P]),
     "ps_enqueue_iteration": (ctypes.c_int, [_P, _I32, _P, ctypes.c_uint64]),

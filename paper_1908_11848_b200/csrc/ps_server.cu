@@ -17,6 +17,8 @@
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -355,8 +357,8 @@ bool host_dma() {
 int apply_small_unroll() {
   static const int u = [] {
     const char* v = getenv("PS_APPLY_SMALL_U");
-    const int x = v ? atoi(v) : 1;
-    return (x == 1 || x == 2 || x == 4) ? x : 1;
+    const int x = v ? atoi(v) : 2;
+    return (x == 1 || x == 2 || x == 4) ? x : 2;
   }();
   return u;
 }
@@ -382,8 +384,12 @@ struct DevGuard {
 // resident update: device or pinned host memory is read in place (the kernel
 // streams a pinned host update over PCIe, no separate copy); pageable host
 // memory and misaligned device views go through staging.
+int res_push(ps_server* h, int worker, const void* g, int g_dtype, int g_on_device, int fuse, double now);
+bool res_active(const ps_server* h);
+
 int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_device, int fuse,
                  double now) {
+  if (res_active(h)) return res_push(h, worker, g, g_dtype, g_on_device, fuse, now);
   if (g_dtype != PS_F32 && g_dtype != PS_F64) return ps_fail(h, PS_E_VALUE, "bad gradient dtype");
   if (!g) return ps_fail(h, PS_E_VALUE, "null gradient");
   const size_t esz = g_dtype == PS_F64 ? 8 : 4;
@@ -422,9 +428,487 @@ int launch_apply(ps_server* h, int worker, const void* g, int g_dtype, int g_on_
   return finish_op(h);
 }
 
+// ---------------------------------------------------------------------------
+// Resident mode (ps_set_resident): the per-call API without a launch or a
+// stream synchronization per call. A persistent kernel of a few CTAs stays on
+// the GPU; the host posts each reference call (apply_gradient, decide_push,
+// handle_push, handle_pull -- server.py:58-91) into a pinned, mapped mailbox
+// and spins on the response the kernel writes back into host memory. CTA 0
+// polls the mailbox over PCIe and forwards the request to the other CTAs
+// through device memory; the last CTA to finish an op commits it (verdict,
+// buffer flip, version, gate decision) exactly like k_apply's last CTA and
+// answers. Weights, gate tables and the cur index are read at L2 (ld.cg):
+// across requests another SM may have written them, and no kernel boundary
+// invalidates L1. An idle kernel retires itself after ~2 s (mbox.alive = 0)
+// and the next call relaunches it, so nothing spins on a GPU forever.
+// ---------------------------------------------------------------------------
+enum { RES_STOP = 0, RES_APPLY = 1, RES_PUSH = 2, RES_DECIDE = 3, RES_PULL = 4 };
+
+struct ResReq {
+  int32_t op, worker;
+  double now;
+  const void* src;       // APPLY / PUSH: the update
+  void* dst;             // PULL: the destination
+  int32_t dtype;         // of src (APPLY / PUSH) or dst (PULL)
+  int32_t host_mem;      // 1: src / dst is pinned host memory
+};
+
+struct ResResp {
+  int32_t status, applied, granted, cur;
+  uint64_t released;
+  int64_t version;
+};
+
+struct ResMbox {                       // pinned host memory, mapped for the device
+  volatile unsigned long long req_seq;
+  unsigned long long _p0[7];
+  ResReq req;
+  unsigned long long _p1[4];
+  volatile unsigned long long resp_seq;
+  volatile int32_t alive;              // the kernel is serving (0: retired / retiring)
+  int32_t _p2;
+  unsigned long long _p3[6];
+  ResResp resp;
+};
+
+struct ResDev {                        // device memory
+  unsigned long long dseq;             // the request CTA 0 forwarded last
+  unsigned long long _p0[7];
+  ResReq req;
+  unsigned long long arrive;           // low: CTAs done, high: non-finite flag counts
+};
+
+struct ResArgs {
+  float* w0;
+  float* w1;
+  long long n, nv;
+  float lr;
+  Ctrl* ctrl;
+  Ctrl* mirror;
+  ResMbox* mbox;                       // device alias of the host mailbox
+  ResDev* rd;
+  unsigned long long seq0;             // first request sequence number to serve
+  unsigned long long idle_ns;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64_v(const volatile unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename G>
+__device__ __forceinline__ float4 res_load_g(const G* g, long long j, bool host);
+template <>
+__device__ __forceinline__ float4 res_load_g<float>(const float* g, long long j, bool host) {
+  const float4* p = reinterpret_cast<const float4*>(g) + j;
+  return host ? __ldcv(p) : __ldcg(p);
+}
+template <>
+__device__ __forceinline__ float4 res_load_g<double>(const double* g, long long j, bool host) {
+  const double2* p = reinterpret_cast<const double2*>(g) + 2 * j;
+  const double2 a = host ? __ldcv(p) : __ldcg(p), b = host ? __ldcv(p + 1) : __ldcg(p + 1);
+  return make_float4((float)a.x, (float)a.y, (float)b.x, (float)b.y);
+}
+
+template <typename G>
+__device__ unsigned res_apply(const ResArgs& a, int cur, const G* g, bool host) {
+  const float4* src = reinterpret_cast<const float4*>(cur ? a.w1 : a.w0);
+  float4* dst = reinterpret_cast<float4*>(cur ? a.w0 : a.w1);
+  unsigned bad = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < a.nv; j += stride) {
+    const float4 gv = res_load_g<G>(g, j, host);
+    const float4 r = apply4(__ldcg(src + j), a.lr, gv);
+    bad |= nonfinite4(gv) ? 1u : 0u;
+    bad |= nonfinite4(r) ? 2u : 0u;
+    __stcg(dst + j, r);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (a.n & 3)) {
+    const long long i = (a.nv << 2) + threadIdx.x;
+    const float* sw = cur ? a.w1 : a.w0;
+    float* dw = cur ? a.w0 : a.w1;
+    const float gi = host ? (float)*(const volatile G*)(g + i) : (float)__ldcg(g + i);
+    const float r = apply1(__ldcg(sw + i), a.lr, gi);
+    bad |= nonfinite(gi) ? 1u : 0u;
+    bad |= nonfinite(r) ? 2u : 0u;
+    __stcg(dw + i, r);
+  }
+  return bad;
+}
+
+template <typename T>
+__device__ void res_pull(const ResArgs& a, int cur, T* dst) {
+  const float4* src = reinterpret_cast<const float4*>(cur ? a.w1 : a.w0);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < a.nv; j += stride) {
+    const float4 v = __ldcg(src + j);
+    if constexpr (sizeof(T) == 4) {
+      reinterpret_cast<float4*>(dst)[j] = v;
+    } else {
+      double2* o = reinterpret_cast<double2*>(dst) + 2 * j;
+      o[0] = make_double2(v.x, v.y);
+      o[1] = make_double2(v.z, v.w);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (a.n & 3)) {
+    const long long i = (a.nv << 2) + threadIdx.x;
+    dst[i] = (T)__ldcg((cur ? a.w1 : a.w0) + i);
+  }
+}
+
+// Warp 0 of the committing CTA: the gate decision on an L2-fresh copy of the
+// tables in shared memory, written back at L2.
+// Only the live words move: the header, the first P entries of each table and
+// the counters (as publish_ctrl).
+__device__ __forceinline__ int live_word(int i, int P) {
+  if (i < 3) return i;
+  if (i < 3 + 5 * P) return 3 + ((i - 3) / P) * PS_MAX_WORKERS + (i - 3) % P;
+  return 3 + 5 * PS_MAX_WORKERS + (i - 3 - 5 * P);
+}
+
+__device__ GateResult res_gate(const ResArgs& a, int worker, double now, ps_gate_state* sg) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long* s8 = reinterpret_cast<unsigned long long*>(sg);
+  unsigned long long* g8 = reinterpret_cast<unsigned long long*>(&a.ctrl->gate);
+  const int P = __ldcg(&a.ctrl->gate.worker_count);
+  const int n = 3 + 5 * P + 4;  // header, tables, deferred / version / rejected / decisions
+  for (int i = lane; i < n; i += 32) { const int w = live_word(i, P); s8[w] = __ldcg(g8 + w); }
+  __syncwarp();
+  const GateResult r = gate_on_push(sg, worker, now);
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) { const int w = live_word(i, P); __stcg(g8 + w, s8[w]); }
+  __syncwarp();
+  return r;
+}
+
+// Warp-collective: the live part of the control block into the host mirror
+// (as publish_ctrl, reading at L2).
+__device__ void res_publish(const ResArgs& a) {
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(a.ctrl);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(a.mirror);
+  const int P = __ldcg(&a.ctrl->gate.worker_count);
+  const int n = 3 + 5 * P + 8;
+  for (int i = threadIdx.x & 31; i < n; i += 32) {
+    int word;
+    if (i < 3) word = i;
+    else if (i < 3 + 5 * P) word = 3 + ((i - 3) / P) * PS_MAX_WORKERS + (i - 3) % P;
+    else word = 3 + 5 * PS_MAX_WORKERS + (i - 3 - 5 * P);
+    d[word] = __ldcg(s + word);
+  }
+}
+
+__device__ void res_respond(const ResArgs& a, unsigned long long seq, int status, int applied, int granted,
+                            unsigned long long released) {
+  // lane 0 of the committing warp
+  ResMbox* m = a.mbox;
+  m->resp.status = status;
+  m->resp.applied = applied;
+  m->resp.granted = granted;
+  m->resp.cur = __ldcg(&a.ctrl->cur);
+  m->resp.released = released;
+  m->resp.version = __ldcg(&a.ctrl->gate.version);
+  __threadfence_system();
+  m->resp_seq = seq;
+}
+
+__global__ void __launch_bounds__(256) k_resident(ResArgs a) {
+  __shared__ ResReq s_req;
+  __shared__ int s_last;
+  __shared__ unsigned s_flags, s_bad;
+  __shared__ ps_gate_state sg;
+  unsigned long long seq = a.seq0;
+  const int lane = threadIdx.x & 31;
+  for (;; ++seq) {
+    if (threadIdx.x == 0) {
+      if (blockIdx.x == 0) {
+        unsigned long long t0 = globaltimer_ns();
+        unsigned backoff = 32;
+        bool got = false;
+        for (;;) {
+          if (ld_acquire_sys_u64_v(&a.mbox->req_seq) == seq) { got = true; break; }
+          if (globaltimer_ns() - t0 > a.idle_ns) {
+            // retire: announce it, then look once more (a request posted
+            // before the host saw alive = 0 is still served)
+            a.mbox->alive = 0;
+            __threadfence_system();
+            if (ld_acquire_sys_u64_v(&a.mbox->req_seq) == seq) { a.mbox->alive = 1; got = true; }
+            break;
+          }
+          __nanosleep(backoff);
+          backoff = backoff < 256 ? backoff * 2 : 256;
+        }
+        ResReq r{};
+        r.op = RES_STOP;
+        if (got) {
+          r.op = *(volatile int32_t*)&a.mbox->req.op;
+          r.worker = *(volatile int32_t*)&a.mbox->req.worker;
+          r.now = *(volatile double*)&a.mbox->req.now;
+          r.src = *(const void* volatile*)&a.mbox->req.src;
+          r.dst = *(void* volatile*)&a.mbox->req.dst;
+          r.dtype = *(volatile int32_t*)&a.mbox->req.dtype;
+          r.host_mem = *(volatile int32_t*)&a.mbox->req.host_mem;
+        }
+        a.rd->req = r;
+        __threadfence();
+        st_release_u64(&a.rd->dseq, seq);
+      } else {
+        unsigned backoff = 32;
+        while (ld_acquire_u64(&a.rd->dseq) != seq) {
+          __nanosleep(backoff);
+          backoff = backoff < 512 ? backoff * 2 : 512;
+        }
+      }
+      ResReq r;
+      r.op = __ldcg(&a.rd->req.op);
+      r.worker = __ldcg(&a.rd->req.worker);
+      r.now = __ldcg(&a.rd->req.now);
+      r.src = (const void*)__ldcg((const unsigned long long*)&a.rd->req.src);
+      r.dst = (void*)__ldcg((const unsigned long long*)&a.rd->req.dst);
+      r.dtype = __ldcg(&a.rd->req.dtype);
+      r.host_mem = __ldcg(&a.rd->req.host_mem);
+      s_req = r;
+      s_bad = 0;
+    }
+    __syncthreads();
+    const ResReq r = s_req;
+    if (r.op == RES_STOP) return;
+    if (r.op == RES_DECIDE) {
+      if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const GateResult g = res_gate(a, r.worker, r.now, &sg);
+        if (lane == 0) {
+          __stcg(&a.ctrl->status, g.status);
+          __stcg(&a.ctrl->granted, (g.status == PS_OK && g.outcome == 0) ? 1 : 0);
+          __stcg((unsigned long long*)&a.ctrl->released, g.released);
+        }
+        __syncwarp();
+        res_publish(a);
+        __syncwarp();
+        if (lane == 0) res_respond(a, seq, g.status, 0, (g.status == PS_OK && g.outcome == 0) ? 1 : 0, g.released);
+      }
+      continue;
+    }
+    const int cur = __ldcg(&a.ctrl->cur);
+    unsigned bad = 0;
+    if (r.op == RES_APPLY || r.op == RES_PUSH) {
+      bad = r.dtype == PS_F64 ? res_apply<double>(a, cur, (const double*)r.src, r.host_mem != 0)
+                              : res_apply<float>(a, cur, (const float*)r.src, r.host_mem != 0);
+    } else {  // RES_PULL
+      if (r.dtype == PS_F64) res_pull<double>(a, cur, (double*)r.dst);
+      else res_pull<float>(a, cur, (float*)r.dst);
+    }
+    bad = __reduce_or_sync(kFull, bad);
+    if (lane == 0 && bad) atomicOr(&s_bad, bad);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (r.host_mem && r.op == RES_PULL) __threadfence_system();  // host stores before the answer
+      const unsigned long long add =
+          1ull | ((unsigned long long)((s_bad & 1u) | ((s_bad & 2u) << 15)) << 32);
+      const unsigned long long prev = atom_add_acq_rel_gpu_u64(&a.rd->arrive, add);
+      s_last = ((unsigned)prev == gridDim.x - 1);
+      s_flags = (unsigned)((prev + add) >> 32);
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x >= 32) continue;
+    // the committing CTA (every CTA's writes acquired through the arrival)
+    int status = PS_OK, applied = 0, granted = 0;
+    unsigned long long released = 0;
+    if (lane == 0) a.rd->arrive = 0;  // nobody arrives again before the answer
+    if (r.op == RES_PULL) {
+      if (lane == 0) {
+        __threadfence_system();
+        res_respond(a, seq, PS_OK, 0, 0, 0);
+      }
+      continue;
+    }
+    if (lane == 0) {
+      const unsigned f = s_flags;
+      if (f & 0xffffu) {
+        status = PS_REJECTED;
+        __stcg(&a.ctrl->gate.rejected, __ldcg(&a.ctrl->gate.rejected) + 1);
+      } else if (f >> 16) {
+        status = PS_E_DIVERGED;
+      } else {
+        __stcg(&a.ctrl->cur, cur ^ 1);
+        __stcg(&a.ctrl->gate.version, __ldcg(&a.ctrl->gate.version) + 1);
+        applied = 1;
+      }
+    }
+    status = __shfl_sync(kFull, status, 0);
+    applied = __shfl_sync(kFull, applied, 0);
+    if (r.op == RES_PUSH && status != PS_E_DIVERGED) {
+      __threadfence();
+      const GateResult g = res_gate(a, r.worker, r.now, &sg);
+      if (g.status != PS_OK) status = g.status;
+      granted = (g.status == PS_OK && g.outcome == 0) ? 1 : 0;
+      released = g.released;
+    }
+    if (lane == 0) {
+      __stcg(&a.ctrl->status, status);
+      __stcg(&a.ctrl->applied, applied);
+      __stcg(&a.ctrl->granted, granted);
+      __stcg((unsigned long long*)&a.ctrl->released, released);
+    }
+    __syncwarp();
+    res_publish(a);
+    __syncwarp();
+    if (lane == 0) res_respond(a, seq, status, applied, granted, released);
+  }
+}
+
 }  // namespace
 
 int ps_order_after_producer(ps_server* h) { return after_producer(h); }
+
+struct ps_resident {
+  int ctas = 0;                 // 0: resident mode off
+  bool running = false;
+  cudaStream_t stream = nullptr;
+  ResMbox* mbox = nullptr;      // pinned host mailbox
+  ResMbox* mbox_dev = nullptr;  // its device alias
+  ResDev* rd = nullptr;
+  unsigned long long seq = 1;   // the next request's sequence number
+  cudaEvent_t ev = nullptr;
+};
+
+namespace {
+
+constexpr unsigned long long kResidentIdleNs = 2ull * 1000 * 1000 * 1000;
+
+int res_launch(ps_server* h) {
+  ps_resident* r = h->res;
+  r->mbox->alive = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  ResArgs a{};
+  a.w0 = h->w[0];
+  a.w1 = h->w[1];
+  a.n = h->d;
+  a.nv = h->d >> 2;  // whole float4s; the n & 3 tail is element-wise
+  a.lr = (float)h->cfg.learning_rate;
+  a.ctrl = h->ctrl;
+  a.mirror = h->hctrl_dev;
+  a.mbox = r->mbox_dev;
+  a.rd = r->rd;
+  a.seq0 = r->seq;
+  a.idle_ns = kResidentIdleNs;
+  // every earlier use of the server's state (on its own stream) is complete
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  k_resident<<<r->ctas, 256, 0, r->stream>>>(a);
+  PS_CK(h, cudaGetLastError());
+  r->running = true;
+  return PS_OK;
+}
+
+bool res_retired(ps_resident* r) {
+  return r->mbox->alive == 0 && cudaStreamQuery(r->stream) == cudaSuccess;
+}
+
+// Post one request and spin on the answer in host memory.
+int res_call(ps_server* h, const ResReq& q, ResResp* out) {
+  ps_resident* r = h->res;
+  int rc;
+  if (!r->running || res_retired(r)) {
+    if (r->running) PS_CK(h, cudaStreamSynchronize(r->stream));
+    if ((rc = res_launch(h))) return rc;
+  }
+  const unsigned long long seq = r->seq;
+  std::memcpy((void*)&r->mbox->req, &q, sizeof(q));
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  r->mbox->req_seq = seq;
+  const auto t0 = std::chrono::steady_clock::now();
+  unsigned long long spins = 0;
+  while (r->mbox->resp_seq != seq) {
+    if ((++spins & 4095) == 0) {
+      const cudaError_t e = cudaStreamQuery(r->stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) return ps_cuda_fail(h, e, "resident server");
+      if (e == cudaSuccess && r->mbox->resp_seq != seq) {
+        // retired before it saw the request: relaunch, it picks it up
+        if ((rc = res_launch(h))) return rc;
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        return ps_fail(h, PS_E_TIMEOUT, "resident server did not answer within 30 s");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  std::memcpy(out, (const void*)&r->mbox->resp, sizeof(*out));
+  r->seq = seq + 1;
+  h->cur = out->cur;
+  return PS_OK;
+}
+
+// Device tensors come from the caller's producer stream: with no kernel
+// launch to carry an event edge, the host waits for that stream's work.
+int res_after_producer(ps_server* h) {
+  if (!h->producer) return PS_OK;
+  ps_resident* r = h->res;
+  if (!r->ev) PS_CK(h, cudaEventCreateWithFlags(&r->ev, cudaEventDisableTiming));
+  PS_CK(h, cudaEventRecord(r->ev, h->producer));
+  PS_CK(h, cudaEventSynchronize(r->ev));
+  return PS_OK;
+}
+
+// Update operand for a resident push: device or pinned host memory in place,
+// anything else staged on the server stream first.
+int res_operand(ps_server* h, const void* g, int g_dtype, int g_on_device, ResReq* q) {
+  if (g_dtype != PS_F32 && g_dtype != PS_F64) return ps_fail(h, PS_E_VALUE, "bad gradient dtype");
+  if (!g) return ps_fail(h, PS_E_VALUE, "null gradient");
+  const size_t bytes = (size_t)h->d * (g_dtype == PS_F64 ? 8 : 4);
+  int rc;
+  q->dtype = g_dtype;
+  if (aligned16(g) && g_on_device) {
+    if ((rc = res_after_producer(h))) return rc;
+    q->src = g;
+    q->host_mem = 0;
+  } else {
+    // host memory (pinned or not): the copy engine into the stage -- a few
+    // resident CTAs reading pinned memory over PCIe are slower than the DMA
+    if (g_on_device && (rc = res_after_producer(h))) return rc;
+    if ((rc = ensure_stage(h, bytes))) return rc;
+    PS_CK(h, cudaMemcpyAsync(h->stage, g, bytes, g_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             h->stream));
+    PS_CK(h, cudaStreamSynchronize(h->stream));
+    q->src = h->stage;
+    q->host_mem = 0;
+  }
+  return PS_OK;
+}
+
+bool res_active(const ps_server* h) { return h->res && h->res->ctas > 0; }
+
+// The kernel published the op's result and the gate tables into the host
+// mirror before answering: the callers read h->hctrl exactly as after a launch.
+int res_push(ps_server* h, int worker, const void* g, int g_dtype, int g_on_device, int fuse, double now) {
+  ResReq q{};
+  q.op = fuse ? RES_PUSH : RES_APPLY;
+  q.worker = worker;
+  q.now = now;
+  int rc = res_operand(h, g, g_dtype, g_on_device, &q);
+  if (rc) return rc;
+  ResResp resp;
+  return res_call(h, q, &resp);
+}
+
+}  // namespace
+
+int ps_resident_pause(ps_server* h) {
+  ps_resident* r = h->res;
+  if (!r || !r->running) return PS_OK;
+  if (r->mbox->alive || cudaStreamQuery(r->stream) != cudaSuccess) {
+    const unsigned long long seq = r->seq;
+    ResReq q{};
+    q.op = RES_STOP;
+    std::memcpy((void*)&r->mbox->req, &q, sizeof(q));
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    r->mbox->req_seq = seq;
+    PS_CK(h, cudaStreamSynchronize(r->stream));
+    // the STOP was consumed unless the kernel retired first: then un-post it
+    r->mbox->req_seq = seq - 1;
+  }
+  PS_CK(h, cudaStreamSynchronize(r->stream));
+  r->running = false;
+  return PS_OK;
+}
+
 
 extern "C" {
 
@@ -509,6 +993,15 @@ int ps_create(const ps_config* cfg, const void* w0_host, int32_t w0_dtype, ps_se
 void ps_destroy(ps_server* h) {
   if (!h) return;
   DevGuard guard(h->dev);
+  if (h->res) {
+    ps_resident_pause(h);
+    if (h->res->stream) cudaStreamDestroy(h->res->stream);
+    if (h->res->mbox) cudaFreeHost(h->res->mbox);
+    cudaFree(h->res->rd);
+    if (h->res->ev) cudaEventDestroy(h->res->ev);
+    delete h->res;
+    h->res = nullptr;
+  }
   if (h->stream) cudaStreamSynchronize(h->stream);
   cudaFree(h->w[0]);
   cudaFree(h->w[1]);
@@ -546,11 +1039,20 @@ int ps_apply(ps_server* h, int32_t worker, const void* g, int32_t g_dtype, int32
 
 int ps_decide(ps_server* h, int32_t worker, double now, int32_t* granted, uint64_t* released) {
   DevGuard guard(h->dev);
-  int rc = mark(h, h->ev0);
-  if (rc) return rc;
-  k_decide<<<1, 32, 0, h->stream>>>(h->ctrl, worker, now, h->hctrl_dev);
-  PS_CK(h, cudaGetLastError());
-  if ((rc = mark(h, h->ev1)) || (rc = finish_op(h))) return rc;
+  int rc;
+  if (h->res && h->res->ctas > 0) {
+    ResReq q{};
+    q.op = RES_DECIDE;
+    q.worker = worker;
+    q.now = now;
+    ResResp resp;
+    if ((rc = res_call(h, q, &resp))) return rc;
+  } else {
+    if ((rc = mark(h, h->ev0))) return rc;
+    k_decide<<<1, 32, 0, h->stream>>>(h->ctrl, worker, now, h->hctrl_dev);
+    PS_CK(h, cudaGetLastError());
+    if ((rc = mark(h, h->ev1)) || (rc = finish_op(h))) return rc;
+  }
   *granted = h->hctrl->granted;
   *released = h->hctrl->released;
   if (h->hctrl->status == PS_E_PROTOCOL)
@@ -601,6 +1103,19 @@ int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_d
   // f32 to host: the copy engine (measured faster than kernel stores over
   // PCIe); f64 to pinned host: the conversion kernel writes it in place
   const bool kernel_dst = dst_on_device || (dst_dtype == PS_F64 && !host_dma() && pinned_host(dst));
+  if (h->res && h->res->ctas > 0 && aligned16(dst) && kernel_dst) {
+    // resident: the persistent kernel copies; the host waits on its answer
+    if (dst_on_device && (rc = res_after_producer(h))) return rc;
+    ResReq q{};
+    q.op = RES_PULL;
+    q.dst = dst;
+    q.dtype = dst_dtype;
+    q.host_mem = dst_on_device ? 0 : 1;
+    ResResp resp;
+    if ((rc = res_call(h, q, &resp))) return rc;
+    if (version) *version = resp.version;
+    return PS_OK;
+  }
   if (aligned16(dst) && kernel_dst) {
     const int grid = grid_for(h, h->nv);
     if (dst_dtype == PS_F32)
@@ -628,6 +1143,7 @@ int ps_read_weights(ps_server* h, void* dst, int32_t dst_dtype, int32_t dst_on_d
 
 int ps_get_state(ps_server* h, ps_gate_state* out) {
   DevGuard guard(h->dev);
+  if (int prc = ps_resident_pause(h)) return prc;
   int rc = sync_ctrl(h);
   if (rc) return rc;
   *out = h->hctrl->gate;
@@ -641,6 +1157,7 @@ int ps_peek_state(const ps_server* h, ps_gate_state* out) {
 
 int ps_set_state(ps_server* h, const ps_gate_state* in) {
   DevGuard guard(h->dev);
+  if (int prc = ps_resident_pause(h)) return prc;
   if (in->worker_count != h->cfg.worker_count || in->paradigm != h->cfg.paradigm)
     return ps_fail(h, PS_E_VALUE, "state does not match the server configuration");
   for (int q = 0; q < in->worker_count; ++q)
@@ -649,6 +1166,29 @@ int ps_set_state(ps_server* h, const ps_gate_state* in) {
   PS_CK(h, cudaMemcpyAsync(&h->ctrl->gate, &h->hctrl->gate, sizeof(ps_gate_state),
                            cudaMemcpyHostToDevice, h->stream));
   PS_CK(h, cudaStreamSynchronize(h->stream));
+  return PS_OK;
+}
+
+int ps_set_resident(ps_server* h, int32_t ctas) {
+  DevGuard guard(h->dev);
+  if (ctas < 0 || ctas > h->sm_count) return ps_fail(h, PS_E_VALUE, "resident CTAs must be in [0, SM count]");
+  if (int rc = ps_resident_pause(h)) return rc;
+  if (ctas == 0) {
+    if (h->res) h->res->ctas = 0;
+    return PS_OK;
+  }
+  if (!h->res) {
+    h->res = new ps_resident();
+    ps_resident* r = h->res;
+    PS_CK(h, cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+    PS_CK(h, cudaHostAlloc((void**)&r->mbox, sizeof(ResMbox), cudaHostAllocMapped));
+    std::memset((void*)r->mbox, 0, sizeof(ResMbox));
+    PS_CK(h, cudaHostGetDevicePointer((void**)&r->mbox_dev, r->mbox, 0));
+    PS_CK(h, cudaMalloc(&r->rd, sizeof(ResDev)));
+    PS_CK(h, cudaMemset(r->rd, 0, sizeof(ResDev)));
+    PS_CK(h, cudaDeviceSynchronize());
+  }
+  h->res->ctas = ctas;
   return PS_OK;
 }
 

@@ -266,13 +266,18 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
   const bool lag = (sched == nullptr) && steps > 2 && ld_relaxed_s32(&ctl->no_lag) == 0;
   unsigned long long R = 0;                  // rejected workers of this run (lag mode)
   // commit step t (relative index k): buffer (c0 + k + 1) % 3 becomes current
+  // (the rejected updates of step t: its own verdict bits plus every pusher of
+  // the step already known to be rejected this run -- those were skipped)
   auto commit = [&](unsigned long long t, unsigned long long rej) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const int k = (int)(t - t0);
       ctl->cur = (c0 + k + 1) % 3;
       const int co = (int)(t & 1);
-      ctl->gate.version += s_n[co] - __popcll(rej);
-      ctl->gate.rejected += __popcll(rej);
+      unsigned long long pushers = 0;
+      for (int i = 0; i < s_n[co]; ++i) pushers |= 1ull << s_order[co][i];
+      const unsigned long long eff = (rej | R) & pushers;
+      ctl->gate.version += s_n[co] - __popcll(eff);
+      ctl->gate.rejected += __popcll(eff);
     }
   };
   auto stop_diverged = [&](unsigned long long tdiv) {
@@ -403,7 +408,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
     } else if (step == 1) {
       if (!resolve(t0)) return;
       resolved = t0;
-    } else if (step >= 2) {
+    } else if (step >= 2 && t - 2 > resolved) {  // (step 2: t0 was resolved in full at step 1)
       if (!resolve_lag(t - 2)) return;
       resolved = t - 2;
     }

@@ -1734,6 +1734,7 @@ extern "C" {
 
 int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
   DevGuard guard(h->dev);
+  if (int prc = ps_resident_pause(h)) return prc;
   std::memset(res, 0, sizeof(*res));
   const int P = h->cfg.worker_count;
   if (sc->budget < 0) return ps_fail(h, PS_E_VALUE, "budget must be >= 0");
@@ -1907,6 +1908,7 @@ int ps_sim_run(ps_server* h, const ps_sim_config* sc, ps_sim_result* res) {
 int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const float* synthetic,
                   int32_t n_synthetic, int32_t reset_gate, int32_t data_ctas, ps_sim_result* res) {
   DevGuard guard(h->dev);
+  if (int prc = ps_resident_pause(h)) return prc;
   std::memset(res, 0, sizeof(*res));
   const int P = h->cfg.worker_count;
   if (n < 0 || (n > 0 && !calls)) return ps_fail(h, PS_E_VALUE, "bad call list");

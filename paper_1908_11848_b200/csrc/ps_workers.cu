@@ -471,6 +471,7 @@ int ps_workers_start(ps_server* h, int64_t log_cap, double time_scale) {
   DevGuardW guard(h->dev);
   if (log_cap < 1) return ps_fail(h, PS_E_VALUE, "log capacity must be >= 1");
   if (!(time_scale > 0)) return ps_fail(h, PS_E_VALUE, "time_scale must be > 0");
+  if (int prc = ps_resident_pause(h)) return prc;
   PS_CK(h, cudaStreamSynchronize(h->stream));
   if (!h->wrt) {
     h->wrt = new ps_worker_rt();

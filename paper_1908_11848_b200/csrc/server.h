@@ -26,6 +26,7 @@ struct ps_sim_buffers {
 };
 
 struct ps_worker_rt;  // ps_workers.cu: free-running workers on device flags
+struct ps_resident;   // ps_server.cu: the persistent per-call server (ps_set_resident)
 
 struct ps_server {
   ps_config cfg{};
@@ -51,7 +52,12 @@ struct ps_server {
   std::string err;
   ps_sim_buffers sim;
   ps_worker_rt* wrt = nullptr;
+  ps_resident* res = nullptr;
 };
+
+// Stop the resident per-call kernel (if running) before any other use of the
+// server's device state; the next per-call op relaunches it.
+int ps_resident_pause(ps_server* h);
 
 void ps_workers_free(ps_server* h);
 

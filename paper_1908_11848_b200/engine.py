@@ -197,6 +197,11 @@ class Engine:
         self.lib.ps_last_kernel_ms(self._h, ctypes.byref(ms))
         return ms.value
 
+    def set_resident(self, ctas=16):
+        """Serve the per-op calls from a persistent kernel through a host-mapped
+        mailbox (no launch / stream sync per call); 0 turns it off."""
+        self.check(self.lib.ps_set_resident(self._h, int(ctas)))
+
     def set_profiling(self, on=True):
         """Bracket every per-op launch with CUDA events (last_kernel_ms)."""
         self.lib.ps_set_profiling(self._h, 1 if on else 0)

@@ -94,7 +94,11 @@ def apply_update(weights, g, learning_rate: float, device: int = 0) -> WeightVec
 
 
 class ParameterServer:
-    def __init__(self, config, dimension: int, policy=None, device: int = 0):
+    """``resident=N`` (N > 0) serves every call from a persistent N-CTA kernel
+    through a host-mapped mailbox instead of a launch + stream sync per call
+    (include/dssp_ps.h, ps_set_resident)."""
+
+    def __init__(self, config, dimension: int, policy=None, device: int = 0, resident=None):
         self.config = config
         self.dimension = int(dimension)
         self._engine = Engine(config.paradigm, config.worker_count, config.staleness.s_lower,
@@ -106,6 +110,11 @@ class ParameterServer:
         self._fused = isinstance(policy, SyncPolicy) and policy._engine is self._engine
         self.pending: dict = {}
         self._cache = None
+        if resident is None:  # PS_RESIDENT: a process-wide default (the tests run both modes)
+            import os
+            resident = int(os.environ.get("PS_RESIDENT", "0") or 0)
+        if resident:
+            self._engine.set_resident(resident)
 
     @property
     def clocks(self):

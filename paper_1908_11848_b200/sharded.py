@@ -371,7 +371,7 @@ def torch_workers_bench(world, rank, local, warm, steps, batch=128):
             ps_ms += step(i)
         torch.cuda.synchronize()
         wall = max_over_ranks(time.perf_counter() - t0)
-        out[name] = {"iters_per_s": steps * world / wall, "server_share_of_wall": ps_ms * 1e-3 / wall,
+        out[name] = {"iters_per_s": steps * world / wall, "server_device_share_of_wall": ps_ms * 1e-3 / wall,
                      "model": "ResNet-50 (torchvision, 10 classes, 23,528,522 params)",
                      "batch_per_worker": batch, "workers": world}
         torch.cuda.synchronize()

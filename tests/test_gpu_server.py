@@ -12,6 +12,15 @@ pytestmark = pytest.mark.gpu
 ps = pytest.importorskip("paper_1908_11848_b200")
 
 
+@pytest.fixture(autouse=True, params=[0, 16], ids=["launch", "resident"])
+def serving_mode(request, monkeypatch):
+    """Every test runs twice: one launch + sync per call, and the resident
+    per-call server (a persistent 16-CTA kernel behind a host-mapped mailbox,
+    ps_set_resident)."""
+    monkeypatch.setenv("PS_RESIDENT", str(request.param))
+    return request.param
+
+
 def _server(paradigm="asp", workers=2, dimension=2, **kw):
     cfg = ps.validate_config(ps.make_config(paradigm=paradigm, worker_count=workers,
                                             dimension=dimension, **kw))
@@ -206,3 +215,25 @@ def test_open_loop_replay_of_reference_call_logs():
                 assert server.handle_pull(p).version == call[2], run["name"]
         want, _ = oracle.replay_open_loop(run, d, seed=0)
         assert np.array_equal(_bits(server.weights.values), _bits(want)), run["name"]
+
+
+def test_resident_server_retires_when_idle_and_relaunches(serving_mode):
+    """The persistent kernel retires after ~2 s without requests (nothing
+    spins on the GPU forever) and the next call relaunches it; state reads
+    and writes pause it in between."""
+    if not serving_mode:
+        pytest.skip("resident mode only")
+    import time
+    d = 4099
+    server = _server("ssp", 2, d, s_lower=1, learning_rate=0.05, seed=1)
+    w = oracle.initial_weights_f64(1, d).astype(np.float32)
+    for k in range(4):
+        g = oracle.synthetic_update(9, k % 2, k, d)
+        server.handle_push(ps.GradientVector(g, k % 2, k), float(k))
+        w = oracle.apply_f32(w, g, 0.05)
+        if k == 1:
+            time.sleep(2.6)          # the kernel retires here
+        if k == 2:
+            server.engine.refresh()  # ps_get_state pauses it
+    assert np.array_equal(_bits(server.weights.values), _bits(w))
+    assert server.weights.version == 4

@@ -8,6 +8,8 @@ from paper_1908_11848_b200.engine import Engine
 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 272_474
 eng = Engine("asp", 4, 0, 0, 0.05, d)
+if int(os.environ.get("PS_RESIDENT", "0") or 0):
+    eng.set_resident(int(os.environ["PS_RESIDENT"]))
 g_dev = torch.randn(d, device="cuda") * 1e-3
 g_host = torch.randn(d).mul_(1e-3).pin_memory().numpy()
 out_dev = torch.empty(d, device="cuda")
