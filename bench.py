@@ -318,7 +318,9 @@ def cpu_sample_main(args):
     for r in range(world):
         lo, hi = shard_range(d, world, r)
         shards.append(_fp32_checksums(w[lo:hi]))
+    extra = cpu_side_lines(world)
     print(json.dumps({"cpu_baseline": {
+        **extra,
         "value": value, "unit": "updates/s", "cores": 1, "kind": kind,
         "sample": f"{len(secs)} push groups of {world} updates of the same C3 workload, "
                   + ("stalesync 0.1.0 unmodified (oracle/_ref)" if kind == "reference"
@@ -415,6 +417,50 @@ def free_running(torch, ps, depth, P, mults, iters, batch=128, devices=None):
             "worker_gpus": list(devices), "server_gpu": devices[0],
             "slowdowns": list(mults), "single_worker_iteration_ms": base_ms,
             "host_syncs_per_run": 1, "per_paradigm": out}
+
+
+def cpu_side_lines(world):
+    """BASELINE.md section 2's other CPU figures, on the same pinned core:
+    the reference's end-to-end run_simulation of configs[0] ("C1",
+    simnet.py:211-218), and -- labelled as NOT the reference -- an fp32
+    numpy in-place restatement of the C3 push group (np.multiply into a
+    temporary, np.subtract in place: bit-identical to the kernels' arithmetic)."""
+    out = {}
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "stalesync")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        from stalesync.config import make_config, validate_config
+        from stalesync.simnet import run_simulation
+        cfg = validate_config(make_config(
+            paradigm="dssp", worker_count=4, s_lower=3, r_max=12, timing_preset="gtx-mix",
+            compute_base=1.0, comm_delay=0.05, model_kind="tiny_mlp", dimension=3072,
+            dataset_size=512, batch_size=32, learning_rate=0.01, epochs=25, seed=0))
+        t0 = time.perf_counter()
+        _, report = run_simulation(cfg)
+        dt = time.perf_counter() - t0
+        out["reference_run_simulation_c1"] = {
+            "seconds": dt, "updates": report.updates_total,
+            "updates_per_s": report.updates_total / dt,
+            "config": "BASELINE configs[0]: tiny_mlp 3072->8->1 (24,593 params), P=4, DSSP(3,12), "
+                      "gtx-mix, 25 epochs (SURVEY.md 8(d))"}
+    d = C3_DIM
+    rng = np.random.default_rng(3)
+    w = rng.uniform(-0.5, 0.5, d).astype(np.float32)
+    g = rng.standard_normal(d, dtype=np.float32)
+    tmp = np.empty_like(w)
+    lr = np.float32(0.05)
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < 3.0 or reps < 2:
+        for _ in range(world):
+            np.multiply(g, lr, out=tmp)
+            np.subtract(w, tmp, out=w)
+        reps += 1
+    dt = time.perf_counter() - t0
+    out["fp32_numpy_restatement_not_reference"] = {
+        "updates_per_s": reps * world / dt, "gb_per_s": reps * world * 12 * d / dt / 1e9,
+        "note": "numpy fp32 in place, 1 core, the C3 push group's applies only (no gate, no pull)"}
+    return out
 
 
 def _run_cpu_child(extra):

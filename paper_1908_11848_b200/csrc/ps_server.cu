@@ -68,14 +68,16 @@ struct Vec4Load<double> {
 // the host reads every op's result and the gate tables without a D2H copy.
 // Only the live part crosses PCIe: the header, the first P entries of each
 // 64-slot gate table, the gate counters and the op result (3 + 5P + 8 words).
-__device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* mirror) {
+// An apply alone changes none of the tables: then only the counters and the
+// result cross PCIe (8 words).
+__device__ __forceinline__ void publish_ctrl(const Ctrl* ctrl, Ctrl* mirror, bool tables = true) {
   static_assert(sizeof(ps_gate_state) == 8 * (3 + 5 * PS_MAX_WORKERS + 4), "gate layout");
   static_assert(sizeof(Ctrl) == sizeof(ps_gate_state) + 32, "ctrl layout");
   const unsigned long long* s = reinterpret_cast<const unsigned long long*>(ctrl);
   unsigned long long* d = reinterpret_cast<unsigned long long*>(mirror);
-  const int P = ctrl->gate.worker_count;
+  const int P = tables ? ctrl->gate.worker_count : 0;
   const int n = 3 + 5 * P + 8;
-  for (int i = threadIdx.x & 31; i < n; i += 32) {
+  for (int i = (threadIdx.x & 31) + (tables ? 0 : 3); i < n; i += 32) {
     int word;
     if (i < 3) word = i;                                              // header
     else if (i < 3 + 5 * P) word = 3 + ((i - 3) / P) * PS_MAX_WORKERS + (i - 3) % P;  // tables
@@ -186,7 +188,7 @@ k_apply(float* __restrict__ w0, float* __restrict__ w1, const G* __restrict__ g,
     }
   }
   __syncwarp();
-  publish_ctrl(ctrl, mirror);
+  publish_ctrl(ctrl, mirror, fuse != 0);
 }
 
 __global__ void k_decide(Ctrl* ctrl, int worker, double now, Ctrl* mirror) {

@@ -581,8 +581,11 @@ def bench_main(args, metric, extras=None):
                 "frac": achieved / 770.0, "frac_vs_900": achieved / 900.0,
                 "traffic": (nvl_delta or {}).get("data_rx_kib"),
                 "traffic_counters": nvl_delta,
-                "traffic_note": "NVML NVLink data counters of rank 0's GPU around the timed DSSP "
-                                "run, bytes per step (rx = what this GPU received)",
+                "traffic_note": "NVML NVLink data counters of rank 0's GPU around the timed DSSP run, "
+                                "bytes per step, when the box supports them (these report "
+                                "NOT_SUPPORTED: profiles/r2_nvml_probe.txt); ncu cannot attach to a "
+                                "multi-rank run, so the link-byte evidence is the single-process ncu "
+                                "capture of the P2P push/pull kernels, profiles/r2_ncu_nvlink_probe.csv",
                 "peak_kind": "measured peer copy per direction (B200_PROFILING.md); frac_vs_900 "
                              "against the NVLink 5 spec",
                 "kernel": "k_shard_run (persistent; whole step: push, apply, pull, verdict, gate)",

@@ -200,6 +200,8 @@ class ReplayReport:
     rejected: int
     pushes: int
     device_ms: float
+    control_ms: float = 0.0   # gate warp: start -> last decision (%globaltimer)
+    data_ms: float = 0.0      # start -> last data warp done
 
     @property
     def decisions(self) -> list:
@@ -250,7 +252,8 @@ class DeviceReplay:
             raw = raw[:n]
         self.engine.refresh(sync=False)  # the run already mirrored the control block
         return ReplayReport(raw=raw, applied=res.applied, rejected=res.rejected,
-                            pushes=res.pushes, device_ms=res.device_ms)
+                            pushes=res.pushes, device_ms=res.device_ms, control_ms=res.control_ms,
+                            data_ms=res.data_ms)
 
     def replica(self, worker, buf):
         """The weights pull k of `worker` materialized, for (k + 1) % 2 == buf."""

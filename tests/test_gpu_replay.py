@@ -165,3 +165,20 @@ def test_replay_empty_stream_and_worker_limit():
     with pytest.raises(ValueError):
         DeviceReplay(big, [("pull", 0)], torch.zeros(56, 1, 8, device="cuda"), 1).run()
     big.close()
+
+
+def test_resident_update_layout_is_validated():
+    """The C-ABI takes the resident updates as a bare pointer: the Python side
+    rejects anything but a contiguous fp32 [P, count, round_up(d,4)] CUDA
+    tensor on the engine's device (misaligned float4 reads otherwise)."""
+    eng = Engine("asp", 2, 0, 0, 0.05, 10)
+    calls = [("apply", 0), ("decide", 0, 1.0)]
+    for bad in (torch.zeros(2, 1, 10, device="cuda"),                  # d not padded to 12
+                torch.zeros(2, 1, 12, device="cuda", dtype=torch.float64),
+                torch.zeros(2, 2, 12, device="cuda"),                  # count mismatch
+                torch.zeros(2, 1, 24, device="cuda")[:, :, ::2],       # not contiguous
+                torch.zeros(2, 1, 12)):                                 # host tensor
+        with pytest.raises(ValueError):
+            DeviceReplay(eng, calls, bad, 1)
+    DeviceReplay(eng, calls, torch.zeros(2, 1, 12, device="cuda"), 1).run()
+    eng.close()

@@ -13,8 +13,14 @@ name = sys.argv[1] if len(sys.argv) > 1 else "dssp"
 s, r = {p: (a, b) for p, a, b in PARADIGMS}[name]
 d = C2_DIM
 calls, _ = reference_calls(name)
+mode = sys.argv[2] if len(sys.argv) > 2 else "full"
+if mode == "gate":      # decides only: the gate warp alone
+    calls = [c for c in calls if c[0] == "decide"]
+elif mode == "data":    # pulls and applies only: the data warps alone
+    calls = [c for c in calls if c[0] != "decide"]
 eng = Engine(name, 4, s, r, 0.05, d, w0=initial_weights_f64(c2_config(name, s, r), d))
 rp = DeviceReplay(eng, calls, torch.from_numpy(synthetic_host(4, 2, d)).cuda(), 2)
 for _ in range(3):
     rr = rp.run(decisions=False)
-print(name, "ms", rr.device_ms, "decides", sum(1 for c in calls if c[0] == "decide"), "calls", len(calls))
+print(name, mode, "device_ms", round(rr.device_ms, 4), "gate_ms", round(rr.control_ms, 4), "data_ms", round(rr.data_ms, 4),
+      "decides", sum(1 for c in calls if c[0] == "decide"), "calls", len(calls))
