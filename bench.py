@@ -504,7 +504,7 @@ def apply_sweep(torch, ps, hbm_peak):
         eng.set_profiling(True)
         g = torch.randn(d, device="cuda", dtype=torch.float32)
         dst = torch.empty(d, device="cuda", dtype=torch.float32)
-        ap, pl = [], []
+        ap, pl, fl = [], [], []
         for it in range(8):
             flush_l2(torch, flush)
             torch.cuda.synchronize()
@@ -516,13 +516,17 @@ def apply_sweep(torch, ps, hbm_peak):
             eng.read(out=dst)
             if it >= 3:
                 pl.append(eng.last_kernel_ms())
+                fl.append(eng.profile_floor_ms())
         eng.close()
-        a_ms, p_ms = statistics.median(ap), statistics.median(pl)
+        a_ms, p_ms, f_ms = statistics.median(ap), statistics.median(pl), statistics.median(fl)
         out.append({"mbytes": mb, "d": d,
                     "apply_ms": round(a_ms, 4), "apply_gbs": round(12 * d / a_ms / 1e6, 1),
                     "apply_frac": round(12 * d / a_ms / 1e6 / hbm_peak, 3),
                     "pull_ms": round(p_ms, 4), "pull_gbs": round(8 * d / p_ms / 1e6, 1),
-                    "pull_frac": round(8 * d / p_ms / 1e6 / hbm_peak, 3)})
+                    "pull_frac": round(8 * d / p_ms / 1e6 / hbm_peak, 3),
+                    # the same event bracket around an empty kernel: the launch
+                    # floor inside every figure above
+                    "empty_kernel_ms": round(f_ms, 4)})
         del g, dst
     del flush
     torch.cuda.empty_cache()

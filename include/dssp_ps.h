@@ -220,6 +220,9 @@ int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, 
  * events cost two API calls per op, so they are off on the hot path). */
 int ps_last_kernel_ms(ps_server* h, double* ms);
 int ps_set_profiling(ps_server* h, int32_t on);
+/* The same bracket around an empty kernel: the floor every per-op figure
+ * above contains (launch as the GPU sees it + the two timestamps). */
+int ps_profile_floor(ps_server* h, double* ms);
 
 /* Device-pointer updates and pull destinations are usually produced/consumed
  * on the caller's own CUDA stream (a cudaStream_t passed as an opaque

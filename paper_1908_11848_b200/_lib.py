@@ -104,6 +104,7 @@ SIGNATURES = {
     "ps_sim_losses": (ctypes.c_int, [_P, _PI64, _PD, _I64, _PI64]),
     "ps_last_kernel_ms": (ctypes.c_int, [_P, _PD]),
     "ps_set_profiling": (ctypes.c_int, [_P, _I32]),
+    "ps_profile_floor": (ctypes.c_int, [_P, _PD]),
     "ps_set_producer_stream": (ctypes.c_int, [_P, _P]),
     "ps_set_resident": (ctypes.c_int, [_P, _I32]),
     "ps_workers_start": (ctypes.c_int, [_P, _I64, _D]),

@@ -1199,6 +1199,22 @@ int ps_last_kernel_ms(ps_server* h, double* ms) {
   return PS_OK;
 }
 
+int ps_profile_floor(ps_server* h, double* ms) {
+  // the profiling bracket around an empty kernel: what every per-op
+  // last_kernel_ms figure contains besides the op itself (the launch as the
+  // GPU sees it and the two timestamps)
+  DevGuard guard(h->dev);
+  k_spin<<<1, 32, 0, h->stream>>>(kProfileSpinNs);
+  PS_CK(h, cudaEventRecord(h->ev0, h->stream));
+  k_spin<<<1, 32, 0, h->stream>>>(0);
+  PS_CK(h, cudaEventRecord(h->ev1, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
+  float e = 0.f;
+  PS_CK(h, cudaEventElapsedTime(&e, h->ev0, h->ev1));
+  *ms = e;
+  return PS_OK;
+}
+
 int ps_set_profiling(ps_server* h, int32_t on) {
   h->profile = on ? 1 : 0;
   return PS_OK;

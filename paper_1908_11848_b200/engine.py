@@ -202,6 +202,12 @@ class Engine:
         mailbox (no launch / stream sync per call); 0 turns it off."""
         self.check(self.lib.ps_set_resident(self._h, int(ctas)))
 
+    def profile_floor_ms(self):
+        """The profiling bracket around an empty kernel (ps_profile_floor)."""
+        ms = ctypes.c_double(0)
+        self.check(self.lib.ps_profile_floor(self._h, ctypes.byref(ms)))
+        return ms.value
+
     def set_profiling(self, on=True):
         """Bracket every per-op launch with CUDA events (last_kernel_ms)."""
         self.lib.ps_set_profiling(self._h, 1 if on else 0)
