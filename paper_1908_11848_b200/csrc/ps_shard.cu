@@ -56,6 +56,22 @@ constexpr int kThreads = 256;
 // per-rank flag words written by peers: ready[G] | V(t) by step parity [2][G]
 // | F(t) redo done [G] | D first diverged step [G]
 constexpr int kFlagWords = 5 * kMaxRanks;
+// streaming-loop shape (build-time knobs for tuning experiments): minimum
+// resident CTAs per SM the register budget must allow, and float4 per thread
+// per trip for G <= 2 / <= 4 / more
+#ifndef PS_SHARD_MINB
+#define PS_SHARD_MINB 2
+#endif
+#ifndef PS_SHARD_U2
+#define PS_SHARD_U2 4
+#endif
+#ifndef PS_SHARD_U4
+#define PS_SHARD_U4 2
+#endif
+#ifndef PS_SHARD_U8
+#define PS_SHARD_U8 1
+#endif
+__host__ __device__ constexpr int shard_unroll(int g) { return g <= 2 ? PS_SHARD_U2 : g <= 4 ? PS_SHARD_U4 : PS_SHARD_U8; }
 constexpr unsigned long long kTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
 struct ShardPtrs {
@@ -131,7 +147,7 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
 }
 
 template <int G_MAX>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, PS_SHARD_MINB)
 k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ w2, long long n_local, ShardPtrs P, int G,
             int me, unsigned long long t0, int steps, float lr, ShardCtl* ctl, const double* now,
             ps_trace_row* trace, long long trace_cap, const int* sched) {
@@ -254,7 +270,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
   __shared__ unsigned s_pull[2];   // workers whose replica the step writes
   const long long nv = (n_local + 3) >> 2;
   const long long lo = P.lo[me];
-  constexpr int U = G_MAX <= 2 ? 4 : G_MAX <= 4 ? 2 : 1;
+  constexpr int U = shard_unroll(G_MAX);
   const long long stride = (long long)ndata * kThreads * U;
   const long long first = (long long)blockIdx.x * kThreads * U + threadIdx.x;
   // buffer i of the rotation, by selects (a dynamically indexed array would
@@ -918,7 +934,7 @@ int shard_run(ps_shard_server* h, int64_t t0, int32_t steps, const double* now, 
   // no more streaming CTAs than one trip over the shard needs: idle CTAs
   // would only lengthen every step's election and polling
   {
-    const int U = gsel <= 2 ? 4 : gsel <= 4 ? 2 : 1;  // float4 per thread per trip (k_shard_run)
+    const int U = shard_unroll(gsel);  // float4 per thread per trip (k_shard_run)
     const long long nv = (h->n_local + 3) / 4;
     const long long need_ctas = (nv + (long long)kThreads * U - 1) / ((long long)kThreads * U);
     if (need_ctas + 1 < total) total = (int)(need_ctas > 0 ? need_ctas : 1) + 1;
