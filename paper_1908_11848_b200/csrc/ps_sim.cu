@@ -786,6 +786,7 @@ struct ReplayGate<0> {  // shared-memory tables (gate.cuh), any P <= 64
 // the reference would have raised.
 template <int PM>
 __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
+  __shared__ double2 dq[32];  // this chunk's decides: (now, call index << 32 | worker)
   const int lane = threadIdx.x & 31;
   const int P = a.P;
   ReplayGate<PM> g;
@@ -838,15 +839,23 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
       pushes += nd;
       nd = 0;
     };
-    // the next decide's (worker, now) is fetched while this one is decided
-    int i = md ? __ffs(md) - 1 : -1;
-    int w = __shfl_sync(kFull, c.worker, i & 31);
-    double now = __shfl_sync(kFull, c.now, i & 31);
-    while (i >= 0 && fail < 0) {
-      md &= md - 1;
-      const int ni = md ? __ffs(md) - 1 : -1;
-      const int nw = __shfl_sync(kFull, c.worker, ni & 31);
-      const double nnow = __shfl_sync(kFull, c.now, ni & 31);
+    // the chunk's decides, compacted once into shared memory in call order
+    // (one scatter per chunk): the serial loop then reads its next (call,
+    // worker, now) with one broadcast load issued a decision ahead, instead
+    // of a find-first-set -> shuffle chain per decide on its critical path
+    const int n_dec_chunk = __popc(md);
+    if ((md >> lane) & 1u) {
+      const int slot = __popc(md & ((1u << lane) - 1u));
+      dq[slot] = make_double2(c.now, __longlong_as_double(((long long)lane << 32) | (unsigned)c.worker));
+    }
+    __syncwarp();
+    double2 q = n_dec_chunk ? dq[0] : make_double2(0.0, 0.0);
+    for (int j = 0; j < n_dec_chunk && fail < 0; ++j) {
+      const double2 nq = dq[(j + 1) & 31];  // the next decide's, in flight during this one
+      const long long packed = __double_as_longlong(q.y);
+      const int i = (int)(packed >> 32);
+      const int w = (int)(unsigned)packed;
+      const double now = q.x;
       check_pulls(prev, i);
       if (fail >= 0) break;
 #ifdef PS_SIM_PROFILE
@@ -860,10 +869,9 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
       if (lane == nd) dword = (r.released << 8) | (unsigned)r.outcome;
       nd += 1;
       prev = i + 1;
-      i = ni;
-      w = nw;
-      now = nnow;
+      q = nq;
     }
+    __syncwarp();
     flush_decisions();
     if (fail < 0) check_pulls(prev, limit);
     if (fail < 0 && limit < m) fail = limit;
