@@ -734,6 +734,17 @@ def e2e_batched(torch, ps, calls, synth_host, d, w0, steps=30):
     return applied / dt, h2d, d2h
 
 
+def _safe(line, key, fn):
+    """A side block of the line: its failure is recorded, not fatal to the
+    headline (which is measured and checked before any side block runs)."""
+    try:
+        line[key] = fn()
+    except Exception as exc:  # noqa: BLE001 -- reported in the line itself
+        import traceback
+        line[key] = {"error": f"{type(exc).__name__}: {exc}"[:500],
+                     "where": traceback.format_exc().splitlines()[-3:]}
+
+
 def single_gpu_extras(torch, ps, line):
     """N = 1 blocks beside the C3 headline (rank 0): BASELINE configs[1]
     ("C2") as the reference's recorded request stream served in one kernel,
@@ -842,15 +853,15 @@ def single_gpu_extras(torch, ps, line):
                                 "handle_pull), pinned host buffers"},
         "cpu_baseline": _run_cpu_child(["c2"]),
     }
-    line["sweep_single_gpu"] = apply_sweep(torch, ps, hbm_peak)
-    line["c4_throttled"] = c4_throttled(torch, ps)
-    line["c4_free_running"] = c4_realtime(torch, ps)
-    line["torch_workers_c2"] = torch_workers(torch, ps)
+    _safe(line, "sweep_single_gpu", lambda: apply_sweep(torch, ps, hbm_peak))
+    _safe(line, "c4_throttled", lambda: c4_throttled(torch, ps))
+    _safe(line, "c4_free_running", lambda: c4_realtime(torch, ps))
+    _safe(line, "torch_workers_c2", lambda: torch_workers(torch, ps))
     # north star (4): real workers blocked and released by device flags, the
     # host out of the iteration loop -- C2-shaped (4 x ResNet-20, 2 of them
     # 2.2x slower like gtx-mix) and configs[3] (3 x ResNet-110 at 1x/2x/4x)
-    line["free_running_c2"] = free_running(torch, ps, 20, 4, (1.0, 1.0, 2.2, 2.2), 40)
-    line["free_running_c4"] = free_running(torch, ps, 110, 3, (1.0, 2.0, 4.0), 24)
+    _safe(line, "free_running_c2", lambda: free_running(torch, ps, 20, 4, (1.0, 1.0, 2.2, 2.2), 40))
+    _safe(line, "free_running_c4", lambda: free_running(torch, ps, 110, 3, (1.0, 2.0, 4.0), 24))
 
 
 def main():

@@ -71,6 +71,27 @@ constexpr int kFlagWords = 5 * kMaxRanks;
 #ifndef PS_SHARD_U8
 #define PS_SHARD_U8 1
 #endif
+// cache policy of the streaming loop's accesses (build-time knob): 0 = default;
+// 1 = replica stores evict-first (st.global.cs: nobody on this GPU reads them
+// back in the run); 2 = also the shard loads L1::no_allocate
+#ifndef PS_SHARD_CACHE
+#define PS_SHARD_CACHE 0
+#endif
+__device__ __forceinline__ float4 shard_ld(const float4* p) {
+  if constexpr (PS_SHARD_CACHE >= 2) {
+    // coherent (not .nc: the rotation rewrites this buffer within the kernel)
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+  }
+  return *p;
+}
+__device__ __forceinline__ void shard_st_w(float4* p, const float4& v) { *p = v; }
+__device__ __forceinline__ void shard_st_rep(float4* p, const float4& v) {
+  if constexpr (PS_SHARD_CACHE >= 1) __stcs(p, v);
+  else *p = v;
+}
 __host__ __device__ constexpr int shard_unroll(int g) { return g <= 2 ? PS_SHARD_U2 : g <= 4 ? PS_SHARD_U4 : PS_SHARD_U8; }
 constexpr unsigned long long kTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
@@ -497,7 +518,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
 #pragma unroll
           for (int i = 0; i < G_MAX; ++i)
             if ((live >> i) & 1u) g[u][i] = ld_stream(src[i] + j);
-          x[u] = wsrc[j];
+          x[u] = shard_ld(wsrc + j);
         }
       }
 #pragma unroll
@@ -511,12 +532,12 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
               x[u] = apply4(x[u], lr, g[u][i]);
             }
           dbad |= nonfinite4(x[u]) ? 1u : 0u;
-          wdst[j] = x[u];
+          shard_st_w(wdst + j, x[u]);
           // every worker's pull of this slice (handle_pull, server.py:84-91):
           // stored straight into each replica, G-1 of them over NVLink
 #pragma unroll
           for (int q = 0; q < G_MAX; ++q)
-            if (q < G && ((pullm >> q) & 1u)) reinterpret_cast<float4*>(P.rep[q] + lo)[j] = x[u];
+            if (q < G && ((pullm >> q) & 1u)) shard_st_rep(reinterpret_cast<float4*>(P.rep[q] + lo) + j, x[u]);
         }
       }
     }

@@ -600,27 +600,34 @@ def bench_main(args, metric, extras=None):
         # workload, pinned to one host core, plus the fp32 replay fingerprints
         # of the weights (a separate process: the checker, not the product)
         from bench import cpu_baseline_c3
-        base = cpu_baseline_c3(world, parity["_weights_applies"])
-        line["cpu_baseline"] = base["cpu_baseline"]
-        want = base["fingerprints"]
-        ok_shard = all(rs["shard"] == [want["shards"][i][0], want["shards"][i][1]]
-                       for i, rs in enumerate(parity["_rank_sums"]))
-        ok_rep = all(rs["replica"] == want["replica"] for rs in parity["_rank_sums"])
-        parity["weights_bit_exact_vs_fp32_replay"] = {"shards": ok_shard, "replicas": ok_rep,
-                                                     "applies": parity["_weights_applies"]}
+        try:
+            base = cpu_baseline_c3(world, parity["_weights_applies"])
+            line["cpu_baseline"] = base["cpu_baseline"]
+            want = base["fingerprints"]
+            ok_shard = all(rs["shard"] == [want["shards"][i][0], want["shards"][i][1]]
+                           for i, rs in enumerate(parity["_rank_sums"]))
+            ok_rep = all(rs["replica"] == want["replica"] for rs in parity["_rank_sums"])
+            parity["weights_bit_exact_vs_fp32_replay"] = {"shards": ok_shard, "replicas": ok_rep,
+                                                         "applies": parity["_weights_applies"]}
+        except Exception as exc:  # noqa: BLE001 -- the checker failed, not the engine
+            line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"[:500]}
+            parity["weights_bit_exact_vs_fp32_replay"] = "unchecked (the CPU checker failed)"
         parity.pop("_rank_sums")
         parity.pop("_weights_applies")
+        from bench import _safe
         if extras is not None:
             import paper_1908_11848_b200 as ps
-            extras(torch, ps, line)
+            _safe(line, "_extras", lambda: extras(torch, ps, line))
+            if line.get("_extras") is None:
+                line.pop("_extras", None)
         if world > 1 and full:
             # configs[3] across GPUs with real workers: 3 x ResNet-110 at
             # 1x/2x/4x, one per GPU, blocked and released by device flags
             # (the server on this rank's GPU, the others over NVLink)
             import paper_1908_11848_b200 as ps
             from bench import free_running
-            line["free_running_c4_multi_gpu"] = free_running(
-                torch, ps, 110, 3, (1.0, 2.0, 4.0), 24, devices=[q % world for q in range(3)])
+            _safe(line, "free_running_c4_multi_gpu", lambda: free_running(
+                torch, ps, 110, 3, (1.0, 2.0, 4.0), 24, devices=[q % world for q in range(3)]))
         if sampler is not None:
             sampler.__exit__(None, None, None)
             line["clocks"] = sampler.summary()
