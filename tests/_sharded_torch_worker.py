@@ -6,8 +6,10 @@ replica and whose gradients live IN the server's update buffer (no copies):
 backward writes the push, a run of the sharded server applies every worker's
 update in ticket order and writes the new weights straight into every
 replica. After each step rank 0 checks its replica bit for bit against an
-fp32 replay of the all-gathered gradients in the order the device gate
-recorded (server.py:37; simnet.py:167-201)."""
+fp32 replay of the all-gathered gradients in the ticket order the REFERENCE
+simulator produces for this schedule (tests/golden/c3_schedule.json.gz;
+server.py:37; simnet.py:167-201), and the device gate's trace against the
+same reference rows."""
 
 import json
 import os
@@ -20,6 +22,7 @@ import torch.nn.functional as F
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import oracle  # noqa: E402
 import paper_1908_11848_b200 as ps  # noqa: E402
 from paper_1908_11848_b200.sharded import ShardedServer, homogeneous_push_times  # noqa: E402
 from paper_1908_11848_b200.workers import CifarResNet, flatten_, synthetic_cifar  # noqa: E402
@@ -48,6 +51,9 @@ def main(out_dir):
         w_ref = w0.clone()
         lr32 = torch.tensor(lr, dtype=torch.float32, device="cuda")
         ok = True
+        ref = next(x for x in oracle.load_golden("c3_schedule.json.gz")["runs"]
+                   if x["name"] == f"c3_{paradigm}_p{world}")
+        ref_rows = [ln.split("\t") for ln in ref["trace"].splitlines() if ln.split("\t")[2] == "push_arrive"]
         for step in range(6):
             x, y = batches[step % len(batches)]
             srv.update.zero_()
@@ -56,7 +62,10 @@ def main(out_dir):
             grads = [torch.empty(d, device="cuda") for _ in range(world)]
             dist.all_gather(grads, srv.update[:d].contiguous())
             srv.run(times[step:step + 1])
-            order = [e.worker for e in srv.trace()][-world:]  # this group's ticket order
+            # this group's ticket order as the reference serves it
+            order = [int(row[1]) for row in ref_rows[step * world:(step + 1) * world]]
+            got = [e.render().split("\t") for e in srv.trace()][-world:]
+            ok = ok and got == ref_rows[step * world:(step + 1) * world]
             for q in order:
                 w_ref = w_ref - grads[q] * lr32
             ok = ok and bool(torch.equal(srv.replica[:d].view(torch.int32), w_ref.view(torch.int32)))
