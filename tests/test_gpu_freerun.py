@@ -240,3 +240,34 @@ def test_torch_resnet_workers_on_device_flags():
     assert np.array_equal(eng.read()[0].view(np.uint32), w.view(np.uint32))
     assert np.all(np.isfinite(w))
     eng.close()
+
+
+def test_torch_resnet_workers_on_peer_gpus():
+    """Real ResNet-20 workers on different GPUs of the box (server on GPU 0),
+    throttled 1x/2x/4x: the recorded gradients replayed in ticket order give
+    the server's weights bit for bit; decisions equal the oracle gate's."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from paper_1908_11848_b200.workers import CifarResNet, TorchWorker, synthetic_cifar
+    torch.manual_seed(0)
+    P, iters = 3, 8
+    devs = [p % n for p in range(P)]
+    workers = [TorchWorker(p, CifarResNet(20), synthetic_cifar(1, 32, seed=p, device=f"cuda:{devs[p]}"),
+                           device=f"cuda:{devs[p]}") for p in range(P)]
+    d = workers[0].dimension
+    w0 = workers[0].params[:d].detach().cpu().numpy().astype(np.float64)
+    for wk in workers[1:]:
+        wk.params.copy_(workers[0].params.to(wk.params.device))
+    eng = Engine("dssp", P, 3, 12, 0.01, d, w0=w0, device=0)
+    rings = [torch.zeros(iters, workers[p].params.numel(), device=f"cuda:{devs[p]}") for p in range(P)]
+    cl = FreeRunningCluster(eng, workers, throttle_ns=[0, 1_000_000, 3_000_000])
+    for p in range(P):
+        cl.record(p, rings[p])
+    cl.capture(warmup=1)
+    rep = cl.run(iters)
+    assert rep.pushes == P * iters
+    _check_gate(rep, "dssp", P, 3, 12)
+    w, _ = _replay(rep, [r.cpu().numpy() for r in rings], d, w0.astype(np.float32), 0.01)
+    assert np.array_equal(eng.read()[0].view(np.uint32), w.view(np.uint32))
+    eng.close()
