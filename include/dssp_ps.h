@@ -363,6 +363,11 @@ int ps_shard_read_shard(ps_shard_server* h, void* dst_host, int64_t* n);
 int ps_shard_read_replica(ps_shard_server* h, void* dst_host);
 int ps_shard_get_state(ps_shard_server* h, ps_gate_state* out);
 int ps_shard_trace(ps_shard_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
+/* Diagnosis only: this owner's streaming pass (every worker's update slice in,
+ * the new shard into every replica) `reps` times with no flags and no peer
+ * participation, so a profiler can replay it in one process and read its
+ * NVLink counters. Destroys the replicas' contents. *ms = device time. */
+int ps_shard_stream_probe(ps_shard_server* h, int32_t reps, double* ms);
 /* Diagnosis only: per-kernel event timing (ready / apply / pull, ms summed). */
 int ps_shard_set_profiling(ps_shard_server* h, int32_t on);
 int ps_shard_phase_ms(ps_shard_server* h, double* out3);

@@ -131,6 +131,7 @@ SIGNATURES = {
     "ps_shard_trace": (ctypes.c_int, [_P, ctypes.POINTER(PSTraceRow), _I64, _PI64]),
     "ps_shard_range": (ctypes.c_int, [_I64, _I32, _I32, _PI64, _PI64]),
     "ps_shard_set_profiling": (ctypes.c_int, [_P, _I32]),
+    "ps_shard_stream_probe": (ctypes.c_int, [_P, _I32, _PD]),
     "ps_shard_phase_ms": (ctypes.c_int, [_P, _PD]),
 }
 

@@ -167,6 +167,84 @@ __device__ bool wait_flags(const unsigned long long* f, int n, unsigned long lon
   return true;
 }
 
+// One owner's streaming pass over its shard for one push group (the body of
+// every step of k_shard_run, and of the one-sided NVLink probe): apply the
+// live pushers' slices (`src[i]`, ticket order; G-1 of every G read over
+// NVLink) to the shard in one read of it, write the new shard and store it
+// into every pulling worker's replica (G-1 of them over NVLink), scanning the
+// update slices and results for non-finite values. U consecutive float4 per
+// thread per trip with all slices loaded first: U*G independent 128-bit loads
+// in flight.
+template <int G_MAX, int U>
+__device__ __forceinline__ void stream_pass(const float4* wsrc, float4* wdst, const float4* const (&src)[G_MAX],
+                                            unsigned live, unsigned pullm, const ShardPtrs& P, int G,
+                                            long long lo, float lr, long long first, long long stride,
+                                            long long nv, unsigned& gbad, unsigned& dbad) {
+  for (long long base = first; base < nv; base += stride) {
+    float4 g[U][G_MAX];
+    float4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = base + (long long)u * kThreads;
+      if (j < nv) {
+#pragma unroll
+        for (int i = 0; i < G_MAX; ++i)
+          if ((live >> i) & 1u) g[u][i] = ld_stream(src[i] + j);
+        x[u] = shard_ld(wsrc + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long j = base + (long long)u * kThreads;
+      if (j < nv) {
+#pragma unroll
+        for (int i = 0; i < G_MAX; ++i)
+          if ((live >> i) & 1u) {
+            gbad |= nonfinite4(g[u][i]) ? (1u << i) : 0u;
+            x[u] = apply4(x[u], lr, g[u][i]);
+          }
+        dbad |= nonfinite4(x[u]) ? 1u : 0u;
+        shard_st_w(wdst + j, x[u]);
+        // every worker's pull of this slice (handle_pull, server.py:84-91):
+        // stored straight into each replica, G-1 of them over NVLink
+#pragma unroll
+        for (int q = 0; q < G_MAX; ++q)
+          if (q < G && ((pullm >> q) & 1u)) shard_st_rep(reinterpret_cast<float4*>(P.rep[q] + lo) + j, x[u]);
+      }
+    }
+  }
+}
+
+// Diagnostics only (ps_shard_stream_probe): this owner's streaming pass of a
+// push group by every worker, repeated `reps` times, with NO flags and no
+// peer participation -- so ncu can replay it in one process while the other
+// ranks idle, and read its NVLink byte counters. It writes the shard's spare
+// buffer and every replica's slice of this shard (the replicas' contents are
+// not preserved: run it on a throwaway server).
+template <int G_MAX>
+__global__ void __launch_bounds__(kThreads, PS_SHARD_MINB)
+k_shard_stream_probe(const float* __restrict__ w, float* __restrict__ spare, long long n_local, ShardPtrs P,
+                     int G, int me, float lr, int reps) {
+  constexpr int U = shard_unroll(G_MAX);
+  const long long nv = (n_local + 3) >> 2;
+  const long long lo = P.lo[me];
+  const long long stride = (long long)gridDim.x * kThreads * U;
+  const long long first = (long long)blockIdx.x * kThreads * U + threadIdx.x;
+  const float4* src[G_MAX];
+  unsigned live = 0;
+#pragma unroll
+  for (int i = 0; i < G_MAX; ++i) {
+    src[i] = reinterpret_cast<const float4*>(P.upd[i < G ? i : 0] + lo);
+    if (i < G) live |= 1u << i;
+  }
+  const unsigned pullm = G >= 32 ? 0xffffffffu : ((1u << G) - 1u);
+  unsigned gbad = 0, dbad = 0;
+  for (int r = 0; r < reps; ++r)
+    stream_pass<G_MAX, U>(reinterpret_cast<const float4*>(w), reinterpret_cast<float4*>(spare), src, live, pullm,
+                          P, G, lo, lr, first, stride, nv, gbad, dbad);
+  if (gbad == 0xdeadbeefu) spare[0] = (float)dbad;  // keep the pass observable
+}
+
 template <int G_MAX>
 __global__ void __launch_bounds__(kThreads, PS_SHARD_MINB)
 k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ w2, long long n_local, ShardPtrs P, int G,
@@ -503,44 +581,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
     }
     unsigned dbad = 0;
     unsigned gbad = 0;  // bit i: the update of pusher order[i] holds a non-finite value here
-    // Optimistic single pass: apply all G updates in ticket order into the
-    // back buffer and every worker's replica while scanning the update
-    // slices. U consecutive float4 per thread per trip with all G slices
-    // loaded first: U*G independent 128-bit loads in flight, G-1 of every G
-    // over NVLink.
-    for (long long base = first; base < nv; base += stride) {
-      float4 g[U][G_MAX];
-      float4 x[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long j = base + (long long)u * kThreads;
-        if (j < nv) {
-#pragma unroll
-          for (int i = 0; i < G_MAX; ++i)
-            if ((live >> i) & 1u) g[u][i] = ld_stream(src[i] + j);
-          x[u] = shard_ld(wsrc + j);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long j = base + (long long)u * kThreads;
-        if (j < nv) {
-#pragma unroll
-          for (int i = 0; i < G_MAX; ++i)
-            if ((live >> i) & 1u) {
-              gbad |= nonfinite4(g[u][i]) ? (1u << i) : 0u;
-              x[u] = apply4(x[u], lr, g[u][i]);
-            }
-          dbad |= nonfinite4(x[u]) ? 1u : 0u;
-          shard_st_w(wdst + j, x[u]);
-          // every worker's pull of this slice (handle_pull, server.py:84-91):
-          // stored straight into each replica, G-1 of them over NVLink
-#pragma unroll
-          for (int q = 0; q < G_MAX; ++q)
-            if (q < G && ((pullm >> q) & 1u)) shard_st_rep(reinterpret_cast<float4*>(P.rep[q] + lo) + j, x[u]);
-        }
-      }
-    }
+    stream_pass<G_MAX, U>(wsrc, wdst, src, live, pullm, P, G, lo, lr, first, stride, nv, gbad, dbad);
     gbad = __reduce_or_sync(kFull, gbad);
     dbad = __reduce_or_sync(kFull, dbad);
     if ((threadIdx.x & 31) == 0 && (gbad | dbad)) atomicOr(&s_bits, gbad | (dbad << 31));
@@ -1052,6 +1093,35 @@ int ps_shard_set_profiling(ps_shard_server* h, int32_t on) {
 
 int ps_shard_phase_ms(ps_shard_server* h, double* out3) {
   for (int k = 0; k < 3; ++k) out3[k] = h->phase_ms[k];
+  return PS_OK;
+}
+
+int ps_shard_stream_probe(ps_shard_server* h, int32_t reps, double* ms) {
+  Dev guard(h->dev);
+  if (reps < 1) return sfail(h, PS_E_VALUE, "reps must be >= 1");
+  const int G = h->world;
+  const void* kern = G <= 2 ? (const void*)k_shard_stream_probe<2> : G <= 4 ? (const void*)k_shard_stream_probe<4>
+                   : G <= 8 ? (const void*)k_shard_stream_probe<8> : (const void*)k_shard_stream_probe<16>;
+  int resident = 0;
+  SCK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, kThreads, 0));
+  const int grid = h->sm_count * (resident < 2 ? resident : 2);
+  // the spare buffer: whichever of the three is neither current nor next
+  SCK(h, cudaMemcpy(h->hctl, h->ctl, sizeof(ShardCtl), cudaMemcpyDeviceToHost));
+  float* bufs[3] = {h->w, h->w_alt, h->w_3};
+  const float* w = bufs[h->hctl->cur % 3];
+  float* spare = bufs[(h->hctl->cur + 2) % 3];
+  long long nl = h->n_local;
+  ShardPtrs ptrs = h->ptrs;
+  int Gv = G, mev = h->rank, r = reps;
+  float lr = (float)h->cfg.learning_rate;
+  void* args[] = {&w, &spare, &nl, &ptrs, &Gv, &mev, &lr, &r};
+  SCK(h, cudaEventRecord(h->ev0, h->stream));
+  SCK(h, cudaLaunchKernel(kern, dim3(grid), dim3(kThreads), args, 0, h->stream));
+  SCK(h, cudaEventRecord(h->ev1, h->stream));
+  SCK(h, cudaStreamSynchronize(h->stream));
+  float e = 0.f;
+  cudaEventElapsedTime(&e, h->ev0, h->ev1);
+  if (ms) *ms = e;
   return PS_OK;
 }
 
