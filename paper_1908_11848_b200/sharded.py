@@ -579,7 +579,12 @@ def bench_main(args, metric, extras=None):
             line["roofline"] = {
                 "bound": "nvlink", "achieved": achieved, "peak": 770.0, "unit": "GB/s",
                 "frac": achieved / 770.0, "frac_vs_900": achieved / 900.0,
-                "traffic": (nvl_delta or {}).get("data_rx_kib"),
+                "traffic": _probe_traffic(world, "received_user_bytes_per_gpu_per_step")
+                           or (nvl_delta or {}).get("data_rx_kib"),
+                "traffic_link_bytes_with_protocol": _probe_traffic(world, "received_link_bytes_per_gpu_per_step"),
+                "traffic_source": "ncu nvlrx/nvltx byte counters of the same streaming pass, one-sided "
+                                  "(profiles/k_shard_run_nvlink_bytes.json, tools/shard_nvlink_probe.py): "
+                                  "received NVLink user bytes per GPU per step",
                 "traffic_counters": nvl_delta,
                 "traffic_note": "NVML NVLink data counters of rank 0's GPU around the timed DSSP run, "
                                 "bytes per step, when the box supports them (these report "
@@ -642,6 +647,17 @@ def bench_main(args, metric, extras=None):
         store.wait(["bench_done"], timedelta(seconds=3600))
     dist.destroy_process_group()
     return 0
+
+
+def _probe_traffic(world, key):
+    """NVLink bytes per GPU per step of the sharded streaming pass at this
+    world size, from the committed ncu capture, or None."""
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "k_shard_run_nvlink_bytes.json")
+    try:
+        return json.load(open(path))["per_world"][str(world)][key]
+    except Exception:
+        return None
 
 
 def _c3_reference_decisions(paradigm, world):
