@@ -316,10 +316,16 @@ def throttled_bench(world, rank, local):
         pushes = sum(len(g[1]) for g in groups[8:])
         trace = srv.trace()
         ok = [e.decision for e in trace] == [e.decision for e in sched.entries if e.kind == "push_arrive"]
+        # and against the reference simulator's trace of the same cluster
+        # (tests/golden/c4_sharded_schedule.json.gz), every rendered row
+        want = _golden_push_rows("c4_sharded_schedule.json.gz", f"c4sh_{name}_p{world}")
+        got_rows = [e.render().split("\t") for e in trace]
+        ref_ok = (got_rows == want) if want else None
         pw = per_worker(sched.entries)
         hist = staleness_histogram(sched.entries)
         out[name] = {"updates_per_s": pushes / (ms * 1e-3), "groups": len(groups) - 8,
                      "updates": pushes, "decisions_match_single_gpu_engine": ok,
+                     "trace_identical_to_reference": ref_ok,
                      "fast_worker_wait_s": pw[0].wait_s, "max_staleness": max(hist) if hist else 0,
                      "throttle": list(throttle)}
         torch.cuda.synchronize()
@@ -660,16 +666,24 @@ def _probe_traffic(world, key):
         return None
 
 
-def _c3_reference_decisions(paradigm, world):
-    """Push rows of the reference simulator's trace of the C3 schedule
-    (tests/golden/c3_schedule.json.gz; recorded by make_golden.py), or [] if
-    the fixture has no run for this worker count."""
+def _golden_push_rows(fixture, name):
+    """Push rows of a reference simulator trace committed under tests/golden
+    (recorded by make_golden.py), or [] if absent."""
     import gzip
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
-                        "c3_schedule.json.gz")
-    with gzip.open(path, "rt") as fh:
-        runs = json.load(fh)["runs"]
+                        fixture)
+    try:
+        with gzip.open(path, "rt") as fh:
+            runs = json.load(fh)["runs"]
+    except OSError:
+        return []
     for r in runs:
-        if r["name"] == f"c3_{paradigm}_p{world}":
+        if r["name"] == name:
             return [ln.split("\t") for ln in r["trace"].splitlines() if ln.split("\t")[2] == "push_arrive"]
     return []
+
+
+def _c3_reference_decisions(paradigm, world):
+    """Push rows of the reference simulator's trace of the C3 schedule
+    (tests/golden/c3_schedule.json.gz), or [] for an unrecorded world size."""
+    return _golden_push_rows("c3_schedule.json.gz", f"c3_{paradigm}_p{world}")

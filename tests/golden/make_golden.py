@@ -24,6 +24,8 @@ Fixtures written (all deterministic; re-running reproduces them byte for byte):
                            (stalesync/server.py:29-69, tests/test_server.py).
   acceptance_corpora.json.gz  the acceptance suite's corpora at full scale
                            (criteria 1, 2, 4): trace digests, final weights.
+  c4_sharded_schedule.json.gz  traces of the bench's throttled cluster across
+                           GPUs (P = 2, 4, 8 at 1x/2x/4x, every paradigm).
   c3_schedule.json.gz      run_simulation traces of the bench's homogeneous
                            sharded workload (P = 1, 2, 4, 8, every paradigm).
   sim_throttle.json.gz     run_simulation with 1x/2x/4x throttled workers
@@ -538,6 +540,27 @@ def sim_throttle():
     _dump("sim_throttle.json.gz", {"runs": out}, gz=True)
 
 
+def c4_sharded_schedule():
+    """The schedule bench.py's configs[3]-across-GPUs block serves
+    (sharded.throttled_bench): P = 2, 4, 8 workers throttled 1x/2x/4x
+    (cycling), homogeneous base, every paradigm. The schedule does not
+    depend on the parameter count, so a small bowl stands in for the
+    ResNet-110-sized server; only the traces are kept."""
+    out = []
+    for workers in (2, 4, 8):
+        throttle = tuple((1, 2, 4)[q % 3] for q in range(workers))
+        for paradigm, s, r in (("dssp", 3, 12), ("ssp", 3, 0), ("bsp", 0, 0), ("asp", 0, 0)):
+            flat = dict(paradigm=paradigm, worker_count=workers, s_lower=s, r_max=r,
+                        timing_preset="homogeneous", compute_base=1.0, comm_delay=0.05,
+                        model_kind="quadratic_bowl", dimension=64, dataset_size=workers * 400,
+                        batch_size=16, learning_rate=0.05, epochs=1, seed=0, loss_every=100000)
+            rec = _run_recorded(flat, False, throttle)
+            rec["name"] = f"c4sh_{paradigm}_p{workers}"
+            rec.pop("calls")
+            out.append(rec)
+    _dump("c4_sharded_schedule.json.gz", {"runs": out}, gz=True)
+
+
 def sim_large():
     """Worker counts beyond the main corpus: P = 1 (serial SGD), and the
     lane-per-worker (9..32) and shared-memory (33..64) control-warp layouts
@@ -563,13 +586,15 @@ def sim_large():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2", "large", "throttle", "c3", "acceptance"]
+    which = sys.argv[1:] or ["controller", "gate", "sim", "apply", "c2", "large", "throttle", "c3", "acceptance", "c4sh"]
     if "throttle" in which:
         sim_throttle()
     if "c3" in which:
         c3_schedule()
     if "acceptance" in which:
         acceptance_corpora()
+    if "c4sh" in which:
+        c4_sharded_schedule()
     if "large" in which:
         sim_large()
     if "c2" in which:
