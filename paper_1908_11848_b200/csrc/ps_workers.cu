@@ -458,7 +458,10 @@ int reset_run(ps_server* h) {
     auto& b = rt->bind[q];
     if (!b.go) continue;
     DevGuardW g(b.dev);
-    PS_CK(h, cudaMemset(b.go, 0, sizeof(unsigned)));
+    // fully complete before any worker stream (non-blocking: no implicit
+    // order with the legacy stream) can raise the flag
+    PS_CK(h, cudaMemsetAsync(b.go, 0, sizeof(unsigned), 0));
+    PS_CK(h, cudaDeviceSynchronize());
   }
   return PS_OK;
 }
@@ -534,7 +537,8 @@ int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const
   if (!b.go) {
     DevGuardW g(wdev);
     PS_CK(h, cudaMalloc(&b.go, 256));
-    PS_CK(h, cudaMemset(b.go, 0, 256));
+    PS_CK(h, cudaMemsetAsync(b.go, 0, 256, 0));
+    PS_CK(h, cudaDeviceSynchronize());
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wdev);
@@ -544,7 +548,10 @@ int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const
   b.grad = grad;
   b.params = params;
   DevGuardW guard(h->dev);
-  PS_CK(h, cudaMemcpy(&rt->c->go[worker], &b.go, sizeof(unsigned*), cudaMemcpyHostToDevice));
+  // (on the server stream and waited for: a pageable cudaMemcpy may return
+  // before its DMA lands, and the worker streams do not order against it)
+  PS_CK(h, cudaMemcpyAsync(&rt->c->go[worker], &b.go, sizeof(unsigned*), cudaMemcpyHostToDevice, h->stream));
+  PS_CK(h, cudaStreamSynchronize(h->stream));
   return PS_OK;
 }
 
