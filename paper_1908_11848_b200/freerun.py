@@ -58,6 +58,7 @@ class FreeRunReport:
     status: int
     aborted: bool = False
     iterations: dict = field(default_factory=dict)
+    stuck: list = field(default_factory=list)   # workers still blocked at the deadline
 
     @property
     def pushes(self) -> int:
@@ -171,9 +172,14 @@ class FreeRunningCluster:
         for dev in sorted({d.index for d in self.devices} | {self.engine.device}):
             torch.cuda.synchronize(dev)
 
-    def run(self, iterations, restart=True):
+    def run(self, iterations, restart=True, deadline_s=120.0):
         """`iterations` per worker, every launch enqueued up front, one host
-        synchronization at the end. Returns a FreeRunReport."""
+        wait at the end. The wait polls the worker streams; past `deadline_s`
+        the run is aborted like the runner's deadline_guard (runner.py:294-298:
+        every go flag raised, later kernels only advance the ticket) and the
+        report comes back with ``aborted`` set and ``stuck`` naming the workers
+        whose streams had not finished -- a blocked stream never hangs the
+        host. Returns a FreeRunReport."""
         import torch
         if restart:
             self._check(self.lib.ps_workers_start(self.engine.handle, self.log_cap, self.time_scale))
@@ -186,9 +192,26 @@ class FreeRunningCluster:
                         self._graphs[p].replay()
                     else:
                         self._iteration(p, self.streams[p].cuda_stream)
-        self._sync_all()
+        stuck = self._wait(t0, deadline_s)
         wall = time.perf_counter() - t0
-        return self.report(wall)
+        rep = self.report(wall)
+        rep.stuck = stuck
+        return rep
+
+    def _wait(self, t0, deadline_s):
+        pending = set(range(self.P))
+        while pending:
+            pending = {p for p in pending if not self.streams[p].query()}
+            if not pending:
+                break
+            if deadline_s is not None and time.perf_counter() - t0 > deadline_s:
+                stuck = sorted(pending)
+                self.abort()
+                self._sync_all()
+                return stuck
+            time.sleep(50e-6)
+        self._sync_all()
+        return []
 
     def report(self, wall=0.0):
         st = PSWorkersReport()

@@ -271,3 +271,26 @@ def test_torch_resnet_workers_on_peer_gpus():
     w, _ = _replay(rep, [r.cpu().numpy() for r in rings], d, w0.astype(np.float32), 0.01)
     assert np.array_equal(eng.read()[0].view(np.uint32), w.view(np.uint32))
     eng.close()
+
+
+def test_deadline_aborts_a_run_that_cannot_finish():
+    """BSP where worker 1 never gets iterations enqueued: worker 0 parks on
+    its go flag forever. The host wait polls the streams and, past the
+    deadline, aborts like deadline_guard (runner.py:294-298): the run ends,
+    reports worker 0 as stuck, and the host never hangs."""
+    d = 64
+    ring = torch.zeros(1, 64, device="cuda")
+    workers = [SyntheticWorker(ring) for _ in range(2)]
+    eng = Engine("bsp", 2, 0, 0, 0.05, d)
+    cl = FreeRunningCluster(eng, workers, graphs=False)
+    cl._check(cl.lib.ps_workers_start(eng.handle, 1024, 1.0))
+    import time
+    t0 = time.perf_counter()
+    with torch.cuda.stream(cl.streams[0]):
+        for _ in range(3):
+            cl._iteration(0, cl.streams[0].cuda_stream)
+    stuck = cl._wait(t0, deadline_s=0.5)
+    assert stuck == [0]
+    rep = cl.report()
+    assert rep.aborted and rep.defers(0) >= 1
+    eng.close()
