@@ -80,6 +80,7 @@ class Engine:
         if rc:
             raise_for(rc, self.lib.ps_last_error(None).decode())
         self._state = _lib.PSGateState()
+        self._stale = False
         self.refresh(sync=False)
 
     def close(self):
@@ -108,10 +109,16 @@ class Engine:
     def refresh(self, sync=True):
         fn = self.lib.ps_get_state if sync else self.lib.ps_peek_state
         self.check(fn(self._h, ctypes.byref(self._state)))
+        self._stale = False
         return self._state
 
     @property
     def state(self):
+        """The gate tables as of the last op (the host-mapped mirror the op
+        kernels publish into; copied on demand, not after every call)."""
+        if self._stale:
+            self.lib.ps_peek_state(self._h, ctypes.byref(self._state))
+            self._stale = False
         return self._state
 
     def write_state(self, state):
@@ -128,7 +135,9 @@ class Engine:
             import torch
             # handle 0 is the legacy default stream: name it cudaStreamLegacy
             # (0x1), because NULL means "no producer" at the C-ABI
-            ptr = torch.cuda.current_stream(tensor.device).cuda_stream or 1
+            raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+            ptr = (raw(tensor.device.index) if raw is not None
+                   else torch.cuda.current_stream(tensor.device).cuda_stream) or 1
         if ptr != getattr(self, "_producer", None):
             self.lib.ps_set_producer_stream(self._h, ptr)
             self._producer = ptr
@@ -146,7 +155,7 @@ class Engine:
         ptr, dt, on_dev, keep = self._gradient_args(values)
         applied = ctypes.c_int32(0)
         rc = self.lib.ps_apply(self._h, int(worker), ptr, dt, on_dev, ctypes.byref(applied))
-        self.lib.ps_peek_state(self._h, ctypes.byref(self._state))
+        self._stale = True
         self.check(rc)
         return bool(applied.value)
 
@@ -155,7 +164,7 @@ class Engine:
         released = ctypes.c_uint64(0)
         rc = self.lib.ps_decide(self._h, int(worker), float(now), ctypes.byref(granted),
                                 ctypes.byref(released))
-        self.lib.ps_peek_state(self._h, ctypes.byref(self._state))
+        self._stale = True
         self.check(rc)
         return bool(granted.value), released.value
 
@@ -166,7 +175,7 @@ class Engine:
         released = ctypes.c_uint64(0)
         rc = self.lib.ps_push(self._h, int(worker), ptr, dt, on_dev, float(now),
                               ctypes.byref(applied), ctypes.byref(granted), ctypes.byref(released))
-        self.lib.ps_peek_state(self._h, ctypes.byref(self._state))
+        self._stale = True
         self.check(rc)
         return bool(applied.value), bool(granted.value), released.value
 
