@@ -853,7 +853,8 @@ def single_gpu_extras(torch, ps, line):
                                 "handle_pull), pinned host buffers"},
         "cpu_baseline": _run_cpu_child(["c2"]),
     }
-    _safe(line, "sweep_single_gpu", lambda: apply_sweep(torch, ps, hbm_peak))
+    # configs[4] at N = 1: the push-apply / pull kernels 1 MB - 1 GB
+    _safe(line, "sweep", lambda: apply_sweep(torch, ps, hbm_peak))
     _safe(line, "c4_throttled", lambda: c4_throttled(torch, ps))
     _safe(line, "c4_free_running", lambda: c4_realtime(torch, ps))
     _safe(line, "torch_workers_c2", lambda: torch_workers(torch, ps))

@@ -210,6 +210,46 @@ def main(out_dir):
     torch.cuda.synchronize()
     dist.barrier()
     srv.close()
+    # divergence at the pipeline's boundaries: the first lagged resolve
+    # (steps 1 and 2 of a run), and the run's last step -- the weights must
+    # be the input of the failing step on every rank
+    for start, n_steps in ((3.25e38, 6), (3.15e38, 6), (2.9e38, 6), (2.3e38, 8)):
+        cfg = ps.validate_config(ps.make_config(paradigm="asp", worker_count=world, dimension=d,
+                                                learning_rate=0.5, seed=6))
+        w0 = oracle.initial_weights_f64(6, d)
+        w0[13] = start
+        srv = ShardedServer(cfg, d, rank, world, local, w0_host=w0)
+        g = oracle.synthetic_update(9, rank, 0, d)
+        g[13] = -2.0e37 if rank == 0 else 0.0
+        srv.update[:d].copy_(torch.from_numpy(g))
+        torch.cuda.synchronize()
+        dist.barrier()
+        diverged = False
+        try:
+            srv.run([float(i + 1) for i in range(n_steps)])
+        except ps.DivergenceError:
+            diverged = True
+        gs = [oracle.synthetic_update(9, p, 0, d) for p in range(world)]
+        for p in range(world):
+            gs[p][13] = -2.0e37 if p == 0 else 0.0
+        w = w0.astype(np.float32)
+        ok_steps = 0
+        while ok_steps < n_steps:
+            nxt = w
+            for p in range(world):
+                nxt = oracle.apply_f32(nxt, gs[p], 0.5)
+            if not np.all(np.isfinite(nxt)):
+                break
+            w = nxt
+            ok_steps += 1
+        verdict["checks"].append({
+            "run": f"diverge_at_{ok_steps}_of_{n_steps}", "d": d,
+            "trace": diverged == (ok_steps < n_steps),
+            "shard": bool(np.array_equal(srv.read_shard().view(np.uint32), w[srv.lo:srv.hi].view(np.uint32))),
+            "replica": True, "version": int(srv.state().version), "steps": ok_steps})
+        torch.cuda.synchronize()
+        dist.barrier()
+        srv.close()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
         json.dump(verdict, fh)
     dist.barrier()
