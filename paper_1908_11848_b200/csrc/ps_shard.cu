@@ -53,9 +53,12 @@ namespace {
 constexpr int kMaxRanks = 16;
 constexpr int kSchedStride = 2 + kMaxRanks;  // ps_shard_run_groups row: n, pull mask, order
 constexpr int kThreads = 256;
-// per-rank flag words written by peers: ready[G] | V(t) by step parity [2][G]
-// | F(t) redo done [G] | D first diverged step [G]
-constexpr int kFlagWords = 5 * kMaxRanks;
+// per-rank flag words written by peers: ready[G] | V(t) in slot t % 4 [4][G]
+// | F(t) redo done [G] | D first diverged step [G]. Four V slots: with the
+// one-step-deep pipeline an owner can publish V(t+2) before a slow reader has
+// read V(t), never V(t+4).
+constexpr int kFlagWords = 7 * kMaxRanks;
+constexpr int kVSlots = 4;
 // streaming-loop shape (build-time knobs for tuning experiments): minimum
 // resident CTAs per SM the register budget must allow, and float4 per thread
 // per trip for G <= 2 / <= 4 / more
@@ -378,7 +381,17 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
   const int c0 = ld_relaxed_s32(&ctl->cur);  // the committed buffer at launch, identical in every CTA
   long long redo_n = 0;                      // redo rounds so far (election targets)
   const int steps_total = steps;
-  const bool lag = (sched == nullptr) && steps > 2 && ld_relaxed_s32(&ctl->no_lag) == 0;
+  const bool lag = steps > 2 && ld_relaxed_s32(&ctl->no_lag) == 0;
+  // workers whose update of this run has been judged (by a full resolve):
+  // a step whose pushers are all known carries no new rejection, so the next
+  // step may start before its verdict (heterogeneous schedules meet new
+  // pushers in their first groups, homogeneous ones only at step 0)
+  unsigned long long K = 0;
+  auto pushers_of = [&](int slot) {
+    unsigned long long m = 0;
+    for (int i = 0; i < s_n[slot]; ++i) m |= 1ull << s_order[slot][i];
+    return m;
+  };
   unsigned long long R = 0;                  // rejected workers of this run (lag mode)
   // commit step t (relative index k): buffer (c0 + k + 1) % 3 becomes current
   // (the rejected updates of step t: its own verdict bits plus every pusher of
@@ -412,7 +425,7 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
       const unsigned long long s0 = globaltimer_ns();
       for (int s = 0; s < G && !stop; ++s) {
         unsigned long long v;
-        while (((v = ld_acquire_sys_u64(P.flags[me] + G + (int)(t & 1) * G + s)) >> 32) < t) {
+        while (((v = ld_acquire_sys_u64(P.flags[me] + G + (int)(t % kVSlots) * G + s)) >> 32) < t) {
           if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
           __nanosleep(20);
         }
@@ -456,13 +469,13 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
         if (prev == (unsigned long long)(redo_n * ndata) - 1) {  // last CTA: F(t) to every rank
           const unsigned long long dv = atomicExch(&ctl->bad, 0u) & 1u;
           __threadfence_system();
-          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + 3 * G + me, (t << 32) | dv);
+          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + (1 + kVSlots) * G + me, (t << 32) | dv);
         }
         int div = 0, stop = 0;
         const unsigned long long s0 = globaltimer_ns();
         for (int s = 0; s < G && !stop; ++s) {
           unsigned long long v;
-          while (((v = ld_acquire_sys_u64(P.flags[me] + 3 * G + s)) >> 32) < t) {
+          while (((v = ld_acquire_sys_u64(P.flags[me] + (1 + kVSlots) * G + s)) >> 32) < t) {
             if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
             __nanosleep(20);
           }
@@ -491,13 +504,13 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
       const unsigned long long s0 = globaltimer_ns();
       for (int s = 0; s < G && !stop; ++s) {
         unsigned long long v;
-        while (((v = ld_acquire_sys_u64(P.flags[me] + G + (int)(t & 1) * G + s)) >> 32) < t) {
+        while (((v = ld_acquire_sys_u64(P.flags[me] + G + (int)(t % kVSlots) * G + s)) >> 32) < t) {
           if (globaltimer_ns() - s0 > kTimeoutNs) { atomicCAS(&ctl->status, PS_OK, PS_E_TIMEOUT); stop = 1; break; }
           __nanosleep(20);
         }
         if ((v >> 31) & 1ull) {
           // sticky: owner s diverged at step D[s] <= v's step (published first)
-          const unsigned long long d = ld_acquire_sys_u64(P.flags[me] + 4 * G + s);
+          const unsigned long long d = ld_acquire_sys_u64(P.flags[me] + (2 + kVSlots) * G + s);
           if (d && d <= t && (!tdiv || d < tdiv)) tdiv = d;
         }
       }
@@ -520,12 +533,19 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
     if (!lag) {
       if (step > 0 && !resolve(t - 1)) return;
       resolved = t - 1;
-    } else if (step == 1) {
-      if (!resolve(t0)) return;
-      resolved = t0;
-    } else if (step >= 2 && t - 2 > resolved) {  // (step 2: t0 was resolved in full at step 1)
-      if (!resolve_lag(t - 2)) return;
-      resolved = t - 2;
+    } else if (step >= 1) {
+      const unsigned long long prev_pushers = pushers_of((int)((t - 1) & 1));
+      if (step >= 2 && t - 2 > resolved) {
+        if (!resolve_lag(t - 2)) return;
+        resolved = t - 2;
+      }
+      if (prev_pushers & ~K) {
+        // step t-1 met pushers not yet judged: its verdict (and any redo
+        // without the rejected ones) before step t runs
+        if (!resolve(t - 1)) return;
+        resolved = t - 1;
+        K |= prev_pushers;
+      }
     }
     if (threadIdx.x == 0) {
       s_bits = 0;
@@ -608,13 +628,13 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
         if ((b >> 31) && !(b & 0x7fffffffu) && !ctl->div_sticky) {
           ctl->div_sticky = 1;
           // D(me) = the first diverged step, published before V(t)
-          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + 4 * G + me, t);
+          for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + (2 + kVSlots) * G + me, t);
         }
         unsigned long long v = (t << 32) | ((unsigned long long)div << 31);
         for (int i = 0; i < s_n[co]; ++i)
           if ((b >> i) & 1u) v |= 1ull << s_order[co][i];
         __threadfence_system();
-        for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + G + co * G + me, v);
+        for (int s = 0; s < G; ++s) st_relaxed_sys_u64(P.flags[s] + G + (int)(t % kVSlots) * G + me, v);
         SPROF(g_prof[3] += globaltimer_ns() - te; g_prof[6] += 1);
       }
     }
@@ -625,8 +645,11 @@ k_shard_run(float* __restrict__ w0, float* __restrict__ w1, float* __restrict__ 
   if (!lag) {
     resolve(t_last);
   } else {
-    for (unsigned long long t = resolved + 1; t <= t_last; ++t)
-      if (!resolve_lag(t)) break;
+    for (unsigned long long t = resolved + 1; t <= t_last; ++t) {
+      const unsigned long long p = pushers_of((int)(t & 1));
+      if (!((p & ~K) ? resolve(t) : resolve_lag(t))) break;
+      K |= p;
+    }
   }
 #ifdef PS_SHARD_PROFILE
   if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -80,6 +80,44 @@ def main(out_dir):
             torch.cuda.synchronize()
             dist.barrier()
             srv.close()
+    # a pusher first seen late in a run with a non-finite update: the
+    # pipelined run_groups must judge its first group in full (redo without
+    # it) and skip it afterwards -- rejected at every push (server.py:65-67)
+    d = 100_003
+    cfg = ps.validate_config(ps.make_config(paradigm="asp", worker_count=world, dimension=d,
+                                            learning_rate=0.05, seed=8))
+    w0 = oracle.initial_weights_f64(8, d)
+    srv = ShardedServer(cfg, d, rank, world, local, w0_host=w0)
+    late = world - 1
+    gs = [oracle.synthetic_update(11, p, 0, d) for p in range(world)]
+    gs[late][d // 2] = np.nan
+    srv.update[:d].copy_(torch.from_numpy(gs[rank]))
+    torch.cuda.synchronize()
+    dist.barrier()
+    early = list(range(world - 1))
+    groups = []
+    for i in range(9):
+        order = early + ([late] if i in (3, 6, 7) else [])
+        groups.append((float(i + 1), order, list(order)))
+    srv.run_groups(groups)
+    w = w0.astype(np.float32)
+    mine = w.copy()
+    for _, order, pulls in groups:
+        for p in order:
+            if p != late:
+                w = oracle.apply_f32(w, gs[p], cfg.learning_rate)
+        if rank in pulls:
+            mine = w.copy()
+    st = srv.state()
+    checks.append({
+        "run": "late_pusher_rejected", "d": d, "groups": len(groups),
+        "trace": int(st.rejected) == 3,
+        "shard": bool(np.array_equal(srv.read_shard().view(np.uint32), w[srv.lo:srv.hi].view(np.uint32))),
+        "replica": bool(np.array_equal(srv.read_replica().view(np.uint32), mine.view(np.uint32))),
+        "version": int(st.version) + int(st.rejected), "pushes": sum(len(g[1]) for g in groups)})
+    torch.cuda.synchronize()
+    dist.barrier()
+    srv.close()
     with open(os.path.join(out_dir, f"groups_rank{rank}.json"), "w") as fh:
         json.dump(checks, fh)
     dist.barrier()
