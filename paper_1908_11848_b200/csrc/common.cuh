@@ -84,6 +84,14 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
   return v;
 }
+// Read-only 128-bit loads that a warp repeats many times in one kernel (the
+// replay's resident update slices): kept in L1, so the repeats are L1 hits.
+__device__ __forceinline__ float4 ld_keep(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ float4 ld_f4(const float4* p) { return *p; }
 __device__ __forceinline__ void st_f4(float4* p, const float4& v) { *p = v; }
 

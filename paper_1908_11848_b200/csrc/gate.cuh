@@ -95,6 +95,42 @@ __device__ __forceinline__ int controller_grid(double lp, double pp, double ls, 
   return (int)__reduce_min_sync(kFull, (hi == mhi && lo == mlo) ? (unsigned)best_r : 0x7fffffffu);
 }
 
+// One lane's own controller (same arguments as controller_grid, 2 <= r_max <=
+// kLaneRMax), for a warp that evaluates up to 32 decisions at once. Per r the
+// crossing of the non-decreasing slow(k) with cand is estimated from
+// (cand - ls) / is, and a window of three k around it is evaluated with
+// controller_grid's exact rounded expressions. The window is then checked to
+// bracket the crossing (slow at its low end <= cand < slow at its high end,
+// or the end of the k range), so its minimum is the full minimum bit for bit;
+// `ok` is cleared when the estimate missed (the caller then runs the exact
+// warp-collective grid for that decision).
+constexpr int kLaneRMax = 16;
+__device__ __forceinline__ int controller_lane(double lp, double pp, double ls, double ps, int r_max, bool& ok) {
+  const double ip = interval_of(lp, pp);
+  const double is = interval_of(ls, ps);
+  const double inv = 1.0 / is;
+  const double top = (double)(r_max + 1);  // k + 1 runs over [1, r_max + 1]
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  int best_r = 0;
+  bool good = r_max >= 2;
+#pragma unroll
+  for (int r = 0; r <= kLaneRMax; ++r) {
+    if (r <= r_max) {
+      const double cand = __dadd_rn(lp, __dmul_rn((double)r, ip));
+      const double x = __dmul_rn(__dsub_rn(cand, ls), inv);
+      const double fc = fmin(fmax(floor(x), 2.0), top - 1.0);  // window {fc-1, fc, fc+1} in [1, top]
+      const double d0 = __dsub_rn(__dadd_rn(ls, __dmul_rn(fc - 1.0, is)), cand);
+      const double d1 = __dsub_rn(__dadd_rn(ls, __dmul_rn(fc, is)), cand);
+      const double d2 = __dsub_rn(__dadd_rn(ls, __dmul_rn(fc + 1.0, is)), cand);
+      const double m = fmin(fmin(fabs(d0), fabs(d1)), fabs(d2));
+      good = good && (fc == 2.0 || d0 <= 0.0) && (fc == top - 1.0 || d2 > 0.0);
+      if (m < best) { best = m; best_r = r; }
+    }
+  }
+  ok = good;
+  return best_r;
+}
+
 __device__ __forceinline__ void record(ps_gate_state* s, int q, double t) {
   s->previous[q] = s->latest[q];
   s->latest[q] = t;

@@ -121,6 +121,7 @@ struct SimArgs {
   long long* decisions;       // replay: (released << 8) | outcome per decide
   unsigned tag;
   unsigned n_ctas;
+  int gate_scan;              // replay: the scan gate when eligible (PS_REPLAY_GATE_SCAN, default on)
 };
 
 // Cycle accounting of the control warp, compiled in with -DPS_SIM_PROFILE.
@@ -778,6 +779,254 @@ struct ReplayGate<0> {  // shared-memory tables (gate.cuh), any P <= 64
   }
 };
 
+// The replay gate as a scan (P <= PM <= 8, r_max <= 16, credits < 256).
+//
+// Of the gate's state only the credits and the deferred set depend on earlier
+// OUTCOMES. Clocks, the two-deep push history and the populated counts follow
+// from the sequence of pushes alone (every push counts and is recorded,
+// policy.py:152-170), and so do min / max / slowest, the gap, the controller's
+// inputs and the release-ready set of every decision (policy.py:60-73,
+// 108-132, 197-206). Per 32-call chunk the warp therefore evaluates all of
+// that for every DECIDE at once, one decision per lane (prefix counts over
+// per-worker ballots, the controller per lane), and packs each into one word
+// -- worker | class | minted credits | ready set. The serial part that is
+// left is the credit / deferred recurrence of policy.py:172-206, ~20 scalar
+// instructions per decision on packed registers. Decisions and final state are
+// those of gate_on_push in call order; tests/test_gpu_replay.py and the
+// golden decide streams hold both paths to the reference.
+template <int PM>
+__device__ bool gate_scan_eligible(const RegGate<PM>& g) {
+  if (g.P > PM || PM > 8) return false;
+  if (g.paradigm == PS_DSSP && (g.r_max > kLaneRMax || g.s_lower + g.r_max > 255)) return false;
+#pragma unroll
+  for (int q = 0; q < PM; ++q)
+    if (g.credits[q] < 0 || g.credits[q] > 255) return false;
+  return true;
+}
+
+template <int PM>
+__device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
+  // credits, 8 bits per worker: one 32-bit word up to 4 workers
+  using CW = typename std::conditional<(PM <= 4), unsigned, unsigned long long>::type;
+  __shared__ unsigned sw[32];  // the chunk's packed decisions by slot
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u, le = lt | (1u << lane);
+  const int P = g.P;
+  const bool dssp = g.paradigm == PS_DSSP, asp = g.paradigm == PS_ASP;
+  long long n_dec = 0, pushes = 0, valid = 0;
+  int status = PS_OK;
+  const long long n = a.n_calls;
+  if (lane == 0) a.out->t_start = globaltimer_ns();
+  CW cw = 0;
+#pragma unroll
+  for (int q = 0; q < PM; ++q) cw |= (CW)(q < P ? g.credits[q] : 0) << (8 * q);
+  unsigned defm = (unsigned)g.deferred;
+  auto load = [&](long long base, ReplayCall& c) {
+    const long long i = base + lane;
+    if (i < n) c = a.calls[i];
+    else { c.now = 0.0; c.kind = -1; c.worker = 0; }
+  };
+  ReplayCall c, nx;
+  load(0, c);
+  for (long long base = 0; base < n; base += 32) {
+    load(base + 32, nx);
+    const int m = n - base < 32 ? (int)(n - base) : 32;
+    const unsigned live = m >= 32 ? kFull : ((1u << m) - 1u);
+    const unsigned badw = __ballot_sync(kFull, lane < m && (c.worker < 0 || c.worker >= P));
+    const int limit = badw ? __ffs(badw) - 1 : m;
+    const unsigned below_limit = limit >= 32 ? kFull : ((1u << limit) - 1u);
+    const unsigned md = __ballot_sync(kFull, c.kind == kCallDecide) & live & below_limit;
+    const unsigned mp = __ballot_sync(kFull, c.kind == kCallPull) & live & below_limit;
+    const bool is_dec = (md >> lane) & 1u;
+    const int w = is_dec ? c.worker : 0;
+    // ---- every decision of the chunk at once (one per lane) ----
+    unsigned mq[PM];
+#pragma unroll
+    for (int q = 0; q < PM; ++q) mq[q] = __ballot_sync(kFull, is_dec && w == q);
+    int cnt[PM];
+    int low = 0x7fffffff, high = -0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < PM; ++q) {
+      cnt[q] = g.clocks[q] + __popc(mq[q] & le);
+      if (q < P) { low = cnt[q] < low ? cnt[q] : low; high = cnt[q] > high ? cnt[q] : high; }
+    }
+    int sl = 0;
+#pragma unroll
+    for (int q = PM - 1; q >= 0; --q)
+      if (q < P && cnt[q] == low) sl = q;
+    const int count = rget<PM>(cnt, w);
+    const int gap = count - low;
+    unsigned ready = 0;
+    if (!asp) {
+#pragma unroll
+      for (int q = 0; q < PM; ++q)
+        if (q < P && cnt[q] - low <= g.threshold) ready |= 1u << q;
+    }
+    int cls = gap <= g.threshold ? 0 : 1;  // SSP / BSP: grant or defer
+    int mint = 0;
+    if (asp) cls = 0;
+    if (dssp) {
+      cls = gap <= g.s_lower ? 0 : (count < high ? 1 : 2);
+      // the controller's inputs after this push is recorded
+      const unsigned mine = rget<PM>(mq, w) & le;     // this worker's pushes up to here
+      const unsigned prior = mine & lt;
+      const double pp_in = __shfl_sync(kFull, c.now, prior ? 31 - __clz(prior) : lane);
+      const double pp = prior ? pp_in : rget<PM>(g.latest, w);
+      const unsigned msl = rget<PM>(mq, sl) & le;
+      const int l1 = msl ? 31 - __clz(msl) : lane;
+      const unsigned rest = msl & ~(1u << (l1 & 31));
+      const double ls_in = __shfl_sync(kFull, c.now, l1);
+      const double ps_in = __shfl_sync(kFull, c.now, rest ? 31 - __clz(rest) : lane);
+      const double ls = msl ? ls_in : rget<PM>(g.latest, sl);
+      const double ps = rest ? ps_in : (msl ? rget<PM>(g.latest, sl) : rget<PM>(g.previous, sl));
+      const int pop_p = rget<PM>(g.populated, w) + __popc(mine);
+      const int pop_sl = rget<PM>(g.populated, sl) + __popc(msl);
+      const bool need = is_dec && cls == 2 && g.r_max > 0 && pop_p >= 2 && pop_sl >= 2;
+      int pred = 0;
+      const unsigned needm = __ballot_sync(kFull, need);
+      if (needm) {
+        bool ok = true;
+        pred = controller_lane(c.now, pp, ls, ps, g.r_max, ok);
+        unsigned miss = __ballot_sync(kFull, need && !ok);
+        while (miss) {  // the estimate missed: the exact warp-collective grid
+          const int j = __ffs(miss) - 1;
+          miss &= miss - 1;
+          const int pj = controller_grid(__shfl_sync(kFull, c.now, j), __shfl_sync(kFull, pp, j),
+                                         __shfl_sync(kFull, ls, j), __shfl_sync(kFull, ps, j), g.r_max);
+          if (lane == j) pred = pj;
+        }
+        if (!need) pred = 0;
+      }
+      int headroom = g.s_lower + g.r_max - gap;
+      headroom = headroom < 0 ? 0 : headroom;
+      mint = pred < headroom ? pred : headroom;
+    }
+    // the outcome and the credits a decision leaves when the worker holds no
+    // credit are fixed by now: pack worker | outcome | credits | ready set
+    const unsigned out0 = cls == 2 ? (mint ? 0u : 1u) : (unsigned)cls;
+    const unsigned word = (unsigned)w | (out0 << 3) | ((unsigned)(cls == 2 ? mint : 0) << 4) | (ready << 12);
+    // decisions compacted into slots 0..nd-1, slot j in lane j
+    const int nd = __popc(md);
+    const int myslot = __popc(md & lt);
+    if (is_dec) sw[myslot] = word;
+    __syncwarp();
+    const unsigned wslot = sw[lane];
+    __syncwarp();
+    // ---- the credit / deferred recurrence, in call order: branch-free,
+    // each slot's result left in its lane ----
+    const unsigned def0 = defm;
+    const CW cw0 = cw;
+    unsigned myres = 0, mydef = 0;
+    CW mycw = 0;
+    int failslot = 32;
+    auto scan = [&](int nlim) {
+      for (int g0 = 0; g0 < nlim; g0 += 8) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int j = g0 + t;
+          const bool act = j < nlim;
+          const unsigned cur = __shfl_sync(kFull, wslot, j & 31);
+          const int p = (int)(cur & 7u), sh = p << 3;
+          const bool bad = act && ((defm >> p) & 1u);  // pushed while deferred
+          failslot = (bad && failslot == 32) ? j : failslot;
+          const unsigned cred = (unsigned)(cw >> sh) & 0xffu;
+          const bool has = cred != 0u;
+          const unsigned nf = has ? cred - 1u : ((cur >> 4) & 0xffu);
+          const unsigned out = has ? 0u : ((cur >> 3) & 1u);
+          const CW ncw = cw ^ ((CW)(cred ^ nf) << sh);
+          const unsigned rel = out ? 0u : (defm & (cur >> 12));
+          const unsigned ndef = (defm | (out << p)) & ~rel;
+          cw = act ? ncw : cw;
+          defm = act ? ndef : defm;
+          const bool mine = lane == j;
+          myres = mine ? ((rel << 8) | out) : myres;
+          mydef = mine ? defm : mydef;
+          mycw = mine ? cw : mycw;
+        }
+      }
+    };
+    scan(nd);
+    int ndone = nd;
+    if (failslot < 32) {  // rare: redo up to the failing decision from the chunk's start
+      ndone = failslot;
+      cw = cw0;
+      defm = def0;
+      scan(ndone);
+    }
+    const unsigned fdl = __ballot_sync(kFull, is_dec && myslot == failslot);
+    const unsigned fail_dec = fdl ? (unsigned)(__ffs(fdl) - 1) : 32u;
+    // ---- pulls: none from a deferred worker (the set after the last decision before it) ----
+    const unsigned done = fail_dec < 32 ? (md & ((1u << fail_dec) - 1u)) : md;
+    const unsigned pl_mask = mp & (fail_dec < 32 ? ((1u << fail_dec) - 1u) : kFull);
+    const int slot_before = __popc(done & lt) - 1;
+    const unsigned dm_sh = __shfl_sync(kFull, mydef, slot_before < 0 ? 0 : slot_before);
+    const unsigned dm_here = slot_before < 0 ? def0 : dm_sh;
+    const unsigned hit = __ballot_sync(kFull, ((pl_mask >> lane) & 1u) && ((dm_here >> (c.worker & 31)) & 1u));
+    int fail = -1;
+    unsigned applied = done;
+    int napplied = ndone;
+    if (hit) {
+      fail = __ffs(hit) - 1;
+      applied = done & ((1u << fail) - 1u);
+      napplied = __popc(applied);
+      // the recurrence rolls back to the last decision before the failing pull
+      const unsigned long long back_cw = (unsigned long long)mycw;
+      const unsigned rd = __shfl_sync(kFull, mydef, napplied > 0 ? napplied - 1 : 0);
+      const unsigned long long rc = __shfl_sync(kFull, back_cw, napplied > 0 ? napplied - 1 : 0);
+      defm = napplied > 0 ? rd : def0;
+      cw = napplied > 0 ? (CW)rc : cw0;
+    } else if (fail_dec < 32) {
+      fail = (int)fail_dec;
+      pushes += 1;
+    } else if (limit < m) {
+      fail = limit;
+    }
+    // ---- the chunk's decisions out, tables forward ----
+    const int nap = napplied;
+    if (lane < nap && n_dec + lane < a.trace_cap) a.decisions[n_dec + lane] = (long long)myres;
+    n_dec += nap;
+    pushes += nap;
+    g.decisions += nap;
+#pragma unroll
+    for (int q = 0; q < PM; ++q) {
+      const unsigned mqa = mq[q] & applied;
+      const int k = __popc(mqa);
+      const int l1 = mqa ? 31 - __clz(mqa) : 0;
+      const unsigned rest = mqa & ~(1u << l1);
+      const double t1 = __shfl_sync(kFull, c.now, l1);
+      const double t2 = __shfl_sync(kFull, c.now, rest ? 31 - __clz(rest) : 0);
+      if (k) {
+        g.previous[q] = k >= 2 ? t2 : g.latest[q];
+        g.latest[q] = t1;
+        g.clocks[q] += k;
+        g.populated[q] += k;
+      }
+    }
+    __syncwarp();
+    if (fail >= 0) {
+      status = PS_E_PROTOCOL;
+      valid = base + fail;
+      break;
+    }
+    valid = base + m;
+    if (lane == 0 && valid < n) st_relaxed_u64(&a.out->validated, (unsigned long long)valid << 1);
+    c = nx;
+  }
+  if (lane == 0) st_relaxed_u64(&a.out->validated, ((unsigned long long)valid << 1) | 1ull);
+#pragma unroll
+  for (int q = 0; q < PM; ++q) g.credits[q] = (int)((cw >> (8 * q)) & (CW)0xffu);
+  g.deferred = defm;
+  if (lane == 0) g.store(a.ctrl->gate);
+  if (lane == 0) {
+    a.out->t_control_done = globaltimer_ns();
+    a.out->events = valid;
+    a.out->pushes = pushes;
+    a.out->trace_rows = n_dec;
+    a.out->unfinished = 0ull;
+    if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
+  }
+}
+
 // The gate warp of a replay: decides every DECIDE in order and validates the
 // protocol (unknown worker, pull or push while deferred). It publishes a
 // watermark -- (calls validated << 1) | done -- once per 32 calls; the data
@@ -789,6 +1038,16 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
   __shared__ double2 dq[32];  // this chunk's decides: (now, call index << 32 | worker)
   const int lane = threadIdx.x & 31;
   const int P = a.P;
+  if constexpr (PM > 0) {
+    if (a.gate_scan) {
+      RegGate<PM> rg;
+      rg.load(a.ctrl->gate, a.reset_gate != 0);
+      if (gate_scan_eligible<PM>(rg)) {
+        gate_warp_replay_scan<PM>(a, rg);
+        return;
+      }
+    }
+  }
   ReplayGate<PM> g;
   g.load(a.ctrl->gate, a.reset_gate != 0, sgate);
   long long n_dec = 0, pushes = 0, valid = 0;
@@ -905,13 +1164,18 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
 constexpr int kRing = 256;  // per-CTA finiteness aggregation ring (> max warp skew in updates)
 
 // Loads of one worker's update slice; V float4 per lane, element u at lo + lane + 32u.
-template <int V>
+// KEEP: the source is read-only for the whole kernel and re-read by this warp
+// (the replay's resident updates) -- cache it in L1. Never for buffers the
+// kernel itself writes (the simulated run's gradient slots): .nc loads are not
+// coherent with this kernel's own stores.
+template <int V, bool KEEP = false>
 __device__ __forceinline__ void load_slice(float4 (&r)[V], const float4* src, long long lo, long long hi,
                                            int lane) {
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     const long long j = lo + lane + 32ll * u;
-    r[u] = j < hi ? ld_stream(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (KEEP) r[u] = j < hi ? ld_keep(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    else r[u] = j < hi ? ld_stream(src + j) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -1199,7 +1463,7 @@ __device__ void data_warp_replay(const SimArgs& a, unsigned dw, unsigned* s_ring
         if (m) {
           ls[k] = __ffs(m) - 1;
           m &= m - 1;
-          if constexpr (V > 0) load_slice<V>(r[k], slice_of(c, ls[k]), lo, hi, lane);
+          if constexpr (V > 0) load_slice<V, true>(r[k], slice_of(c, ls[k]), lo, hi, lane);
         }
       }
 #pragma unroll
@@ -1286,7 +1550,7 @@ __device__ void data_warp_replay(const SimArgs& a, unsigned dw, unsigned* s_ring
           calls &= calls - 1;
           idx[k] = i;
           if constexpr (V > 0)
-            if (((c0.ma & ~bits) >> i) & 1u) load_slice<V>(g[k], slice_of(c0, i), lo, hi, lane);
+            if (((c0.ma & ~bits) >> i) & 1u) load_slice<V, true>(g[k], slice_of(c0, i), lo, hi, lane);
         }
       }
       if constexpr (V > 0) {
@@ -1463,7 +1727,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
           calls &= calls - 1;
           idx[k] = i;
           offk[k] = __shfl_sync(kFull, c.off, i);
-          if (((c.ma & ~rej) >> i) & 1u) load_slice<V>(g[k], synth4 + offk[k], lo, hi, lane);
+          if (((c.ma & ~rej) >> i) & 1u) load_slice<V, true>(g[k], synth4 + offk[k], lo, hi, lane);
         }
       }
 #pragma unroll
@@ -1509,24 +1773,33 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
       if (__any_sync(kFull, ga != ga)) gb |= 1u << i;
     }
   };
+  // CTA aggregation in shared memory: per ring slot a bits word and an
+  // arrival count, both native 32-bit shared atomics (a 64-bit shared atomic
+  // add is a compare-and-swap loop, and the CTA's warps all hit the same slot)
   auto publish = [&](long long chunk, unsigned bits) {
     if (lane == 0) {
-      unsigned long long* w = &s_ring[chunk & (kRingChunks - 1)];
-      if (bits) atomicOr(w, (unsigned long long)bits);
-      const unsigned long long old = atomicAdd(w, 1ull << 32);
-      if ((unsigned)(old >> 32) == (unsigned)warps_here - 1) {  // last warp of this CTA
-        const unsigned long long b = atomicExch(w, 0ull) & 0xffffffffull;
-        if (b) atomicOr(&gchunk[chunk], b);
+      unsigned* w = &s_ring32[2 * (chunk & (kRingChunks - 1))];
+      if (bits) atomicOr(w, bits);
+      __threadfence_block();  // the bits before the arrival
+      if (atomicAdd(w + 1, 1u) == (unsigned)warps_here - 1) {  // last warp of this CTA
+        __threadfence_block();
+        const unsigned b = atomicExch(w, 0u);
+        atomicExch(w + 1, 0u);
+        if (b) atomicOr(&gchunk[chunk], (unsigned long long)b);
         atomicAdd(&gchunk[chunk], 1ull << 32);
       }
     }
   };
-  auto verdict = [&](long long chunk) -> unsigned {
+  // `first`: a sample of the chunk's word loaded ahead (have_first), so the
+  // common case -- the verdict is long final -- costs no load latency here
+  auto verdict = [&](long long chunk, unsigned long long first = 0ull, bool have_first = false) -> unsigned {
     unsigned long long v = 0;
     if (lane == 0) {
-      while ((unsigned)((v = ld_relaxed_u64(&gchunk[chunk])) >> 32) < a.n_ctas) {
+      v = have_first ? first : ld_relaxed_u64(&gchunk[chunk]);
+      while ((unsigned)(v >> 32) < a.n_ctas) {
         if (globaltimer_ns() - t0 > a.timeout_ns) { timed_out = true; break; }
         __nanosleep(20);
+        v = ld_relaxed_u64(&gchunk[chunk]);
       }
     }
     timed_out = __shfl_sync(kFull, (int)timed_out, 0) != 0;
@@ -1542,10 +1815,10 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   for (int j = 0; j <= L; ++j) { LV[j] = 0; RB[j] = 0; FIN[j] = true; C[j].wb = 0; C[j].ma = 0; C[j].mp = 0; }
   // resolve pending entry J (chunk number `chunk - J`): commit it, or roll
   // back to its checkpoint and replay it and everything newer with verdicts
-  auto resolve = [&](auto J_, long long chunk) {
+  auto resolve = [&](auto J_, long long chunk, unsigned long long first = 0ull, bool have_first = false) {
     constexpr int J = decltype(J_)::value;
     if (FIN[J]) return;
-    const unsigned bits = verdict(chunk - J) & LV[J];
+    const unsigned bits = verdict(chunk - J, first, have_first) & LV[J];
     if (timed_out) return;
     if (!(bits & C[J].ma)) {
       applied += __popc(C[J].ma & LV[J]);
@@ -1571,9 +1844,13 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   int2 raw = load_raw(0);
   bool stop = false;
   long long chunk = 0;
+  unsigned long long wm = 0;  // the gate's watermark, loaded a chunk ahead
+  if (lane == 0) wm = ld_relaxed_u64(&a.out->validated);
   for (long long base = 0; base < n && !stop && !timed_out; base += 32, ++chunk) {
-    unsigned long long wm = 0;
-    if (lane == 0) wm = ld_relaxed_u64(&a.out->validated);
+    // the verdict word of the oldest pending chunk, in flight while this one is numbered
+    unsigned long long vpre = 0;
+    const bool vhave = lane == 0 && !FIN[L] && chunk - 1 - L >= 0;
+    if (vhave) vpre = ld_relaxed_u64(&gchunk[chunk - 1 - L]);
     Chunk cur;
     number(raw, cur);
     raw = load_raw(base + 32);  // in flight for the next chunk
@@ -1595,7 +1872,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     const int m = upto > base ? (int)(upto - base) : 0;
     const unsigned live = m >= 32 ? kFull : ((1u << m) - 1u);
     // the oldest pending chunk must be final before its slot is reused
-    resolve(std::integral_constant<int, L>{}, chunk - 1);
+    resolve(std::integral_constant<int, L>{}, chunk - 1, vpre, vhave);
 #pragma unroll
     for (int j = L; j > 0; --j) {
       C[j] = C[j - 1]; LV[j] = LV[j - 1]; RB[j] = RB[j - 1]; FIN[j] = FIN[j - 1];
@@ -1609,6 +1886,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     exec(cur, live, 0u, gb, rb);
     RB[0] = rb;
     publish(chunk, gb);
+    if (lane == 0) wm = ld_relaxed_u64(&a.out->validated);  // for the next chunk
   }
   // drain: every pending chunk final, oldest first
   if (!timed_out) {
@@ -1985,6 +2263,10 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   a.n_data_warps = (unsigned)((grid - 1) * (kSimThreads / 32));
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.base_version = h->hctrl->gate.version;
+  {
+    const char* v = getenv("PS_REPLAY_GATE_SCAN");
+    a.gate_scan = v ? atoi(v) != 0 : 1;
+  }
   void* args[] = {&a};
   PS_CK(h, cudaEventRecord(h->ev0, h->stream));
   if ((rc = ps_order_after_producer(h))) return rc;  // resident updates may come from the caller's stream

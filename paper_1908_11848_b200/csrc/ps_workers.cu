@@ -52,6 +52,7 @@ using namespace dssp;
 namespace {
 
 constexpr int kWThreads = 256;
+constexpr int kWUnroll = 4;
 
 struct WSlot {                    // per worker; reset by the last CTA of each kernel
   unsigned start;                 // CTAs that have started (first one takes the ticket)
@@ -212,14 +213,32 @@ __global__ void __launch_bounds__(kWThreads) k_wpush(WArgs a) {
     rec = reinterpret_cast<float4*>(a.record + (s->pushes % a.record_cap) * a.dpad);
   unsigned bad = 0;
   if (!skip) {
-    const long long stride = (long long)gridDim.x * kWThreads;
-    for (long long j = (long long)blockIdx.x * kWThreads + threadIdx.x; j < a.nv; j += stride) {
-      const float4 g = ld_stream(g4 + j);
-      const float4 r = apply4(src[j], a.lr, g);
-      bad |= nonfinite4(g) ? 1u : 0u;
-      bad |= nonfinite4(r) ? 2u : 0u;
-      dst[j] = r;
-      if (rec) rec[j] = g;
+    // kWUnroll float4 per thread per trip, every load issued before the
+    // first use: the weights may sit across NVLink, where one load in flight
+    // per thread would leave the link idle
+    const long long stride = (long long)gridDim.x * kWThreads * kWUnroll;
+    for (long long base = (long long)blockIdx.x * kWThreads * kWUnroll + threadIdx.x; base < a.nv;
+         base += stride) {
+      float4 g[kWUnroll], w[kWUnroll];
+#pragma unroll
+      for (int u = 0; u < kWUnroll; ++u) {
+        const long long j = base + (long long)u * kWThreads;
+        if (j < a.nv) {
+          g[u] = ld_stream(g4 + j);
+          w[u] = src[j];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kWUnroll; ++u) {
+        const long long j = base + (long long)u * kWThreads;
+        if (j < a.nv) {
+          const float4 r = apply4(w[u], a.lr, g[u]);
+          bad |= nonfinite4(g[u]) ? 1u : 0u;
+          bad |= nonfinite4(r) ? 2u : 0u;
+          dst[j] = r;
+          if (rec) rec[j] = g[u];
+        }
+      }
     }
     if (blockIdx.x == 0 && threadIdx.x < (a.n & 3)) {
       const long long i = (a.nv << 2) + threadIdx.x;
@@ -322,9 +341,21 @@ __global__ void __launch_bounds__(kWThreads) k_wpull(WArgs a) {
     const int cur = ld_volatile_s32_(&a.ctrl->cur);
     const float4* src = reinterpret_cast<const float4*>(cur ? a.w1 : a.w0);
     float4* dst = reinterpret_cast<float4*>(a.params);
-    const long long stride = (long long)gridDim.x * kWThreads;
-    for (long long j = (long long)blockIdx.x * kWThreads + threadIdx.x; j < a.nv; j += stride)
-      dst[j] = src[j];
+    const long long stride = (long long)gridDim.x * kWThreads * kWUnroll;
+    for (long long base = (long long)blockIdx.x * kWThreads * kWUnroll + threadIdx.x; base < a.nv;
+         base += stride) {
+      float4 v[kWUnroll];
+#pragma unroll
+      for (int u = 0; u < kWUnroll; ++u) {
+        const long long j = base + (long long)u * kWThreads;
+        if (j < a.nv) v[u] = src[j];
+      }
+#pragma unroll
+      for (int u = 0; u < kWUnroll; ++u) {
+        const long long j = base + (long long)u * kWThreads;
+        if (j < a.nv) dst[j] = v[u];
+      }
+    }
     if (blockIdx.x == 0 && threadIdx.x < (a.n & 3)) {
       const long long i = (a.nv << 2) + threadIdx.x;
       a.params[i] = (cur ? a.w1 : a.w0)[i];
@@ -542,7 +573,18 @@ int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, wdev);
-  b.ctas = sms / 8 > 4 ? sms / 8 : 4;   // a small footprint: the workers keep their GPU
+  // a small footprint for small models (the workers keep their GPU); more
+  // CTAs as the vector grows -- each CTA keeps a bounded number of loads in
+  // flight, and a remote (NVLink) apply is latency-bound per CTA -- up to
+  // half the SMs (PS_WORKERS_CTAS overrides)
+  {
+    const long long per_cta = 256LL * kWUnroll * 4;  // float4 per CTA: about four trips
+    long long want = ((h->d >> 2) + per_cta - 1) / per_cta;
+    const long long lo_c = sms / 8 > 4 ? sms / 8 : 4, hi_c = sms / 2 > lo_c ? sms / 2 : lo_c;
+    want = want < lo_c ? lo_c : want > hi_c ? hi_c : want;
+    const char* v = getenv("PS_WORKERS_CTAS");
+    b.ctas = v && atoi(v) > 0 ? atoi(v) : (int)want;
+  }
   b.dev = wdev;
   b.stream = (cudaStream_t)cuda_stream;
   b.grad = grad;
