@@ -18,6 +18,10 @@ if mode == "gate":      # decides only: the gate warp alone
     calls = [c for c in calls if c[0] == "decide"]
 elif mode == "data":    # pulls and applies only: the data warps alone
     calls = [c for c in calls if c[0] != "decide"]
+elif mode == "pulls":   # the pulls alone
+    calls = [c for c in calls if c[0] == "pull"]
+elif mode == "applies":  # the applies alone
+    calls = [c for c in calls if c[0] == "apply"]
 eng = Engine(name, 4, s, r, 0.05, d, w0=initial_weights_f64(c2_config(name, s, r), d))
 rp = DeviceReplay(eng, calls, torch.from_numpy(synthetic_host(4, 2, d)).cuda(), 2)
 for _ in range(3):
