@@ -801,6 +801,17 @@ def single_gpu_extras(torch, ps, line):
                               "calls_per_step": len(calls), "updates_per_step": n_apply,
                               "defers_per_step": sum(1 for o, _ in check.decisions if o == "defer")}
         parity.setdefault("replay_decisions_identical_to_reference", {})[name] = got == want
+    # the same data side with the control taken out (ps_replay_ceiling), on
+    # this box: the roofline of the replay, which is latency-, not HBM-bound
+    n_pull = sum(1 for c in reference_calls("dssp")[0] if c[0] == "pull")
+    n_apply = sum(1 for c in reference_calls("dssp")[0] if c[0] == "apply")
+    ceil_ms = replays["dssp"].engine.replay_ceiling_ms(n_pull, n_apply, reps=7)
+    data_ceiling = {"ms": ceil_ms, "pulls": n_pull, "applies": n_apply,
+                    "frac_of_step": ceil_ms / per_paradigm["dssp"]["ms_per_step"],
+                    "what": "every data warp streams the step's pulls (stores of its register-resident "
+                            "slice into 8 rotating replicas) and applies (L1-kept loads of 8 rotating "
+                            "updates + w - lr*g) with no numbering, gate, verdicts or checkpoints, on the "
+                            "replay's own grid and slices; frac_of_step = ceiling / DSSP step"}
     for name, s, r in PARADIGMS:
         cfg, sim = sims[name]
         times, applied = [], 0
@@ -836,10 +847,12 @@ def single_gpu_extras(torch, ps, line):
         "workload": "C2 (BASELINE configs[1]): ResNet-20-sized single-GPU server d=272474 fp32, "
                     "P=4, gtx-mix; step = the server serving the reference's recorded request "
                     "stream of one run (1,000 pushes, 1,004 pulls, 1,000 decisions) in one kernel",
-        "bound": "latency: the 1 MB of weights live in registers and the updates in L2 for the "
-                 "whole stream (dram_bytes_per_launch from ncu), so it is reported per call and "
-                 "per decision, not as an HBM fraction",
+        "bound": "latency: the 1 MB of weights live in registers and the updates in L1/L2 for "
+                 "the whole stream (dram_bytes_per_launch from ncu), so it is reported per call and "
+                 "per decision and against data_ceiling (the same loads and stores with no "
+                 "control), not as an HBM fraction",
         "dram_bytes_per_launch": traffic,
+        "data_ceiling": data_ceiling,
         "value": per_paradigm["dssp"]["updates_per_s"], "unit": "updates/s",
         "per_paradigm": per_paradigm, "device_simulation": device_sim, "parity": parity,
         "e2e": {"value": eb_value, "unit": "updates/s", "h2d_bytes_per_step": eb_h2d,

@@ -211,6 +211,13 @@ int ps_replay_decisions(ps_server* h, int64_t* out, int64_t cap, int64_t* n);
  * a simulation keeps its staging (PULL_ARRIVE) and active (PULL_RETURN)
  * copies there. dst_host receives d fp32 values. */
 int ps_replay_read_replica(ps_server* h, int32_t worker, int32_t buf, float* dst_host);
+/* Measurement only (no reference counterpart): the replay's data side with
+ * no control at all -- every data warp streams `pulls` stores of its
+ * register-resident slice into 8 rotating scratch replicas and `applies`
+ * loads + applies from 8 rotating scratch updates, interleaved, on the
+ * replay's own grid and slice layout. The best of `reps` device times is the
+ * ceiling ps_replay_run's data warps are measured against. */
+int ps_replay_ceiling(ps_server* h, int32_t pulls, int32_t applies, int32_t reps, double* best_ms);
 int ps_sim_trace(ps_server* h, ps_trace_row* rows, int64_t cap, int64_t* n);
 /* Loss samples of the last run: (version, 0.5*||w - c||^2 in fp64). */
 int ps_sim_losses(ps_server* h, int64_t* versions, double* losses, int64_t cap, int64_t* n);

@@ -101,6 +101,7 @@ SIGNATURES = {
     "ps_replay_run": (ctypes.c_int, [_P, _P, _I64, _P, _I32, _I32, _I32, ctypes.POINTER(PSSimResult)]),
     "ps_replay_decisions": (ctypes.c_int, [_P, _PI64, _I64, _PI64]),
     "ps_replay_read_replica": (ctypes.c_int, [_P, _I32, _I32, _P]),
+    "ps_replay_ceiling": (ctypes.c_int, [_P, _I32, _I32, _I32, _PD]),
     "ps_sim_losses": (ctypes.c_int, [_P, _PI64, _PD, _I64, _PI64]),
     "ps_last_kernel_ms": (ctypes.c_int, [_P, _PD]),
     "ps_set_profiling": (ctypes.c_int, [_P, _I32]),

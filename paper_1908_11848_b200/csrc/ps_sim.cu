@@ -1949,6 +1949,49 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   else data_warp<V>(a, dw, s_ring, kSimThreads / 32);
 }
 
+// ps_replay_ceiling: the replay's data warps with the control taken out (see
+// include/dssp_ps.h). Same slice layout and load / store instructions as
+// data_warp_replay_spec; the call stream is fixed (apply, pull, apply, ...).
+template <int V>
+__global__ void __launch_bounds__(kSimThreads) k_replay_ceiling(const float4* W, float4* rep, const float4* upd,
+                                                                long long nv, long long dv4, int pulls,
+                                                                int applies, float lr, float4* sink,
+                                                                unsigned n_data_warps) {
+  if (blockIdx.x == 0) return;  // the replay's CTA 0 is the gate
+  const int lane = threadIdx.x & 31;
+  const long long dw = ((long long)(blockIdx.x - 1) * kSimThreads + threadIdx.x) >> 5;
+  const long long per = (nv + n_data_warps - 1) / n_data_warps;
+  const long long lo = dw * per < nv ? dw * per : nv, hi = lo + per < nv ? lo + per : nv;
+  float4 w[V];
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const long long j = lo + lane + 32ll * u;
+    w[u] = j < hi ? W[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int n = pulls > applies ? pulls : applies;
+  for (int c = 0; c < n; ++c) {
+    if (c < applies) {
+      float4 g[V];
+      load_slice<V, true>(g, upd + (long long)(c & 7) * dv4, lo, hi, lane);
+#pragma unroll
+      for (int u = 0; u < V; ++u) w[u] = apply4(w[u], lr, g[u]);
+    }
+    if (c < pulls) {
+      float4* dst = rep + (long long)(c & 7) * dv4;
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const long long j = lo + lane + 32ll * u;
+        if (j < hi) dst[j] = w[u];
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+    const long long j = lo + lane + 32ll * u;
+    if (j < hi) sink[j] = w[u];
+  }
+}
+
 // After the run: fold the data side's counters into the control block.
 __global__ void k_sim_finish(Ctrl* ctrl, SimOut* out) {
   ctrl->gate.version += out->applied;
@@ -2297,6 +2340,45 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   if (o.status == PS_E_DIVERGED)
     return ps_fail(h, PS_E_DIVERGED, "weights went non-finite on worker " + std::to_string(o.diverged_worker));
   if (o.status == PS_E_PROTOCOL) return ps_fail(h, PS_E_PROTOCOL, "protocol violation in the replayed calls");
+  return PS_OK;
+}
+
+int ps_replay_ceiling(ps_server* h, int32_t pulls, int32_t applies, int32_t reps, double* best_ms) {
+  DevGuard guard(h->dev);
+  if (pulls < 0 || applies < 0 || reps < 1) return ps_fail(h, PS_E_VALUE, "pulls, applies >= 0 and reps >= 1");
+  int grid = 0;
+  const void* kern = nullptr;
+  int rc = select_loop_kernel(h, 4, 0, &grid, &kern);  // the replay's grid for this vector
+  if (rc) return rc;
+  const long long dwarps = (long long)(grid - 1) * (kSimThreads / 32);
+  const long long need_v = ((h->nv + dwarps - 1) / dwarps + 31) / 32;
+  if (need_v > 4) return ps_fail(h, PS_E_VALUE, "the ceiling probe covers register-resident slices (V <= 4)");
+  float4 *scratch = nullptr;
+  const size_t dv4 = (size_t)h->dpad / 4;
+  PS_CK(h, cudaMalloc(&scratch, (17 * dv4) * sizeof(float4)));  // 8 replicas, 8 updates, 1 sink
+  rc = PS_OK;
+  double best = 1e30;
+  if (cudaMemsetAsync(scratch, 0, 17 * dv4 * sizeof(float4), h->stream) != cudaSuccess) rc = PS_E_CUDA;
+  for (int r = 0; r < reps && rc == PS_OK; ++r) {
+    cudaEventRecord(h->ev0, h->stream);
+    const float4* W = reinterpret_cast<const float4*>(h->w[h->cur]);
+    float4* rep = scratch;
+    const float4* upd = scratch + 8 * dv4;
+    float4* sink = scratch + 16 * dv4;
+    const float lr = (float)h->cfg.learning_rate;
+    const unsigned ndw = (unsigned)dwarps;
+    if (need_v <= 1) k_replay_ceiling<1><<<grid, kSimThreads, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
+    else if (need_v <= 2) k_replay_ceiling<2><<<grid, kSimThreads, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
+    else k_replay_ceiling<4><<<grid, kSimThreads, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
+    cudaEventRecord(h->ev1, h->stream);
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess) { rc = PS_E_CUDA; break; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    if (ms < best) best = ms;
+  }
+  cudaFree(scratch);
+  if (rc) return ps_fail(h, rc, "replay ceiling probe failed");
+  *best_ms = best;
   return PS_OK;
 }
 

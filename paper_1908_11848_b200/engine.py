@@ -217,6 +217,13 @@ class Engine:
         self.check(self.lib.ps_profile_floor(self._h, ctypes.byref(ms)))
         return ms.value
 
+    def replay_ceiling_ms(self, pulls, applies, reps=5):
+        """The replay's data side with no control (ps_replay_ceiling): best
+        device ms of `pulls` stores and `applies` loads+applies per warp."""
+        ms = ctypes.c_double(0)
+        self.check(self.lib.ps_replay_ceiling(self._h, int(pulls), int(applies), int(reps), ctypes.byref(ms)))
+        return ms.value
+
     def set_profiling(self, on=True):
         """Bracket every per-op launch with CUDA events (last_kernel_ms)."""
         self.lib.ps_set_profiling(self._h, 1 if on else 0)

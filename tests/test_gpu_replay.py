@@ -182,3 +182,16 @@ def test_resident_update_layout_is_validated():
             DeviceReplay(eng, calls, bad, 1)
     DeviceReplay(eng, calls, torch.zeros(2, 1, 12, device="cuda"), 1).run()
     eng.close()
+
+
+def test_replay_ceiling_probe():
+    """ps_replay_ceiling (measurement export): the C2-shaped data side with no
+    control runs, reports a positive time, grows with the call count, and
+    refuses a bad request like every other export."""
+    eng = Engine("dssp", 4, 3, 12, 0.05, 272_474)
+    short = eng.replay_ceiling_ms(100, 100, reps=3)
+    full = eng.replay_ceiling_ms(1004, 1000, reps=3)
+    assert 0 < short < full
+    with pytest.raises(ValueError):
+        eng.replay_ceiling_ms(10, 10, reps=0)
+    eng.close()
