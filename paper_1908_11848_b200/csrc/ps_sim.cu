@@ -1642,10 +1642,10 @@ __device__ void data_warp_replay(const SimArgs& a, unsigned dw, unsigned* s_ring
 // the checkpoint and re-executes that chunk and the later ones with their
 // final verdicts -- pulls included, so every replica ends up exactly as the
 // in-order server would have written it.
-template <int V>
+template <int V, int KG4 = 2>
 __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s_ring32, int warps_here) {
   static_assert(V > 0 && V <= 4, "register-resident slices of at most 4 float4 per lane");
-  constexpr int KG = V == 1 ? 16 : V == 2 ? 8 : 2;  // calls per group
+  constexpr int KG = V == 1 ? 16 : V == 2 ? 8 : KG4;  // calls per group
   constexpr int L = V <= 2 ? 3 : 2;  // chunks executed before their verdict is read
   constexpr int kRingChunks = kRing / 2;
   unsigned long long* s_ring = reinterpret_cast<unsigned long long*>(s_ring32);
@@ -1949,17 +1949,35 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   else data_warp<V>(a, dw, s_ring, kSimThreads / 32);
 }
 
+// The replay alone with NT threads per CTA (select_replay_nt): fewer, wider
+// data warps per SM -- the per-call control of a warp is the same whatever
+// its slice width, so wider slices spend it on more data.
+template <int V, int CTL, int NT, int KG4>
+__global__ void __launch_bounds__(NT, 1) k_replay_nt(SimArgs a) {
+  __shared__ ps_gate_state sg;
+  __shared__ __align__(8) unsigned s_ring[kRing];
+  for (int i = threadIdx.x; i < kRing; i += blockDim.x) s_ring[i] = 0;
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (threadIdx.x >= 32) return;
+    gate_warp_replay<CTL>(a, &sg);
+    return;
+  }
+  const unsigned dw = ((blockIdx.x - 1) * NT + threadIdx.x) >> 5;
+  data_warp_replay_spec<V, KG4>(a, dw, s_ring, NT / 32);
+}
+
 // ps_replay_ceiling: the replay's data warps with the control taken out (see
 // include/dssp_ps.h). Same slice layout and load / store instructions as
 // data_warp_replay_spec; the call stream is fixed (apply, pull, apply, ...).
 template <int V>
-__global__ void __launch_bounds__(kSimThreads) k_replay_ceiling(const float4* W, float4* rep, const float4* upd,
+__global__ void __launch_bounds__(kSimThreads, 1) k_replay_ceiling(const float4* W, float4* rep, const float4* upd,
                                                                 long long nv, long long dv4, int pulls,
                                                                 int applies, float lr, float4* sink,
                                                                 unsigned n_data_warps) {
   if (blockIdx.x == 0) return;  // the replay's CTA 0 is the gate
   const int lane = threadIdx.x & 31;
-  const long long dw = ((long long)(blockIdx.x - 1) * kSimThreads + threadIdx.x) >> 5;
+  const long long dw = ((long long)(blockIdx.x - 1) * blockDim.x + threadIdx.x) >> 5;
   const long long per = (nv + n_data_warps - 1) / n_data_warps;
   const long long lo = dw * per < nv ? dw * per : nv, hi = lo + per < nv ? lo + per : nv;
   float4 w[V];
@@ -2055,6 +2073,43 @@ int select_loop_kernel(ps_server* h, int P, int data_ctas, int* grid_out, const 
   *grid_out = grid;
   *kern_out = kern;
   return PS_OK;
+}
+
+// The replay's default kernel when P <= 8 and the slice fits V <= 4 float4 per
+// lane at 4 data warps per CTA (PS_REPLAY_NT=256 selects the 8-warp k_sim):
+// the elapsed time of a replay is set by the per-call latency of one warp's
+// instruction stream, not by its slice width, so 4 warps per SM with twice
+// the slice each do the same work with half the per-call control
+// (profiles/r2_c2_replay_narrow_cta.txt: 0.431 vs 0.445 ms).
+bool select_replay_nt(ps_server* h, int P, int data_ctas, int* grid_out, const void** kern_out, int* nt_out) {
+  const char* v = getenv("PS_REPLAY_NT");
+  if ((v && atoi(v) != 128) || P > 8) return false;
+  int grid = data_ctas > 0 ? data_ctas + 1 : h->sm_count;
+  if (grid > h->sm_count) grid = h->sm_count;
+  if (grid < 2) grid = 2;
+  const long long dwarps = (long long)(grid - 1) * 4;
+  const long long need_v = ((h->nv + dwarps - 1) / dwarps + 31) / 32;
+  if (need_v > 4) return false;
+  const int vi = need_v <= 2 ? 0 : 1;
+  const int pi = P <= 2 ? 0 : P <= 4 ? 1 : 2;
+  static const void* const table[2][3] = {
+      {(const void*)k_replay_nt<2, 2, 128, 2>, (const void*)k_replay_nt<2, 4, 128, 2>, (const void*)k_replay_nt<2, 8, 128, 2>},
+      {(const void*)k_replay_nt<4, 2, 128, 2>, (const void*)k_replay_nt<4, 4, 128, 2>, (const void*)k_replay_nt<4, 8, 128, 2>}};
+  static int occupancy[2][3] = {{-1, -1, -1}, {-1, -1, -1}};
+  const void* kern = table[vi][pi];
+  int per_sm = occupancy[vi][pi];
+  if (per_sm < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0) != cudaSuccess) {
+      cudaGetLastError();
+      per_sm = 0;
+    }
+    occupancy[vi][pi] = per_sm;
+  }
+  if (per_sm < 1 || grid > per_sm * h->sm_count) return false;
+  *grid_out = grid;
+  *kern_out = kern;
+  *nt_out = 128;
+  return true;
 }
 
 }  // namespace
@@ -2277,9 +2332,10 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
                                   h->stream));
   PS_CK(h, cudaMemsetAsync(b.gcount, 0, slots * sizeof(unsigned), h->stream));
   PS_CK(h, cudaMemsetAsync(b.out, 0, sizeof(SimOut), h->stream));
-  int grid = 0;
+  int grid = 0, nt = kSimThreads;
   const void* kern = nullptr;
-  if ((rc = select_loop_kernel(h, P, data_ctas, &grid, &kern))) return rc;
+  if (!select_replay_nt(h, P, data_ctas, &grid, &kern, &nt))
+    if ((rc = select_loop_kernel(h, P, data_ctas, &grid, &kern))) return rc;
   SimArgs a{};
   a.mode = 1;
   a.P = P;
@@ -2303,7 +2359,7 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   a.decisions = b.decisions;
   a.ctrl = h->ctrl;
   a.out = (SimOut*)b.out;
-  a.n_data_warps = (unsigned)((grid - 1) * (kSimThreads / 32));
+  a.n_data_warps = (unsigned)((grid - 1) * (nt / 32));
   a.timeout_ns = 20ull * 1000 * 1000 * 1000;
   a.base_version = h->hctrl->gate.version;
   {
@@ -2313,7 +2369,7 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   void* args[] = {&a};
   PS_CK(h, cudaEventRecord(h->ev0, h->stream));
   if ((rc = ps_order_after_producer(h))) return rc;  // resident updates may come from the caller's stream
-  PS_CK(h, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSimThreads), args, 0, h->stream));
+  PS_CK(h, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(nt), args, 0, h->stream));
   PS_CK(h, cudaEventRecord(h->ev1, h->stream));
   k_sim_finish<<<1, 1, 0, h->stream>>>(h->ctrl, (SimOut*)b.out);
   PS_CK(h, cudaGetLastError());
@@ -2346,17 +2402,18 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
 int ps_replay_ceiling(ps_server* h, int32_t pulls, int32_t applies, int32_t reps, double* best_ms) {
   DevGuard guard(h->dev);
   if (pulls < 0 || applies < 0 || reps < 1) return ps_fail(h, PS_E_VALUE, "pulls, applies >= 0 and reps >= 1");
-  int grid = 0;
+  int grid = 0, nt = kSimThreads;
   const void* kern = nullptr;
-  int rc = select_loop_kernel(h, 4, 0, &grid, &kern);  // the replay's grid for this vector
-  if (rc) return rc;
-  const long long dwarps = (long long)(grid - 1) * (kSimThreads / 32);
+  int rc = PS_OK;
+  // the replay's own grid and CTA shape for this vector (P = 4: the C2 shape)
+  if (!select_replay_nt(h, 4, 0, &grid, &kern, &nt))
+    if ((rc = select_loop_kernel(h, 4, 0, &grid, &kern))) return rc;
+  const long long dwarps = (long long)(grid - 1) * (nt / 32);
   const long long need_v = ((h->nv + dwarps - 1) / dwarps + 31) / 32;
   if (need_v > 4) return ps_fail(h, PS_E_VALUE, "the ceiling probe covers register-resident slices (V <= 4)");
   float4 *scratch = nullptr;
   const size_t dv4 = (size_t)h->dpad / 4;
   PS_CK(h, cudaMalloc(&scratch, (17 * dv4) * sizeof(float4)));  // 8 replicas, 8 updates, 1 sink
-  rc = PS_OK;
   double best = 1e30;
   if (cudaMemsetAsync(scratch, 0, 17 * dv4 * sizeof(float4), h->stream) != cudaSuccess) rc = PS_E_CUDA;
   for (int r = 0; r < reps && rc == PS_OK; ++r) {
@@ -2367,9 +2424,9 @@ int ps_replay_ceiling(ps_server* h, int32_t pulls, int32_t applies, int32_t reps
     float4* sink = scratch + 16 * dv4;
     const float lr = (float)h->cfg.learning_rate;
     const unsigned ndw = (unsigned)dwarps;
-    if (need_v <= 1) k_replay_ceiling<1><<<grid, kSimThreads, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
-    else if (need_v <= 2) k_replay_ceiling<2><<<grid, kSimThreads, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
-    else k_replay_ceiling<4><<<grid, kSimThreads, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
+    if (need_v <= 1) k_replay_ceiling<1><<<grid, nt, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
+    else if (need_v <= 2) k_replay_ceiling<2><<<grid, nt, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
+    else k_replay_ceiling<4><<<grid, nt, 0, h->stream>>>(W, rep, upd, h->nv, dv4, pulls, applies, lr, sink, ndw);
     cudaEventRecord(h->ev1, h->stream);
     if (cudaStreamSynchronize(h->stream) != cudaSuccess || cudaGetLastError() != cudaSuccess) { rc = PS_E_CUDA; break; }
     float ms = 0.f;

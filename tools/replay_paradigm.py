@@ -24,7 +24,8 @@ elif mode == "applies":  # the applies alone
     calls = [c for c in calls if c[0] == "apply"]
 eng = Engine(name, 4, s, r, 0.05, d, w0=initial_weights_f64(c2_config(name, s, r), d))
 rp = DeviceReplay(eng, calls, torch.from_numpy(synthetic_host(4, 2, d)).cuda(), 2)
+ctas = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # data CTAs (0: one per SM after the gate's)
 for _ in range(3):
-    rr = rp.run(decisions=False)
-print(name, mode, "device_ms", round(rr.device_ms, 4), "gate_ms", round(rr.control_ms, 4), "data_ms", round(rr.data_ms, 4),
+    rr = rp.run(decisions=False, data_ctas=ctas)
+print(name, mode, "ctas", ctas, "device_ms", round(rr.device_ms, 4), "gate_ms", round(rr.control_ms, 4), "data_ms", round(rr.data_ms, 4),
       "decides", sum(1 for c in calls if c[0] == "decide"), "calls", len(calls))
