@@ -92,6 +92,20 @@ __device__ __forceinline__ float4 ld_keep(const float4* p) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
   return v;
 }
+// Predicated forms (no branch): the load leaves +0 when p is false; the
+// store does nothing.
+__device__ __forceinline__ float4 ld_keep_if(bool p, const float4* ptr) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];\n\t}"
+      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w) : "l"(ptr), "r"((int)p));
+  return v;
+}
+__device__ __forceinline__ void st_f4_if(bool p, float4* ptr, const float4& v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t"
+               "@q st.global.v4.f32 [%1], {%2,%3,%4,%5};\n\t}"
+               :: "r"((int)p), "l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
 __device__ __forceinline__ float4 ld_f4(const float4* p) { return *p; }
 __device__ __forceinline__ void st_f4(float4* p, const float4& v) { *p = v; }
 

@@ -1645,7 +1645,10 @@ __device__ void data_warp_replay(const SimArgs& a, unsigned dw, unsigned* s_ring
 template <int V, int KG4 = 2>
 __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s_ring32, int warps_here) {
   static_assert(V > 0 && V <= 4, "register-resident slices of at most 4 float4 per lane");
-  constexpr int KG = V == 1 ? 16 : V == 2 ? 8 : KG4;  // calls per group
+#ifndef PS_REPLAY_KG2
+#define PS_REPLAY_KG2 8
+#endif
+  constexpr int KG = V == 1 ? 16 : V == 2 ? PS_REPLAY_KG2 : KG4;  // calls per group
   constexpr int L = V <= 2 ? 3 : 2;  // chunks executed before their verdict is read
   constexpr int kRingChunks = kRing / 2;
   unsigned long long* s_ring = reinterpret_cast<unsigned long long*>(s_ring32);
@@ -1666,6 +1669,11 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     const long long j = lo + lane + 32ll * u;
     wr[u] = j < hi ? W[j] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  // this lane's element u is float4 lo + lane + 32u of every buffer
+  const float4* const sbase = synth4 + lo + lane;
+  float4* const rbase = rep4 + lo + lane;
+  const int span = (int)(hi - lo) - lane;  // element u is in the slice iff 32u < span
+  (void)sbase; (void)rbase; (void)span;
   const unsigned long long t0 = globaltimer_ns();
   int sidx_lo = 0, sidx_hi = 0, stg_lo = 0, stg_hi = 0;
   long long applied = 0, rejected = 0;
@@ -1714,6 +1722,42 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     // per-lane bits, one warp reduction per chunk (not a vote per apply)
     unsigned lrb = 0;
     unsigned calls = (c.ma | c.mp) & live;
+#ifndef PS_REPLAY_BRANCHED_SLOTS
+    // straight-line slots: every slot runs the same predicated code, so the
+    // compiler can interleave the slots of a group. A slot that is not a live
+    // apply loads nothing and keeps g = +0, and w - lr*(+0) == w bit for bit
+    // (also for -0, inf and NaN), so its apply is an exact identity; its
+    // result is not checked.
+    const unsigned mapp = c.ma & ~rej;
+    while (calls) {
+      unsigned bitk[KG];
+      float4 g[KG][V];
+      unsigned offk[KG];
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const int i = __ffs(calls) - 1;  // -1 once the chunk is exhausted
+        calls &= calls - 1;
+        bitk[k] = i >= 0 ? (1u << i) : 0u;
+        offk[k] = __shfl_sync(kFull, c.off, i & 31);
+        const bool ld = (mapp & bitk[k]) != 0u;
+#pragma unroll
+        for (int u = 0; u < V; ++u) g[k][u] = ld_keep_if(ld && 32 * u < span, sbase + offk[k] + 32 * u);
+      }
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const bool pl = (c.mp & bitk[k]) != 0u;
+#pragma unroll
+        for (int u = 0; u < V; ++u) st_f4_if(pl && 32 * u < span, rbase + offk[k] + 32 * u, wr[u]);
+        float ra = 0.f;
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          wr[u] = apply4(wr[u], a.lr, g[k][u]);
+          ra = acc_nonfinite(ra, wr[u]);
+        }
+        lrb |= (ra != ra) ? (mapp & bitk[k]) : 0u;
+      }
+    }
+#else
     while (calls) {
       int idx[KG];
       unsigned offk[KG];
@@ -1756,6 +1800,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
         }
       }
     }
+#endif
     rb = __reduce_or_sync(kFull, lrb);
     gb = 0;
     // rare: which of the non-finite results come from a non-finite update
@@ -2075,15 +2120,14 @@ int select_loop_kernel(ps_server* h, int P, int data_ctas, int* grid_out, const 
   return PS_OK;
 }
 
-// The replay's default kernel when P <= 8 and the slice fits V <= 4 float4 per
-// lane at 4 data warps per CTA (PS_REPLAY_NT=256 selects the 8-warp k_sim):
-// the elapsed time of a replay is set by the per-call latency of one warp's
-// instruction stream, not by its slice width, so 4 warps per SM with twice
-// the slice each do the same work with half the per-call control
-// (profiles/r2_c2_replay_narrow_cta.txt: 0.431 vs 0.445 ms).
+// PS_REPLAY_NT=128: the replay on 4 data warps per CTA with twice the slice
+// each (P <= 8, V <= 4). With branched call slots it beat the 8-warp k_sim
+// (0.431 vs 0.445 ms, profiles/r2_c2_replay_narrow_cta.txt); with the
+// straight-line slots the 8-warp kernel is faster again (0.36-0.37 vs 0.41
+// ms, profiles/r2_c2_replay_straight_slots.txt), so this is opt-in.
 bool select_replay_nt(ps_server* h, int P, int data_ctas, int* grid_out, const void** kern_out, int* nt_out) {
   const char* v = getenv("PS_REPLAY_NT");
-  if ((v && atoi(v) != 128) || P > 8) return false;
+  if (!v || atoi(v) != 128 || P > 8) return false;
   int grid = data_ctas > 0 ? data_ctas + 1 : h->sm_count;
   if (grid > h->sm_count) grid = h->sm_count;
   if (grid < 2) grid = 2;
