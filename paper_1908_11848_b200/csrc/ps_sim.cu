@@ -89,6 +89,7 @@ struct SimOut {
   int status, diverged_worker;
   unsigned long long t_start, t_control_done, t_data_done;  // %globaltimer ns
   unsigned long long validated;  // replay: (calls validated by the gate << 1) | done
+  unsigned long long dvalid;     // replay: (data-call descriptors published << 1) | done
 };
 
 struct SimArgs {
@@ -122,7 +123,104 @@ struct SimArgs {
   unsigned tag;
   unsigned n_ctas;
   int gate_scan;              // replay: the scan gate when eligible (PS_REPLAY_GATE_SCAN, default on)
+  unsigned long long* dstream;  // replay: the gate's data-call descriptors (DataEmit)
+  long long n_data;           // replay: pulls + applies in the stream (upper bound of dstream)
 };
+
+// The replay's data calls as a descriptor stream. A second warp of CTA 0 --
+// the emitter, beside the gate warp -- numbers the pulls and applies (apply:
+// resident update k % n_synthetic of the worker's k-th apply; pull: replica
+// (k + 1) % 2 of its k-th pull) and compacts them into one 64-bit word per
+// data call: run tag << 32 | pull << 16 | worker << 8 | buffer. It runs ahead
+// of the gate, and follows the gate's validated-calls watermark with a
+// data-call watermark (count << 1 | done), so the data never passes a
+// protocol error. The register-slice data warps read that stream instead of
+// every call and numbering it themselves: decides never reach them and the
+// per-call bookkeeping is done once, not once per data warp, and off the
+// gate's critical path. The tag makes every word self-validating (a reader
+// re-polls a word from an older run), so nobody needs an acquire -- which
+// would invalidate the L1 where the data warps keep the resident updates.
+__device__ void emit_warp_replay(const SimArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const long long n = a.n_calls;
+  const long long nchunks = (n + 31) / 32;
+  const unsigned long long t0 = globaltimer_ns();
+  int sidx_lo = 0, sidx_hi = 0, stg_lo = 0, stg_hi = 0;  // lane q: workers q and q + 32
+  long long count = 0, published = -1;
+  // per call chunk k: data calls before the end of k (dprefix) and its mask
+  // (dmask); written and read by this warp only
+  long long* dprefix = reinterpret_cast<long long*>(a.dstream + a.n_data + 32);
+  unsigned* dmask = reinterpret_cast<unsigned*>(dprefix + nchunks + 2);
+  bool done = false;
+  auto try_publish = [&](long long emitted) {
+    unsigned long long v = 0;
+    if (lane == 0) v = ld_relaxed_u64(&a.out->validated);
+    v = __shfl_sync(kFull, v, 0);
+    const long long vc = (long long)(v >> 1);
+    const bool gdone = v & 1ull;
+    long long dc;
+    bool final_ = false;
+    if (gdone && vc <= emitted * 32) {  // the gate is done and we have emitted past its end
+      const long long kk = vc / 32, r = vc % 32;
+      dc = (kk > 0 ? dprefix[kk - 1] : 0) + (r ? __popc(dmask[kk] & ((1u << r) - 1u)) : 0);
+      final_ = true;
+    } else {
+      const long long kk = (vc / 32 < emitted ? vc / 32 : emitted);  // whole chunks validated and emitted
+      dc = kk > 0 ? dprefix[kk - 1] : 0;
+    }
+    if (final_ || dc > published) {
+      if (lane == 0) st_relaxed_u64(&a.out->dvalid, ((unsigned long long)dc << 1) | (final_ ? 1ull : 0ull));
+      published = dc;
+    }
+    done = final_;
+  };
+  int2 nxt = make_int2(-1, 0);
+  if (lane < n) nxt = *reinterpret_cast<const int2*>(&a.calls[lane].kind);
+  for (long long k = 0; k < nchunks && !done; ++k) {
+    const int kind = nxt.x, worker = nxt.y;
+    const long long i1 = (k + 1) * 32 + lane;
+    nxt = i1 < n ? *reinterpret_cast<const int2*>(&a.calls[i1].kind) : make_int2(-1, 0);
+    const bool okw = worker >= 0 && worker < a.P;
+    const bool isa = okw && kind == kCallApply, isp = okw && kind == kCallPull;
+    const unsigned md = __ballot_sync(kFull, isa || isp);
+    if (md) {
+      const unsigned ma = __ballot_sync(kFull, isa);
+      const unsigned peers = __match_any_sync(kFull, isa ? worker : isp ? 64 + worker : 128 + lane);
+      const int rank = __popc(peers & lt);
+      const int wq = worker & 31;
+      const int s_lo = __shfl_sync(kFull, sidx_lo, wq), s_hi = __shfl_sync(kFull, sidx_hi, wq);
+      const int g_lo = __shfl_sync(kFull, stg_lo, wq), g_hi = __shfl_sync(kFull, stg_hi, wq);
+      int buf = 0;
+      if (isa) buf = ((worker < 32 ? s_lo : s_hi) + rank) % a.n_synth;
+      if (isp) buf = (worker < 32 ? g_lo : g_hi) ^ ((rank + 1) & 1);
+      if (isa || isp)
+        st_relaxed_u64(a.dstream + count + __popc(md & lt),
+                       ((unsigned long long)a.tag << 32) | (isp ? 1u << 16 : 0u) | ((unsigned)worker << 8) | (unsigned)buf);
+      // per-worker counters forward: the last lane of each (worker, kind) group
+      // tells the worker's home lane through a shuffle round per group leader
+      for (unsigned lead = __ballot_sync(kFull, (isa || isp) && rank == __popc(peers) - 1); lead; lead &= lead - 1) {
+        const int l = __ffs(lead) - 1;
+        const int wl = __shfl_sync(kFull, worker, l);
+        const int cnt = __shfl_sync(kFull, __popc(peers), l);
+        const bool app = (ma >> l) & 1u;
+        if (lane == (wl & 31)) {
+          if (app) { if (wl < 32) sidx_lo += cnt; else sidx_hi += cnt; }
+          else { if (wl < 32) stg_lo ^= cnt & 1; else stg_hi ^= cnt & 1; }
+        }
+      }
+    }
+    count += __popc(md);
+    if (lane == 0) { dmask[k] = md; dprefix[k] = count; }
+    __syncwarp();
+    try_publish(k + 1);
+  }
+  while (!done) {
+    if (globaltimer_ns() - t0 > a.timeout_ns) break;
+    __nanosleep(64);
+    try_publish(nchunks);
+  }
+}
 
 // Cycle accounting of the control warp, compiled in with -DPS_SIM_PROFILE.
 #ifdef PS_SIM_PROFILE
@@ -1140,7 +1238,7 @@ __device__ void gate_warp_replay(const SimArgs& a, ps_gate_state* sgate) {
       break;
     }
     valid = base + m;
-    // relaxed: the watermark publishes no data, only how far the data may go
+    // relaxed: the call watermark publishes no data, only how far the data may go
     if (lane == 0 && valid < n) st_relaxed_u64(&a.out->validated, (unsigned long long)valid << 1);
     c = nx;
   }
@@ -1656,7 +1754,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int P = a.P, nsyn = a.n_synth;
-  const long long n = a.n_calls;
+  const long long n = a.n_data;  // the gate publishes the data calls (DataEmit)
   const long long per = (a.nv + a.n_data_warps - 1) / a.n_data_warps;
   const long long lo = (long long)dw * per < a.nv ? (long long)dw * per : a.nv;
   const long long hi = lo + per < a.nv ? lo + per : a.nv;
@@ -1675,7 +1773,6 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   const int span = (int)(hi - lo) - lane;  // element u is in the slice iff 32u < span
   (void)sbase; (void)rbase; (void)span;
   const unsigned long long t0 = globaltimer_ns();
-  int sidx_lo = 0, sidx_hi = 0, stg_lo = 0, stg_hi = 0;
   long long applied = 0, rejected = 0;
   int diverged = -1;  // worker of the first non-finite result seen by this warp
   bool timed_out = false;
@@ -1683,35 +1780,29 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   // the resident updates (apply) or the replicas (pull) -- 32 bits suffice for
   // the slice widths this path serves (V <= 4)
   struct Chunk { int wb; unsigned ma, mp, off; };
-  auto load_raw = [&](long long base) {
-    const long long i = base + lane;
-    return i < n ? *reinterpret_cast<const int2*>(&a.calls[i].kind) : make_int2(-1, 0);
-  };
-  auto number = [&](int2 kw, Chunk& c) {
-    const int kind = kw.x, worker = kw.y;
-    int buf = 0;
-    const bool okw = worker >= 0 && worker < P;
-    const bool isa = okw && kind == kCallApply, isp = okw && kind == kCallPull;
+  const unsigned dv4 = (unsigned)(a.dpad >> 2);
+  // one data call per lane from the gate's descriptor stream (DataEmit)
+  auto decode = [&](unsigned d, bool in, Chunk& c) {
+    const bool isp = in && ((d >> 16) & 1u), isa = in && !((d >> 16) & 1u);
     c.ma = __ballot_sync(kFull, isa);
     c.mp = __ballot_sync(kFull, isp);
-    const unsigned peers = __match_any_sync(kFull, isa ? worker : isp ? 64 + worker : 128 + lane);
-    const int rank = __popc(peers & lt);
-    const int wq = worker & 31;
-    const int s_lo = __shfl_sync(kFull, sidx_lo, wq), s_hi = __shfl_sync(kFull, sidx_hi, wq);
-    const int g_lo = __shfl_sync(kFull, stg_lo, wq), g_hi = __shfl_sync(kFull, stg_hi, wq);
-    if (isa) buf = ((worker < 32 ? s_lo : s_hi) + rank) % nsyn;
-    if (isp) buf = (worker < 32 ? g_lo : g_hi) ^ ((rank + 1) & 1);
-    c.wb = (okw ? worker : 0) << 8 | buf;
-    const unsigned dv4 = (unsigned)(a.dpad >> 2);
+    const int worker = (int)((d >> 8) & 127u), buf = (int)(d & 255u);
+    c.wb = worker << 8 | buf;
     c.off = isa ? (unsigned)(worker * nsyn + buf) * dv4 : isp ? (unsigned)(worker * 2 + buf) * dv4 : 0u;
-    for (int q = 0; q < P; ++q) {
-      const int na = __popc(__ballot_sync(kFull, isa && worker == q));
-      const int np = __popc(__ballot_sync(kFull, isp && worker == q));
-      if (lane == (q & 31)) {
-        if (q < 32) { sidx_lo += na; stg_lo ^= np & 1; }
-        else { sidx_hi += na; stg_hi ^= np & 1; }
-      }
+  };
+  // descriptors [base, upto): each word carries the run's tag, so a word not
+  // yet written by this run is re-polled (rare: the watermark said it is there)
+  const unsigned tag = a.tag;
+  auto load_desc = [&](long long base, long long upto) -> unsigned long long {
+    const long long i = base + lane;
+    return i < upto ? ld_relaxed_u64(a.dstream + i) : ((unsigned long long)tag << 32);
+  };
+  auto settle = [&](unsigned long long v, long long base, long long upto) -> unsigned {
+    while (__any_sync(kFull, (unsigned)(v >> 32) != tag)) {
+      if ((unsigned)(v >> 32) != tag) v = load_desc(base, upto);
+      if (globaltimer_ns() - t0 > a.timeout_ns) { timed_out = true; break; }
     }
+    return (unsigned)v;
   };
   auto acc_nonfinite = [](float acc, const float4& v) {
     return __fmaf_rn(v.w, 0.f, __fmaf_rn(v.z, 0.f, __fmaf_rn(v.y, 0.f, __fmaf_rn(v.x, 0.f, acc))));
@@ -1886,19 +1977,17 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
       FIN[jj] = true;
     }
   };
-  int2 raw = load_raw(0);
   bool stop = false;
   long long chunk = 0;
-  unsigned long long wm = 0;  // the gate's watermark, loaded a chunk ahead
-  if (lane == 0) wm = ld_relaxed_u64(&a.out->validated);
+  unsigned long long wm = 0;  // the gate's data watermark, loaded a chunk ahead
+  if (lane == 0) wm = ld_relaxed_u64(&a.out->dvalid);
+  unsigned long long dnext = 0;  // the next chunk's descriptors, when already published
+  bool have_next = false;
   for (long long base = 0; base < n && !stop && !timed_out; base += 32, ++chunk) {
-    // the verdict word of the oldest pending chunk, in flight while this one is numbered
+    // the verdict word of the oldest pending chunk, in flight while this one is decoded
     unsigned long long vpre = 0;
     const bool vhave = lane == 0 && !FIN[L] && chunk - 1 - L >= 0;
     if (vhave) vpre = ld_relaxed_u64(&gchunk[chunk - 1 - L]);
-    Chunk cur;
-    number(raw, cur);
-    raw = load_raw(base + 32);  // in flight for the next chunk
     const long long need = n - base < 32 ? n : base + 32;
     if (lane == 0) {
       unsigned backoff = 32;
@@ -1906,7 +1995,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
         if (globaltimer_ns() - t0 > a.timeout_ns) { wm = ~0ull; break; }
         __nanosleep(backoff);
         backoff = backoff < 256 ? backoff * 2 : 256;
-        wm = ld_relaxed_u64(&a.out->validated);
+        wm = ld_relaxed_u64(&a.out->dvalid);
       }
     }
     wm = __shfl_sync(kFull, wm, 0);
@@ -1916,6 +2005,14 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     else upto = need;
     const int m = upto > base ? (int)(upto - base) : 0;
     const unsigned live = m >= 32 ? kFull : ((1u << m) - 1u);
+    Chunk cur;
+    decode(settle(have_next ? dnext : load_desc(base, upto), base, upto), lane < m, cur);
+    if (timed_out) break;
+    {
+      const long long nb = base + 32, nneed = n - nb < 32 ? n : nb + 32;
+      have_next = !stop && nb < n && (long long)(wm >> 1) >= nneed;
+      if (have_next) dnext = load_desc(nb, nneed);  // in flight while this chunk runs
+    }
     // the oldest pending chunk must be final before its slot is reused
     resolve(std::integral_constant<int, L>{}, chunk - 1, vpre, vhave);
 #pragma unroll
@@ -1931,7 +2028,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     exec(cur, live, 0u, gb, rb);
     RB[0] = rb;
     publish(chunk, gb);
-    if (lane == 0) wm = ld_relaxed_u64(&a.out->validated);  // for the next chunk
+    if (lane == 0) wm = ld_relaxed_u64(&a.out->dvalid);  // for the next chunk
   }
   // drain: every pending chunk final, oldest first
   if (!timed_out) {
@@ -1973,7 +2070,10 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   // CTA 0 is the control warp alone: no data warp competes with it for its
   // SM sub-partition's issue slot (the scheduler favours higher warp ids).
   if (blockIdx.x == 0) {
-    if (threadIdx.x >= 32) return;
+    if (threadIdx.x >= 32) {
+      if (a.mode == 1 && threadIdx.x < 64) emit_warp_replay(a);  // beside the gate warp
+      return;
+    }
     if (a.mode == 1) {
       if constexpr (CTL == 2 || CTL == 4 || CTL == 8) gate_warp_replay<CTL>(a, &s.gate);
       else gate_warp_replay<0>(a, &s.gate);
@@ -2004,7 +2104,10 @@ __global__ void __launch_bounds__(NT, 1) k_replay_nt(SimArgs a) {
   for (int i = threadIdx.x; i < kRing; i += blockDim.x) s_ring[i] = 0;
   __syncthreads();
   if (blockIdx.x == 0) {
-    if (threadIdx.x >= 32) return;
+    if (threadIdx.x >= 32) {
+      if (threadIdx.x < 64) emit_warp_replay(a);  // beside the gate warp
+      return;
+    }
     gate_warp_replay<CTL>(a, &sg);
     return;
   }
@@ -2372,6 +2475,20 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   cap = b.dec_cap;
   if ((rc = grow(h, &b.decisions, &cap, (size_t)n + 1))) return rc;
   b.dec_cap = cap;
+  long long n_data = 0;  // pulls + applies: the most descriptors the gate can publish
+  for (int64_t i = 0; i < n; ++i) n_data += (calls[i].kind == PS_CALL_PULL || calls[i].kind == PS_CALL_APPLY);
+  cap = b.dstream_cap;
+  // + the emitter's per-chunk prefix counts (8 B) and masks (4 B)
+  if ((rc = grow(h, &b.dstream, &cap, (size_t)n_data + 32 + 2 * ((size_t)n / 32 + 3)))) return rc;
+  if (cap != b.dstream_cap) {  // fresh words: no tag of any run
+    PS_CK(h, cudaMemsetAsync(b.dstream, 0, cap * sizeof(unsigned long long), h->stream));
+    b.dtag = 0;
+  }
+  b.dstream_cap = cap;
+  if (++b.dtag == 0) {  // 32-bit tag space wrapped: clear stale words once
+    PS_CK(h, cudaMemsetAsync(b.dstream, 0, cap * sizeof(unsigned long long), h->stream));
+    b.dtag = 1;
+  }
   if (n) PS_CK(h, cudaMemcpyAsync(b.calls, calls, (size_t)n * sizeof(ReplayCall), cudaMemcpyHostToDevice,
                                   h->stream));
   PS_CK(h, cudaMemsetAsync(b.gcount, 0, slots * sizeof(unsigned), h->stream));
@@ -2400,6 +2517,9 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   a.n_ctas = (unsigned)(grid - 1);
   a.calls = (const ReplayCall*)b.calls;
   a.n_calls = n;
+  a.dstream = b.dstream;
+  a.n_data = n_data;
+  a.tag = b.dtag;  // the descriptor words of this run
   a.decisions = b.decisions;
   a.ctrl = h->ctrl;
   a.out = (SimOut*)b.out;

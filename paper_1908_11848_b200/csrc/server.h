@@ -20,7 +20,9 @@ struct ps_sim_buffers {
   void* out = nullptr;                 // SimOut
   void* calls = nullptr;               // replay: ps_replay_call[calls_cap]
   long long* decisions = nullptr;      // replay: one word per decide
-  size_t calls_cap = 0, dec_cap = 0;
+  unsigned long long* dstream = nullptr;  // replay: the gate's data-call descriptors (tagged)
+  unsigned dtag = 0;                   // replay: run tag of the descriptor words
+  size_t calls_cap = 0, dec_cap = 0, dstream_cap = 0;
   int64_t last_decisions = 0;
   int64_t last_trace_rows = 0, last_loss_samples = 0, last_loss_every = 0, last_base_version = 0;
 };
