@@ -1820,16 +1820,17 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
     // (also for -0, inf and NaN), so its apply is an exact identity; its
     // result is not checked.
     const unsigned mapp = c.ma & ~rej;
-    while (calls) {
+    // the descriptor stream holds only data calls, in order: slot s is lane s
+    const int ncalls = 32 - __clz(calls);
+    for (int s0 = 0; s0 < ncalls; s0 += KG) {
       unsigned bitk[KG];
       float4 g[KG][V];
       unsigned offk[KG];
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
-        const int i = __ffs(calls) - 1;  // -1 once the chunk is exhausted
-        calls &= calls - 1;
-        bitk[k] = i >= 0 ? (1u << i) : 0u;
-        offk[k] = __shfl_sync(kFull, c.off, i & 31);
+        const int i = s0 + k;  // <= 31: s0 < ncalls <= 32 and KG divides 32
+        bitk[k] = calls & (1u << i);
+        offk[k] = __shfl_sync(kFull, c.off, i);
         const bool ld = (mapp & bitk[k]) != 0u;
 #pragma unroll
         for (int u = 0; u < V; ++u) g[k][u] = ld_keep_if(ld && 32 * u < span, sbase + offk[k] + 32 * u);
