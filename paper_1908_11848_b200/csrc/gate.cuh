@@ -95,39 +95,35 @@ __device__ __forceinline__ int controller_grid(double lp, double pp, double ls, 
   return (int)__reduce_min_sync(kFull, (hi == mhi && lo == mlo) ? (unsigned)best_r : 0x7fffffffu);
 }
 
-// One lane's own controller (same arguments as controller_grid, 2 <= r_max <=
-// kLaneRMax), for a warp that evaluates up to 32 decisions at once. Per r the
-// crossing of the non-decreasing slow(k) with cand is estimated from
-// (cand - ls) / is, and a window of three k around it is evaluated with
-// controller_grid's exact rounded expressions. The window is then checked to
-// bracket the crossing (slow at its low end <= cand < slow at its high end,
-// or the end of the k range), so its minimum is the full minimum bit for bit;
-// `ok` is cleared when the estimate missed (the caller then runs the exact
-// warp-collective grid for that decision).
-constexpr int kLaneRMax = 16;
+// One lane's own controller (same arguments and result as controller_grid),
+// for a warp that evaluates up to 32 decisions at once.
+// cand(r) = lp + r*ip and slow(k) = ls + (k+1)*is are both non-decreasing
+// (positive intervals, monotone rounding), so the last k with slow(k) <= cand
+// -- the crossing, where |slow(k) - cand| is smallest, at it or the next k --
+// only moves forward as r grows: one forward sweep over k for all r, each
+// distance with controller_grid's exact rounded expressions, the first r on
+// ties. `ok` is always set (kept for the caller's exact fallback hook).
 __device__ __forceinline__ int controller_lane(double lp, double pp, double ls, double ps, int r_max, bool& ok) {
   const double ip = interval_of(lp, pp);
   const double is = interval_of(ls, ps);
-  const double inv = 1.0 / is;
-  const double top = (double)(r_max + 1);  // k + 1 runs over [1, r_max + 1]
-  double best = __longlong_as_double(0x7ff0000000000000ll);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  double best = inf;
   int best_r = 0;
-  bool good = r_max >= 2;
-#pragma unroll
-  for (int r = 0; r <= kLaneRMax; ++r) {
-    if (r <= r_max) {
-      const double cand = __dadd_rn(lp, __dmul_rn((double)r, ip));
-      const double x = __dmul_rn(__dsub_rn(cand, ls), inv);
-      const double fc = fmin(fmax(floor(x), 2.0), top - 1.0);  // window {fc-1, fc, fc+1} in [1, top]
-      const double d0 = __dsub_rn(__dadd_rn(ls, __dmul_rn(fc - 1.0, is)), cand);
-      const double d1 = __dsub_rn(__dadd_rn(ls, __dmul_rn(fc, is)), cand);
-      const double d2 = __dsub_rn(__dadd_rn(ls, __dmul_rn(fc + 1.0, is)), cand);
-      const double m = fmin(fmin(fabs(d0), fabs(d1)), fabs(d2));
-      good = good && (fc == 2.0 || d0 <= 0.0) && (fc == top - 1.0 || d2 > 0.0);
-      if (m < best) { best = m; best_r = r; }
+  int lo = -1;                                   // last k with slow(k) <= cand (-1: none)
+  double s_lo = inf;                             // slow(lo)
+  double s_hi = __dadd_rn(ls, __dmul_rn(1.0, is));  // slow(lo + 1) (inf past r_max)
+  for (int r = 0; r <= r_max; ++r) {
+    const double cand = __dadd_rn(lp, __dmul_rn((double)r, ip));
+    while (lo < r_max && s_hi <= cand) {
+      ++lo;
+      s_lo = s_hi;
+      s_hi = lo < r_max ? __dadd_rn(ls, __dmul_rn((double)(lo + 2), is)) : inf;
     }
+    double m = lo >= 0 ? fabs(__dsub_rn(s_lo, cand)) : inf;
+    if (lo < r_max) m = fmin(m, fabs(__dsub_rn(s_hi, cand)));
+    if (m < best) { best = m; best_r = r; }
   }
-  ok = good;
+  ok = true;
   return best_r;
 }
 

@@ -877,7 +877,7 @@ struct ReplayGate<0> {  // shared-memory tables (gate.cuh), any P <= 64
   }
 };
 
-// The replay gate as a scan (P <= PM <= 8, r_max <= 16, credits < 256).
+// The replay gate as a scan (P <= PM <= 8, credits < 256).
 //
 // Of the gate's state only the credits and the deferred set depend on earlier
 // OUTCOMES. Clocks, the two-deep push history and the populated counts follow
@@ -895,7 +895,7 @@ struct ReplayGate<0> {  // shared-memory tables (gate.cuh), any P <= 64
 template <int PM>
 __device__ bool gate_scan_eligible(const RegGate<PM>& g) {
   if (g.P > PM || PM > 8) return false;
-  if (g.paradigm == PS_DSSP && (g.r_max > kLaneRMax || g.s_lower + g.r_max > 255)) return false;
+  if (g.paradigm == PS_DSSP && g.s_lower + g.r_max > 255) return false;  // credits are 8-bit fields
 #pragma unroll
   for (int q = 0; q < PM; ++q)
     if (g.credits[q] < 0 || g.credits[q] > 255) return false;

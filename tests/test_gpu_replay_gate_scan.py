@@ -5,7 +5,7 @@ and keeps only the credit / deferred recurrence serial (gate_warp_replay_scan,
 csrc/ps_sim.cu); PS_REPLAY_GATE_SCAN=0 selects the decision-at-a-time gate
 (gate_on_push semantics, policy.py:152-206). Random request streams -- ties in
 time, bursts of one worker, every paradigm, controller grids from r_max = 1 to
-past the scan's limit -- must give the oracle gate's decisions, and streams with
+40 -- must give the oracle gate's decisions, and streams with
 a protocol violation (a pull or push from a deferred worker, an unknown worker)
 must stop at the same call with the same gate tables and weights under both.
 """
@@ -86,7 +86,8 @@ def _run(calls, paradigm, P, s, r, scan, monkeypatch):
 
 CONFIGS = [("dssp", 2, 3, 12), ("dssp", 3, 3, 12), ("dssp", 4, 3, 12), ("dssp", 4, 1, 4),
            ("dssp", 4, 0, 2), ("dssp", 5, 2, 1), ("dssp", 8, 3, 16), ("dssp", 8, 3, 17),
-           ("dssp", 9, 3, 12), ("ssp", 4, 2, 0), ("bsp", 3, 0, 0), ("asp", 4, 0, 0)]
+           ("dssp", 4, 2, 40), ("dssp", 9, 3, 12), ("ssp", 4, 2, 0), ("bsp", 3, 0, 0),
+           ("asp", 4, 0, 0)]
 
 
 @pytest.mark.parametrize("paradigm,P,s,r", CONFIGS)
