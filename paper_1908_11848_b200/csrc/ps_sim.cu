@@ -926,6 +926,12 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
   };
   ReplayCall c, nx;
   load(0, c);
+#ifdef PS_SIM_PROFILE
+  long long pc_pre = 0, pc_dssp = 0, pc_ctl = 0, pc_scan = 0, pc_tail = 0, pc_t = clock64();
+#define SCAN_STAMP(acc) do { const long long t_ = clock64(); acc += t_ - pc_t; pc_t = t_; } while (0)
+#else
+#define SCAN_STAMP(acc) do {} while (0)
+#endif
   for (long long base = 0; base < n; base += 32) {
     load(base + 32, nx);
     const int m = n - base < 32 ? (int)(n - base) : 32;
@@ -960,6 +966,7 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
       for (int q = 0; q < PM; ++q)
         if (q < P && cnt[q] - low <= g.threshold) ready |= 1u << q;
     }
+    SCAN_STAMP(pc_pre);
     int cls = gap <= g.threshold ? 0 : 1;  // SSP / BSP: grant or defer
     int mint = 0;
     if (asp) cls = 0;
@@ -982,19 +989,13 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
       const bool need = is_dec && cls == 2 && g.r_max > 0 && pop_p >= 2 && pop_sl >= 2;
       int pred = 0;
       const unsigned needm = __ballot_sync(kFull, need);
-      if (needm) {
+      SCAN_STAMP(pc_dssp);
+      if (needm) {  // one lane per decision, one forward sweep of its grid
         bool ok = true;
         pred = controller_lane(c.now, pp, ls, ps, g.r_max, ok);
-        unsigned miss = __ballot_sync(kFull, need && !ok);
-        while (miss) {  // the estimate missed: the exact warp-collective grid
-          const int j = __ffs(miss) - 1;
-          miss &= miss - 1;
-          const int pj = controller_grid(__shfl_sync(kFull, c.now, j), __shfl_sync(kFull, pp, j),
-                                         __shfl_sync(kFull, ls, j), __shfl_sync(kFull, ps, j), g.r_max);
-          if (lane == j) pred = pj;
-        }
         if (!need) pred = 0;
       }
+      SCAN_STAMP(pc_ctl);
       int headroom = g.s_lower + g.r_max - gap;
       headroom = headroom < 0 ? 0 : headroom;
       mint = pred < headroom ? pred : headroom;
@@ -1051,6 +1052,7 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
       defm = def0;
       scan(ndone);
     }
+    SCAN_STAMP(pc_scan);
     const unsigned fdl = __ballot_sync(kFull, is_dec && myslot == failslot);
     const unsigned fail_dec = fdl ? (unsigned)(__ffs(fdl) - 1) : 32u;
     // ---- pulls: none from a deferred worker (the set after the last decision before it) ----
@@ -1109,7 +1111,14 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
     valid = base + m;
     if (lane == 0 && valid < n) st_relaxed_u64(&a.out->validated, (unsigned long long)valid << 1);
     c = nx;
+    SCAN_STAMP(pc_tail);
   }
+#ifdef PS_SIM_PROFILE
+  if (lane == 0)
+    printf("[scan-gate] calls %lld: pre %lld dssp %lld controller %lld recurrence %lld tail %lld cycles\n", n, pc_pre,
+           pc_dssp, pc_ctl, pc_scan, pc_tail);
+#endif
+#undef SCAN_STAMP
   if (lane == 0) st_relaxed_u64(&a.out->validated, ((unsigned long long)valid << 1) | 1ull);
 #pragma unroll
   for (int q = 0; q < PM; ++q) g.credits[q] = (int)((cw >> (8 * q)) & (CW)0xffu);
