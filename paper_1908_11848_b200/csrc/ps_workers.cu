@@ -40,6 +40,7 @@
 // stays blocked, and later kernels only advance the ticket.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -114,7 +115,17 @@ struct WArgs {
   unsigned long long timeout_ns;
   unsigned* my_go;                // this worker's go flag (local to the launching GPU)
   int sys;                        // 1: the cluster spans GPUs (system-scope hand-off)
+  long long clk_off;              // server GPU %globaltimer - this GPU's (ns), calibrated at bind
 };
+
+// The gate's clock: seconds since ps_workers_start on the SERVER GPU's
+// %globaltimer. A worker on a peer GPU reads its own timer, shifted by the
+// offset calibrated when it was bound (the GPUs' timers are not one clock:
+// controller intervals mix every worker's timestamps, runner.py:234).
+__device__ __forceinline__ double gate_now(const WCtl* c, long long clk_off) {
+  const long long t = (long long)globaltimer_ns() + clk_off - (long long)c->t0;
+  return (double)t * 1e-9 * c->time_scale;
+}
 
 __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p, int sys) {
   return sys ? ld_acquire_sys_u64(p) : ld_acquire_u64(p);
@@ -296,7 +307,7 @@ __global__ void __launch_bounds__(kWThreads) k_wpush(WArgs a) {
   __syncwarp();
   // runner.py:234: the decision's timestamp is taken at decision time
   double now = 0.0;
-  if (lane == 0) now = (double)(globaltimer_ns() - c->t0) * 1e-9 * c->time_scale;
+  if (lane == 0) now = gate_now(c, a.clk_off);
   now = __shfl_sync(kFull, now, 0);
   const GateResult r = gate_on_push(&sg, a.worker, now);
   __syncwarp();
@@ -369,7 +380,7 @@ __global__ void __launch_bounds__(kWThreads) k_wpull(WArgs a) {
     if (k < a.pull_cap) {
       WPull e;
       e.ticket = t;
-      e.now = (double)(globaltimer_ns() - c->t0) * 1e-9 * c->time_scale;
+      e.now = gate_now(c, a.clk_off);
       e.worker = a.worker; e._pad = 0;
       e.version = a.ctrl->gate.version;
       a.pull[k] = e;
@@ -424,6 +435,7 @@ struct ps_worker_rt {
     long long record_cap = 0;
     unsigned* go = nullptr;       // the worker's go flag, in its own GPU's memory
     int ctas = 0;
+    long long clk_off = 0;        // server GPU clock - worker GPU clock (ns)
   } bind[PS_MAX_WORKERS];
 };
 
@@ -470,6 +482,7 @@ WArgs make_args(ps_server* h, int worker) {
   a.timeout_ns = 60ull * 1000 * 1000 * 1000;
   a.my_go = rt->bind[worker].go;
   a.sys = rt->sys;
+  a.clk_off = rt->bind[worker].clk_off;
   return a;
 }
 
@@ -528,6 +541,36 @@ int ps_workers_start(ps_server* h, int64_t log_cap, double time_scale) {
   return reset_run(h);
 }
 
+__global__ void k_read_timer(unsigned long long* out) { *out = globaltimer_ns(); }
+
+// (this GPU's %globaltimer - the host's steady clock) in ns, from the sample
+// with the shortest host round trip: the GPU read lies within it, so the
+// error is at most half of it (a few us).
+static int gpu_minus_host_ns(ps_server* h, int dev, long long* out) {
+  DevGuardW g(dev);
+  unsigned long long* d = nullptr;
+  PS_CK(h, cudaMalloc(&d, sizeof(unsigned long long)));
+  long long best_rtt = -1, best = 0;
+  int rc = PS_OK;
+  for (int i = 0; i < 9 && rc == PS_OK; ++i) {
+    unsigned long long v = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    k_read_timer<<<1, 1>>>(d);
+    if (cudaMemcpy(&v, d, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) { rc = PS_E_CUDA; break; }
+    const auto t1 = std::chrono::steady_clock::now();
+    const long long a = std::chrono::duration_cast<std::chrono::nanoseconds>(t0.time_since_epoch()).count();
+    const long long b = std::chrono::duration_cast<std::chrono::nanoseconds>(t1.time_since_epoch()).count();
+    if (i > 0 && (best_rtt < 0 || b - a < best_rtt)) {  // sample 0 warms the launch path
+      best_rtt = b - a;
+      best = (long long)v - (a + (b - a) / 2);
+    }
+  }
+  cudaFree(d);
+  if (rc) return ps_fail(h, rc, "clock calibration failed");
+  *out = best;
+  return PS_OK;
+}
+
 int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const float* grad,
                           float* params) {
   if (!h->wrt) return ps_fail(h, PS_E_VALUE, "call ps_workers_start first");
@@ -584,6 +627,15 @@ int ps_bind_worker_stream(ps_server* h, int32_t worker, void* cuda_stream, const
     want = want < lo_c ? lo_c : want > hi_c ? hi_c : want;
     const char* v = getenv("PS_WORKERS_CTAS");
     b.ctas = v && atoi(v) > 0 ? atoi(v) : (int)want;
+  }
+  // a worker on a peer GPU stamps its decisions with the server GPU's clock
+  b.clk_off = 0;
+  if (wdev != h->dev) {
+    long long ws = 0, ss = 0;
+    int rc = gpu_minus_host_ns(h, h->dev, &ss);
+    if (!rc) rc = gpu_minus_host_ns(h, wdev, &ws);
+    if (rc) return rc;
+    b.clk_off = ss - ws;
   }
   b.dev = wdev;
   b.stream = (cudaStream_t)cuda_stream;

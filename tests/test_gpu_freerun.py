@@ -127,6 +127,13 @@ def test_free_running_workers_on_peer_gpus(paradigm, s, r):
     rep = cl.run(iters)
     assert rep.pushes == P * iters
     _check_gate(rep, paradigm, P, s, r)
+    # one clock for the whole cluster: the decisions are taken in ticket
+    # order, so their timestamps -- read on whichever GPU ran the push,
+    # shifted onto the server GPU's clock -- never go back by more than the
+    # calibration error, and all of them lie inside the run
+    now = rep.decisions["now"]
+    assert np.all(np.diff(now) > -50e-6), np.diff(now).min()
+    assert 0 <= now.min() and now.max() <= rep.wall_s + 0.05, (now.min(), now.max(), rep.wall_s)
     w, snaps = _replay(rep, rings, d, oracle.initial_weights_f64(0, d).astype(np.float32), 0.05)
     assert np.array_equal(eng.read()[0].view(np.uint32), w.view(np.uint32))
     for p in range(P):
