@@ -1015,7 +1015,7 @@ void ps_destroy(ps_server* h) {
   cudaFree(s.ops); cudaFree(s.gcount);
   cudaFree(s.rep); cudaFree(s.gbuf); cudaFree(s.center); cudaFree(s.ctime);
   cudaFree(s.trace); cudaFree(s.losses); cudaFree(s.out);
-  cudaFree(s.calls); cudaFree(s.decisions); cudaFree(s.dstream);
+  cudaFree(s.calls); cudaFree(s.decisions); cudaFree(s.dstream); cudaFree(s.pred);
   ps_workers_free(h);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);

@@ -125,6 +125,8 @@ struct SimArgs {
   int gate_scan;              // replay: the scan gate when eligible (PS_REPLAY_GATE_SCAN, default on)
   unsigned long long* dstream;  // replay: the gate's data-call descriptors (DataEmit)
   long long n_data;           // replay: pulls + applies in the stream (upper bound of dstream)
+  unsigned long long* pred;    // replay: controller results by call (predict_warp_replay)
+  int pred_ahead;             // replay: the gate reads them (PS_REPLAY_CTL_AHEAD, default on)
 };
 
 // The replay's data calls as a descriptor stream. A second warp of CTA 0 --
@@ -902,7 +904,7 @@ __device__ bool gate_scan_eligible(const RegGate<PM>& g) {
   return true;
 }
 
-template <int PM>
+template <int PM, bool PREDICT = false>
 __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
   // credits, 8 bits per worker: one 32-bit word up to 4 workers
   using CW = typename std::conditional<(PM <= 4), unsigned, unsigned long long>::type;
@@ -914,7 +916,10 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
   long long n_dec = 0, pushes = 0, valid = 0;
   int status = PS_OK;
   const long long n = a.n_calls;
-  if (lane == 0) a.out->t_start = globaltimer_ns();
+  if (!PREDICT && lane == 0) a.out->t_start = globaltimer_ns();
+  // PREDICT: this warp is the controller-ahead helper (see predict_warp_replay)
+  const bool ahead = !PREDICT && a.pred_ahead && dssp;
+  const unsigned long long t_pred = globaltimer_ns();
   CW cw = 0;
 #pragma unroll
   for (int q = 0; q < PM; ++q) cw |= (CW)(q < P ? g.credits[q] : 0) << (8 * q);
@@ -934,6 +939,9 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
 #endif
   for (long long base = 0; base < n; base += 32) {
     load(base + 32, nx);
+    // the helper's controller results for this chunk, in flight meanwhile
+    unsigned long long pv = 0;
+    if (ahead) pv = base + lane < n ? ld_relaxed_u64(a.pred + base + lane) : 0ull;
     const int m = n - base < 32 ? (int)(n - base) : 32;
     const unsigned live = m >= 32 ? kFull : ((1u << m) - 1u);
     const unsigned badw = __ballot_sync(kFull, lane < m && (c.worker < 0 || c.worker >= P));
@@ -990,15 +998,46 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
       int pred = 0;
       const unsigned needm = __ballot_sync(kFull, need);
       SCAN_STAMP(pc_dssp);
-      if (needm) {  // one lane per decision, one forward sweep of its grid
+      if (needm && ahead) {  // computed by the helper warp, tagged with this run
+        while (__any_sync(kFull, need && (unsigned)(pv >> 32) != a.tag)) {
+          if (need && (unsigned)(pv >> 32) != a.tag) pv = ld_relaxed_u64(a.pred + base + lane);
+          if (globaltimer_ns() - t_pred > a.timeout_ns) break;
+        }
+        pred = need ? (int)(unsigned)pv : 0;
+      } else if (needm) {  // one lane per decision, one forward sweep of its grid
         bool ok = true;
         pred = controller_lane(c.now, pp, ls, ps, g.r_max, ok);
         if (!need) pred = 0;
+        if constexpr (PREDICT) {
+          if (need) st_relaxed_u64(a.pred + base + lane, ((unsigned long long)a.tag << 32) | (unsigned)pred);
+        }
       }
       SCAN_STAMP(pc_ctl);
       int headroom = g.s_lower + g.r_max - gap;
       headroom = headroom < 0 ? 0 : headroom;
       mint = pred < headroom ? pred : headroom;
+    }
+    if constexpr (PREDICT) {
+      // the helper only moves the tables on (every decide of the valid
+      // prefix counts: the gate stops at the first protocol error anyway)
+#pragma unroll
+      for (int q = 0; q < PM; ++q) {
+        const unsigned mqa = mq[q];
+        const int k = __popc(mqa);
+        const int l1 = mqa ? 31 - __clz(mqa) : 0;
+        const unsigned rest = mqa & ~(1u << l1);
+        const double t1 = __shfl_sync(kFull, c.now, l1);
+        const double t2 = __shfl_sync(kFull, c.now, rest ? 31 - __clz(rest) : 0);
+        if (k) {
+          g.previous[q] = k >= 2 ? t2 : g.latest[q];
+          g.latest[q] = t1;
+          g.clocks[q] += k;
+          g.populated[q] += k;
+        }
+      }
+      if (limit < m) break;
+      c = nx;
+      continue;
     }
     // the outcome and the credits a decision leaves when the worker holds no
     // credit are fixed by now: pack worker | outcome | credits | ready set
@@ -1119,6 +1158,7 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
            pc_dssp, pc_ctl, pc_scan, pc_tail);
 #endif
 #undef SCAN_STAMP
+  if constexpr (PREDICT) return;
   if (lane == 0) st_relaxed_u64(&a.out->validated, ((unsigned long long)valid << 1) | 1ull);
 #pragma unroll
   for (int q = 0; q < PM; ++q) g.credits[q] = (int)((cw >> (8 * q)) & (CW)0xffu);
@@ -1132,6 +1172,20 @@ __device__ void gate_warp_replay_scan(const SimArgs& a, RegGate<PM>& g) {
     a.out->unfinished = 0ull;
     if (status != PS_OK) atomicCAS(&a.out->status, PS_OK, status);
   }
+}
+
+// The controller-ahead helper (CTA 0, warp 2): the DSSP controller grids of a
+// replay depend only on the push sequence (policy.py:108-132 reads the
+// push history, never an outcome), so this warp runs the scan gate's
+// per-chunk evaluation ahead of the gate warp and publishes every grid's
+// result, tagged with the run, for the gate to read instead of computing it.
+template <int PM>
+__device__ void predict_warp_replay(const SimArgs& a) {
+  if (!a.pred_ahead || !a.gate_scan) return;
+  RegGate<PM> rg;
+  rg.load(a.ctrl->gate, a.reset_gate != 0);
+  if (rg.paradigm != PS_DSSP || !gate_scan_eligible<PM>(rg)) return;
+  gate_warp_replay_scan<PM, true>(a, rg);
 }
 
 // The gate warp of a replay: decides every DECIDE in order and validates the
@@ -2082,6 +2136,8 @@ __global__ void __launch_bounds__(kSimThreads) k_sim(SimArgs a) {
   if (blockIdx.x == 0) {
     if (threadIdx.x >= 32) {
       if (a.mode == 1 && threadIdx.x < 64) emit_warp_replay(a);  // beside the gate warp
+      if constexpr (CTL == 2 || CTL == 4 || CTL == 8)
+        if (a.mode == 1 && threadIdx.x >= 64 && threadIdx.x < 96) predict_warp_replay<CTL>(a);
       return;
     }
     if (a.mode == 1) {
@@ -2116,6 +2172,7 @@ __global__ void __launch_bounds__(NT, 1) k_replay_nt(SimArgs a) {
   if (blockIdx.x == 0) {
     if (threadIdx.x >= 32) {
       if (threadIdx.x < 64) emit_warp_replay(a);  // beside the gate warp
+      else if (threadIdx.x < 96) predict_warp_replay<CTL>(a);
       return;
     }
     gate_warp_replay<CTL>(a, &sg);
@@ -2495,8 +2552,13 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
     b.dtag = 0;
   }
   b.dstream_cap = cap;
+  cap = b.pred_cap;
+  if ((rc = grow(h, &b.pred, &cap, (size_t)n + 32))) return rc;
+  if (cap != b.pred_cap) PS_CK(h, cudaMemsetAsync(b.pred, 0, cap * sizeof(unsigned long long), h->stream));
+  b.pred_cap = cap;
   if (++b.dtag == 0) {  // 32-bit tag space wrapped: clear stale words once
-    PS_CK(h, cudaMemsetAsync(b.dstream, 0, cap * sizeof(unsigned long long), h->stream));
+    PS_CK(h, cudaMemsetAsync(b.dstream, 0, b.dstream_cap * sizeof(unsigned long long), h->stream));
+    PS_CK(h, cudaMemsetAsync(b.pred, 0, b.pred_cap * sizeof(unsigned long long), h->stream));
     b.dtag = 1;
   }
   if (n) PS_CK(h, cudaMemcpyAsync(b.calls, calls, (size_t)n * sizeof(ReplayCall), cudaMemcpyHostToDevice,
@@ -2529,6 +2591,11 @@ int ps_replay_run(ps_server* h, const ps_replay_call* calls, int64_t n, const fl
   a.n_calls = n;
   a.dstream = b.dstream;
   a.n_data = n_data;
+  a.pred = b.pred;
+  {
+    const char* v = getenv("PS_REPLAY_CTL_AHEAD");
+    a.pred_ahead = v ? atoi(v) != 0 : 1;
+  }
   a.tag = b.dtag;  // the descriptor words of this run
   a.decisions = b.decisions;
   a.ctrl = h->ctrl;

@@ -22,6 +22,8 @@ struct ps_sim_buffers {
   long long* decisions = nullptr;      // replay: one word per decide
   unsigned long long* dstream = nullptr;  // replay: the gate's data-call descriptors (tagged)
   unsigned dtag = 0;                   // replay: run tag of the descriptor words
+  unsigned long long* pred = nullptr;  // replay: controller results by call (tagged)
+  size_t pred_cap = 0;
   size_t calls_cap = 0, dec_cap = 0, dstream_cap = 0;
   int64_t last_decisions = 0;
   int64_t last_trace_rows = 0, last_loss_samples = 0, last_loss_every = 0, last_base_version = 0;
