@@ -1810,7 +1810,10 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
 #define PS_REPLAY_KG2 8
 #endif
   constexpr int KG = V == 1 ? 16 : V == 2 ? PS_REPLAY_KG2 : KG4;  // calls per group
-  constexpr int L = V <= 2 ? 3 : 2;  // chunks executed before their verdict is read
+#ifndef PS_REPLAY_LAG
+#define PS_REPLAY_LAG 3
+#endif
+  constexpr int L = V <= 2 ? PS_REPLAY_LAG : 2;  // chunks executed before their verdict is read
   constexpr int kRingChunks = kRing / 2;
   unsigned long long* s_ring = reinterpret_cast<unsigned long long*>(s_ring32);
   unsigned long long* gchunk = reinterpret_cast<unsigned long long*>(a.gword);
@@ -2097,6 +2100,7 @@ __device__ void data_warp_replay_spec(const SimArgs& a, unsigned dw, unsigned* s
   // drain: every pending chunk final, oldest first
   if (!timed_out) {
     const long long newest = chunk - 1;
+    if constexpr (L >= 4) resolve(std::integral_constant<int, (L >= 4 ? 4 : 0)>{}, newest);
     if constexpr (L >= 3) resolve(std::integral_constant<int, (L >= 3 ? 3 : 0)>{}, newest);
     resolve(std::integral_constant<int, 2>{}, newest);
     resolve(std::integral_constant<int, 1>{}, newest);
